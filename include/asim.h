@@ -1,0 +1,261 @@
+/* asim.h -- C ABI of libasim.so: the batched SLO-attainment simulator that
+ * AlpaServe's placement search calls for every candidate placement
+ * (arXiv 2302.11665; PAPER.md cited as P:<line>).
+ *
+ * What it computes.  Given
+ *   - a set of models with per-(model, parallel config) stage latencies and
+ *     per-device memory ("parallelize(m, g, p)", Alg. 1; §4.1
+ *     P:670-684),
+ *   - a device cluster (device count, per-device memory budget),
+ *   - a time-sorted request trace W with per-model SLOs ("we assume we know
+ *     the arrival process in advance"; "SLO Scale"), and
+ *   - a batch of candidate placements ("a specific cluster group partition,
+ *     model selection, and parallel configuration"),
+ * it returns for every candidate the number of requests that finish within
+ * their SLO ("SLO attainment") plus the sum of their latencies, and the
+ * argmax candidate ("pick_highest_SLO_attainment", Alg. 1).
+ *
+ * Runtime semantics (§4.3; readings C1-C13):
+ *   - each group is a tandem of s FCFS single-server stages with unbounded
+ *     buffers; a request of model m on a group with config p occupies stage k
+ *     for stage_ns[m][p][k]; tail_ns[m][p] is added to its finish time only;
+ *   - each request goes to the hosting group with the earliest predicted
+ *     finish, ties to the lowest group index ("the group with the shortest
+ *     queue length", P:791 -- reading C1);
+ *   - the group rejects it at receipt if finish - arrival > slo_ns[m]
+ *     ("rejects the request if it cannot", P:792 -- readings C2, C3);
+ *   - equal timestamps are taken in trace order; all stages idle at t = 0.
+ * Everything is int64 nanoseconds and integer counts: results are exact and
+ * deterministic (bit-identical to the CPU oracle in oracle/).
+ *
+ * Conventions.
+ *   - Every call returns asim_status: 0 = OK, < 0 = error; the message is in
+ *     asim_last_error(ctx).  No call throws or aborts across the ABI.  Input
+ *     errors are detected on the host before anything is launched.  After
+ *     ASIM_ECUDA the context is unusable (destroy it).
+ *   - ptr_kind says whether bulk arrays are host (ASIM_HOST) or device
+ *     (ASIM_DEVICE, allocated on the context's device) pointers.  Device
+ *     inputs/outputs are stream-ordered on `cuda_stream` (a cudaStream_t;
+ *     NULL = legacy default stream); host outputs are complete on return.
+ *   - Problem and trace arrays are COPIED into context-owned device memory;
+ *     candidate and result arrays are BORROWED for the duration of the call.
+ *   - One context per (thread, device); a context is not thread-safe.
+ */
+#ifndef ASIM_H
+#define ASIM_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASIM_ABI_VERSION 1
+#define ASIM_MAX_GROUPS 64   /* host_mask is a uint64 bit set over groups      */
+#define ASIM_MAX_STAGES 64   /* per config                                      */
+#define ASIM_MAX_SLOTS 128   /* sum of stages over the groups of one placement  */
+#define ASIM_MAX_MODELS 65535
+
+typedef int32_t asim_status;
+enum {
+  ASIM_OK = 0,
+  ASIM_EINVAL = -1,    /* null required pointer, bad size or enum            */
+  ASIM_EUNSORTED = -2, /* trace not non-decreasing, or a negative arrival    */
+  ASIM_ERANGE = -3,    /* id / count out of range, or an int64 overflow bound */
+  ASIM_ENOMEM = -4,    /* device or host allocation failed                   */
+  ASIM_ECUDA = -5,     /* CUDA runtime error (context now unusable)          */
+  ASIM_ESTATE = -6     /* call order: e.g. evaluate before set_problem/trace */
+};
+enum { ASIM_HOST = 0, ASIM_DEVICE = 1 };
+
+typedef struct asim_ctx asim_ctx;       /* opaque */
+typedef struct asim_search asim_search; /* opaque */
+
+int32_t asim_abi_version(void);
+
+/* Create a context on CUDA device `cuda_device` (sm_100a required).
+ * *out receives the context; on error *out is NULL. */
+asim_status asim_create(int32_t cuda_device, asim_ctx** out);
+/* Free the context and every device buffer it owns.  NULL is a no-op. */
+void asim_destroy(asim_ctx* ctx);
+/* Message of the last failed call on ctx; owned by ctx, valid until its next
+ * call.  NULL ctx -> message of the last failed asim_create on this thread. */
+const char* asim_last_error(const asim_ctx* ctx);
+/* Number of kernels this context has launched so far (for the benchmark's
+ * gpu_launches count). */
+int64_t asim_launch_count(const asim_ctx* ctx);
+
+/* Kernel statistics for the benchmark's roofline (asim_set_profiling(ctx, 1)
+ * records CUDA events around every simulation launch on its stream).
+ *   sim_launches / sim_ms  simulation-kernel launches and their summed
+ *                          device time (ms, CUDA events)
+ *   stage_updates          algorithmic work: one max-plus update of one
+ *                          pipeline stage of one hosting group, per request
+ *                          and candidate
+ *   request_evals          (request, candidate) pairs simulated
+ * asim_get_stats synchronises the recorded events. */
+typedef struct {
+  int64_t launches;
+  int64_t sim_launches;
+  double sim_ms;
+  int64_t stage_updates;
+  int64_t request_evals;
+} asim_stats;
+asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
+asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);
+asim_status asim_reset_stats(asim_ctx* ctx);
+
+/* ---------------------------------------------------------------- problem */
+/* "a set of models" + "a cluster resource specification".  All
+ * arrays are host pointers, row-major, and are copied.
+ *   num_models M in [1, ASIM_MAX_MODELS]; num_configs P >= 1;
+ *   max_stages S in [1, ASIM_MAX_STAGES]
+ *   slo_ns[M]         >= 0; INT64_MAX = no deadline
+ *   cfg_stages[P]     s_p in [1, S]  (inter-op degree, §4.1)
+ *   cfg_devices[P]    devices used by one group of config p (s_p * n_p), >= 1
+ *   stage_ns[M][P][S] occupancy of stage k (k < s_p), >= 0
+ *   tail_ns[M][P]     overhead added to the finish only, >= 0
+ *   mem_bytes[M][P]   bytes per device of one replica; < 0 = (m,p) not placeable
+ *   num_devices       cluster size D >= 1;  device_budget_bytes >= 0
+ * Bound (reading C20): sum_k stage_ns + tail_ns <= 2^60 for every (m, p).
+ * Errors: ASIM_EINVAL (null/size), ASIM_ERANGE (values out of range). */
+typedef struct {
+  int32_t num_models, num_configs, max_stages;
+  const int64_t* slo_ns;
+  const int32_t* cfg_stages;
+  const int32_t* cfg_devices;
+  const int64_t* stage_ns;
+  const int64_t* tail_ns;
+  const int64_t* mem_bytes;
+  int32_t num_devices;
+  int64_t device_budget_bytes;
+} asim_problem;
+asim_status asim_set_problem(asim_ctx* ctx, const asim_problem* problem);
+
+/* ------------------------------------------------------------------ trace */
+/* The workload W: n requests, arrival_ns[n] non-decreasing and >= 0,
+ * model[n] in [0, M).  Requires asim_set_problem first (ASIM_ESTATE).
+ * Copied into device memory (ptr_kind says where the inputs live).
+ * n may be 0 (attainment 1.0, reading C9).  Errors: ASIM_EUNSORTED,
+ * ASIM_ERANGE (model id, arrival > 2^62, or max arrival + n * max service
+ * >= 2^62), ASIM_EINVAL. */
+asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
+                           const int32_t* model, int32_t ptr_kind, void* cuda_stream);
+
+/* ------------------------------------------------------------- candidates */
+/* Full candidates: C placements of up to max_groups groups.
+ *   group_cfg[C][max_groups]  config id of group g, -1 = no group
+ *   host_mask[C][M]           bit g set <=> model m has a replica on group g
+ * Candidate validity (data, not errors): a candidate that violates memory
+ * ("if sel' is in memory constraint", Alg. 1; per device, sum over the
+ * hosted models of mem_bytes[m][p_g] <= budget), uses more than num_devices
+ * devices, or hosts m on a config with mem_bytes < 0, gets good = -1.
+ * Structural errors (ASIM_ERANGE): config id out of range, a mask bit on a
+ * group with cfg -1 or g >= max_groups, sum of stages > ASIM_MAX_SLOTS. */
+typedef struct {
+  int64_t num_candidates;
+  int32_t max_groups; /* <= ASIM_MAX_GROUPS */
+  const int32_t* group_cfg;
+  const uint64_t* host_mask;
+  int32_t ptr_kind;
+} asim_candidates;
+
+/* One greedy step in delta form: candidate c = base placement cand_base[c]
+ * plus one replica of model cand_model[c] on group cand_group[c]
+ * (sel.add_model_to_group(m, g), Alg. 1).  cand_model[c] = -1 means the
+ * base itself.  The addition must name an existing group (ASIM_ERANGE);
+ * adding a model the group already hosts leaves the base unchanged. */
+typedef struct {
+  int32_t num_bases, max_groups;
+  const int32_t* base_group_cfg;  /* [B][max_groups] */
+  const uint64_t* base_host_mask; /* [B][M] */
+  int64_t num_candidates;
+  const int32_t* cand_base;  /* [C] */
+  const int32_t* cand_model; /* [C] */
+  const int32_t* cand_group; /* [C] */
+  int32_t ptr_kind;
+} asim_deltas;
+
+/* Outputs, host or device per ptr_kind.
+ *   good[C]               required; requests finished within SLO; -1 infeasible
+ *   sum_latency_ns[C]     optional (NULL); sum of (finish - arrival) over good
+ *   good_per_model[C][M]  optional; good split by model
+ *   argmax[1]             optional; index of the max good (ties -> lowest
+ *                         index), -1 if no candidate is feasible */
+typedef struct {
+  int64_t* good;
+  int64_t* sum_latency_ns;
+  int64_t* good_per_model;
+  int64_t* argmax;
+  int32_t ptr_kind;
+} asim_results;
+
+asim_status asim_evaluate(asim_ctx* ctx, const asim_candidates* cands, asim_results* out,
+                          void* cuda_stream);
+asim_status asim_evaluate_deltas(asim_ctx* ctx, const asim_deltas* cands, asim_results* out,
+                                 void* cuda_stream);
+
+/* SLO attainment = good / n; n == 0 -> 1.0; good < 0 -> -1.0. */
+double asim_attainment(int64_t good, int64_t n);
+
+/* ----------------------------------------------------------------- search */
+/* The placement search: Alg. 1 (simulator-guided greedy, beam k = 1,
+ * P:696-737) run for every (group partition, parallel config) of Alg. 2's
+ * single-bucket enumeration, all runs advanced in lockstep so one
+ * launch evaluates every active run's candidates.  Readings C11-C13:
+ *   - candidates of a run are its feasible additions (m, g), m-major,
+ *     g-minor; a step's global candidate list concatenates the active runs in
+ *     run order;
+ *   - each run adds its argmax (ties -> lowest index) and keeps its best
+ *     selection on strict '>'; a run stops when it has no feasible addition;
+ *   - the best run (strict '>', first wins) is the result.
+ * Runs: spec->num_runs = 0 enumerates Alg. 2's single bucket from the
+ * problem: for every divisor `size` of num_devices (ascending) and every
+ * config p with cfg_devices[p] == size (ascending id), one run of
+ * num_devices/size groups of config p.  Otherwise run r has run_num_groups[r]
+ * groups with configs run_group_cfg[sum_{r'<r} G_r' ...] (host arrays).
+ *
+ * Stepwise protocol (for candidate sharding across GPUs):
+ *   asim_search_prepare  -> *num_candidates = C of this step (0 = finished)
+ *   asim_search_evaluate -> good of global candidates [begin, end) into
+ *                           good_dev[0 .. end-begin) (device, stream-ordered)
+ *   (all-gather the shards into one device array of C int64)
+ *   asim_search_apply    -> per-run argmax over good_all_dev[C]; apply
+ * asim_search_run does the whole loop on this context's GPU.
+ * The search borrows ctx (problem and trace must stay set while it lives). */
+typedef struct {
+  int32_t num_runs;              /* 0 = Alg. 2 single-bucket enumeration */
+  const int32_t* run_num_groups; /* [num_runs] */
+  const int32_t* run_group_cfg;  /* [sum run_num_groups] */
+  int32_t dedup;                 /* 1 = evaluate one representative of provably
+                                    identical candidates (exact) */
+} asim_search_spec;
+
+typedef struct {
+  int32_t best_run;        /* -1 if no run improved on the empty placement   */
+  int64_t best_good;
+  int32_t num_groups;      /* of the best run                                 */
+  int32_t* group_cfg;      /* [ASIM_MAX_GROUPS] caller-provided (nullable)    */
+  uint64_t* host_mask;     /* [M] caller-provided (nullable)                  */
+  int64_t steps;           /* lockstep iterations executed                    */
+  int64_t candidates;      /* sum over steps of C (simulate() calls)          */
+  int64_t evaluated;       /* candidates actually simulated (after dedup)     */
+  int64_t request_evals;   /* sum over evaluated candidates of n (requests)   */
+} asim_search_result;
+
+asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim_search** out);
+void asim_search_destroy(asim_search* s);
+asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates);
+asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int64_t* good_dev,
+                                 void* cuda_stream);
+asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void* cuda_stream);
+asim_status asim_search_run(asim_search* s, void* cuda_stream);
+asim_status asim_search_result_get(const asim_search* s, asim_search_result* out);
+/* Per-run outcome: best good of run r and its selection (host arrays). */
+asim_status asim_search_run_info(const asim_search* s, int32_t run, int32_t* num_groups,
+                                 int32_t* group_cfg, uint64_t* host_mask, int64_t* best_good,
+                                 int64_t* steps);
+int32_t asim_search_num_runs(const asim_search* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASIM_H */

@@ -1,0 +1,119 @@
+// ctx.h -- host-side context shared by ctx.cpp and search.cpp (private).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/asim.h"
+#include "asim_internal.h"
+
+// Grow-only device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 256 ? 256 : bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct HostProblem {
+  int32_t M = 0, P = 0, S = 0;
+  std::vector<int64_t> slo, stage, tail, mem;
+  std::vector<int32_t> cfg_stages, cfg_devices;
+  int32_t num_devices = 0;
+  int64_t budget = 0;
+  int64_t max_service = 0;  // max over (m,p) of sum_k stage + tail
+  int64_t mem_at(int m, int p) const { return mem[(int64_t)m * P + p]; }
+};
+
+struct asim_ctx {
+  int device = 0;
+  std::string err;
+  int64_t launches = 0;
+  bool broken = false;
+
+  bool has_problem = false;
+  HostProblem hp;
+  DBuf d_stage, d_tail, d_slo, d_cfg_stages;
+
+  bool has_trace = false;
+  int64_t n = 0;
+  int64_t max_arrival = 0;
+  DBuf d_arrival, d_model;
+
+  // statistics (asim_set_profiling)
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  int64_t sim_launches = 0;
+  double sim_ms = 0.0;
+  int64_t request_evals = 0;
+  DBuf d_counter;  // unsigned long long stage-update counter
+
+  // scratch for evaluate()
+  DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;
+  DBuf d_good, d_sum, d_pm, d_argmax;
+
+  asim::DevProblem dev_problem() const {
+    asim::DevProblem p;
+    p.M = hp.M;
+    p.P = hp.P;
+    p.S = hp.S;
+    p.stage = d_stage.as<int64_t>();
+    p.tail = d_tail.as<int64_t>();
+    p.slo = d_slo.as<int64_t>();
+    p.cfg_stages = d_cfg_stages.as<int32_t>();
+    return p;
+  }
+  asim::DevTrace dev_trace() const {
+    asim::DevTrace t;
+    t.n = n;
+    t.arrival = d_arrival.as<int64_t>();
+    t.model = d_model.as<uint16_t>();
+    return t;
+  }
+};
+
+// helpers implemented in ctx.cpp
+asim_status asim_fail(asim_ctx* ctx, asim_status code, const std::string& msg);
+asim_status asim_cuda(asim_ctx* ctx, cudaError_t e, const char* what);
+// Validate the call order and the overflow bound (reading C20).
+asim_status asim_ready(asim_ctx* ctx);
+// Upload host vector to a grow-only device buffer (async on stream).
+template <class T>
+cudaError_t upload(DBuf& buf, const std::vector<T>& v, cudaStream_t st) {
+  cudaError_t e = buf.ensure(v.size() * sizeof(T) + 8);
+  if (e != cudaSuccess || v.empty()) return e;
+  return cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st);
+}
+
+// Batch encoding shared by evaluate, evaluate_deltas and the search.
+struct HostBatch {
+  int32_t G = 0;
+  std::vector<int32_t> base_cfg;   // [B][G]
+  std::vector<uint64_t> base_mask; // [B][M]
+  std::vector<int32_t> cand_base, cand_model, cand_group;
+  std::vector<uint8_t> cand_ok;
+  int32_t slots = 1;               // max over bases of sum of stages
+};
+// Upload a batch and launch the simulation of candidates [0, C) writing
+// good/sum/per-model at out (device pointers, indexed by candidate).
+asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
+                           const asim::DevOut& out, cudaStream_t st);

@@ -1,0 +1,313 @@
+// search.cpp -- the placement search driver (host, native): Alg. 1
+// "Simulator-Guided Greedy Model Selection" with beam k = 1 for
+// every (group partition, parallel config) of Alg. 2's single bucket
+// (P:740-786), all runs advanced in lockstep so that one kernel launch
+// evaluates the candidates of every active run.
+//
+// Per lockstep step:
+//   prepare   a1: every active run lists its feasible additions (m, g),
+//             m-major / g-minor ("for (m, (g, p)) in M x (G, P)", P:706;
+//             "if sel' is in memory constraint"); runs without any
+//             stop ("if new_sels = {} then break").
+//   evaluate  the simulation kernel on a contiguous shard of the step's list.
+//   apply     a7: per run, argmax (ties -> lowest index, "pick_highest",
+//             P:722) and sel <- sel + (m*, g*); best_sel on strict '>'.
+//
+// Exact de-duplication (spec->dedup): adding model m to either of two EMPTY
+// groups g1 < g2 with the same config gives the same simulation whenever g1
+// and g2 sit between the same pair of m's hosting groups in index order
+// (relabelling g1 <-> g2 maps one simulation onto the other and preserves
+// every dispatch tie-break, reading C1).  Only the lowest such g -- the one
+// the argmax would pick on a tie anyway -- is listed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+
+namespace {
+
+struct Run {
+  int32_t G = 0;
+  std::vector<int32_t> cfg;
+  std::vector<uint64_t> sel;   // [M] current selection
+  std::vector<int64_t> used;   // [G] bytes per device
+  std::vector<uint64_t> best;  // [M] best selection so far
+  int64_t best_good = 0;
+  bool active = true;
+  int64_t steps = 0;
+};
+
+}  // namespace
+
+struct asim_search {
+  asim_ctx* ctx = nullptr;
+  std::vector<Run> runs;
+  bool dedup = false;
+  int32_t G = 0;  // max groups over runs
+  // step state
+  bool prepared = false;
+  HostBatch hb;
+  std::vector<int32_t> base_run;  // base -> run id
+  std::vector<int64_t> seg;       // [bases + 1] candidate offsets per base
+  DBuf d_good_all;
+  std::vector<int64_t> h_good;
+  // statistics
+  int64_t steps = 0, candidates = 0, evaluated = 0;
+};
+
+static asim_status sfail(asim_search* s, asim_status code, const std::string& m) {
+  return asim_fail(s ? s->ctx : nullptr, code, m);
+}
+
+extern "C" {
+
+asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim_search** out) {
+  if (!ctx || !out) return ASIM_EINVAL;
+  *out = nullptr;
+  asim_status st = asim_ready(ctx);
+  if (st) return st;
+  if (!spec) return asim_fail(ctx, ASIM_EINVAL, "null spec");
+  const HostProblem& hp = ctx->hp;
+  std::vector<std::vector<int32_t>> groups;
+  if (spec->num_runs == 0) {
+    // Alg. 2 single bucket: D/size equal groups, one config each (C13)
+    for (int32_t size = 1; size <= hp.num_devices; ++size) {
+      if (hp.num_devices % size) continue;
+      for (int32_t p = 0; p < hp.P; ++p) {
+        if (hp.cfg_devices[p] != size) continue;
+        const int32_t G = hp.num_devices / size;
+        if (G > ASIM_MAX_GROUPS)
+          return asim_fail(ctx, ASIM_ERANGE,
+                           "Alg. 2 run with more than ASIM_MAX_GROUPS groups; pass explicit runs");
+        groups.emplace_back(G, p);
+      }
+    }
+  } else {
+    if (spec->num_runs < 0 || !spec->run_num_groups || !spec->run_group_cfg)
+      return asim_fail(ctx, ASIM_EINVAL, "bad run list");
+    int64_t off = 0;
+    for (int32_t r = 0; r < spec->num_runs; ++r) {
+      const int32_t G = spec->run_num_groups[r];
+      if (G < 1 || G > ASIM_MAX_GROUPS) return asim_fail(ctx, ASIM_ERANGE, "run_num_groups");
+      std::vector<int32_t> cfg(spec->run_group_cfg + off, spec->run_group_cfg + off + G);
+      off += G;
+      int32_t slots = 0;
+      for (int32_t c : cfg) {
+        if (c < 0 || c >= hp.P) return asim_fail(ctx, ASIM_ERANGE, "run_group_cfg");
+        slots += hp.cfg_stages[c];
+      }
+      if (slots > ASIM_MAX_SLOTS) return asim_fail(ctx, ASIM_ERANGE, "run exceeds ASIM_MAX_SLOTS");
+      groups.push_back(std::move(cfg));
+    }
+  }
+  asim_search* s = new (std::nothrow) asim_search();
+  if (!s) return asim_fail(ctx, ASIM_ENOMEM, "host allocation failed");
+  s->ctx = ctx;
+  s->dedup = spec->dedup != 0;
+  for (auto& cfg : groups) {
+    Run r;
+    r.G = (int32_t)cfg.size();
+    r.cfg = cfg;
+    r.sel.assign(hp.M, 0);
+    r.best.assign(hp.M, 0);
+    r.used.assign(r.G, 0);
+    int64_t devices = 0;
+    for (int32_t c : cfg) devices += hp.cfg_devices[c];
+    if (devices > hp.num_devices) r.active = false;  // the empty placement is already infeasible
+    s->G = std::max(s->G, r.G);
+    s->runs.push_back(std::move(r));
+  }
+  *out = s;
+  return ASIM_OK;
+}
+
+void asim_search_destroy(asim_search* s) {
+  if (!s) return;
+  s->d_good_all.release();
+  delete s;
+}
+
+int32_t asim_search_num_runs(const asim_search* s) { return s ? (int32_t)s->runs.size() : 0; }
+
+asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
+  if (!s || !num_candidates) return ASIM_EINVAL;
+  asim_status st = asim_ready(s->ctx);
+  if (st) return st;
+  if (s->prepared) return sfail(s, ASIM_ESTATE, "prepare called twice without apply");
+  const HostProblem& hp = s->ctx->hp;
+  const int32_t M = hp.M, G = s->G;
+  HostBatch& hb = s->hb;
+  hb = HostBatch();
+  hb.G = G;
+  s->base_run.clear();
+  s->seg.assign(1, 0);
+  int64_t full = 0;
+  for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r) {
+    Run& run = s->runs[r];
+    if (!run.active) continue;
+    const int32_t b = (int32_t)s->base_run.size();
+    std::vector<uint8_t> empty(run.G, 1);
+    for (int32_t m = 0; m < M; ++m)
+      for (int32_t g = 0; g < run.G; ++g)
+        if ((run.sel[m] >> g) & 1ULL) empty[g] = 0;
+    int64_t n_run = 0;
+    for (int32_t m = 0; m < M; ++m) {
+      std::map<std::pair<int32_t, int32_t>, bool> seen;  // (cfg, rank among hosts) of empty groups
+      for (int32_t g = 0; g < run.G; ++g) {
+        if ((run.sel[m] >> g) & 1ULL) continue;  // a model at most once per group (C11)
+        const int64_t mb = hp.mem_at(m, run.cfg[g]);
+        if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
+        ++full;
+        ++n_run;
+        if (s->dedup && empty[g]) {
+          const uint64_t below = g ? (run.sel[m] & ((1ULL << g) - 1)) : 0ULL;
+          auto key = std::make_pair(run.cfg[g], (int32_t)__builtin_popcountll(below));
+          if (seen.count(key)) continue;
+          seen[key] = true;
+        }
+        hb.cand_base.push_back(b);
+        hb.cand_model.push_back(m);
+        hb.cand_group.push_back(g);
+        hb.cand_ok.push_back(1);
+      }
+    }
+    if (n_run == 0) {  // no feasible addition: this run's Alg. 1 loop ends
+      run.active = false;
+      continue;
+    }
+    s->base_run.push_back(r);
+    for (int32_t g = 0; g < G; ++g) hb.base_cfg.push_back(g < run.G ? run.cfg[g] : -1);
+    hb.base_mask.insert(hb.base_mask.end(), run.sel.begin(), run.sel.end());
+    int32_t slots = 0;
+    for (int32_t c : run.cfg) slots += hp.cfg_stages[c];
+    hb.slots = std::max(hb.slots, slots);
+    s->seg.push_back((int64_t)hb.cand_base.size());
+  }
+  s->prepared = true;
+  *num_candidates = (int64_t)hb.cand_base.size();
+  if (*num_candidates == 0) s->prepared = false;  // search finished
+  s->candidates += full;
+  s->evaluated += *num_candidates;
+  if (*num_candidates) ++s->steps;
+  return ASIM_OK;
+}
+
+asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int64_t* good_dev,
+                                 void* cuda_stream) {
+  if (!s) return ASIM_EINVAL;
+  if (!s->prepared) return sfail(s, ASIM_ESTATE, "evaluate before prepare");
+  const int64_t C = (int64_t)s->hb.cand_base.size();
+  if (begin < 0 || end < begin || end > C) return sfail(s, ASIM_ERANGE, "shard range");
+  if (end == begin) return ASIM_OK;
+  if (!good_dev) return sfail(s, ASIM_EINVAL, "null good_dev");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != s->ctx->device) cudaSetDevice(s->ctx->device);
+  asim::DevOut out;
+  out.good = good_dev;
+  out.sum_latency = nullptr;
+  out.good_per_model = nullptr;
+  out.out_offset = begin;
+  out.stage_updates = nullptr;
+  asim_status st = asim_run_batch(s->ctx, s->hb, begin, end, out,
+                                  static_cast<cudaStream_t>(cuda_stream));
+  if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
+  return st;
+}
+
+asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void* cuda_stream) {
+  if (!s) return ASIM_EINVAL;
+  if (!s->prepared) return sfail(s, ASIM_ESTATE, "apply before prepare");
+  if (!good_all_dev) return sfail(s, ASIM_EINVAL, "null good_all_dev");
+  const int64_t C = (int64_t)s->hb.cand_base.size();
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  s->h_good.resize(C);
+  cudaError_t e = cudaMemcpyAsync(s->h_good.data(), good_all_dev, C * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return asim_cuda(s->ctx, e, "copy step results");
+  const HostProblem& hp = s->ctx->hp;
+  for (size_t b = 0; b < s->base_run.size(); ++b) {
+    Run& run = s->runs[s->base_run[b]];
+    int64_t bi = -1, bg = -1;
+    for (int64_t c = s->seg[b]; c < s->seg[b + 1]; ++c)
+      if (s->h_good[c] > bg) {  // first maximum: lowest index on ties (C12)
+        bg = s->h_good[c];
+        bi = c;
+      }
+    if (bi < 0) return sfail(s, ASIM_ERANGE, "step results contain no feasible candidate");
+    const int32_t m = s->hb.cand_model[bi], g = s->hb.cand_group[bi];
+    run.sel[m] |= 1ULL << g;
+    run.used[g] += hp.mem_at(m, run.cfg[g]);
+    ++run.steps;
+    if (bg > run.best_good) {  // "if sel*.slo_att > best_sel.slo_att"
+      run.best_good = bg;
+      run.best = run.sel;
+    }
+  }
+  s->prepared = false;
+  return ASIM_OK;
+}
+
+asim_status asim_search_run(asim_search* s, void* cuda_stream) {
+  if (!s) return ASIM_EINVAL;
+  for (;;) {
+    int64_t C = 0;
+    asim_status st = asim_search_prepare(s, &C);
+    if (st) return st;
+    if (C == 0) return ASIM_OK;
+    cudaError_t e = s->d_good_all.ensure(C * 8 + 8);
+    if (e != cudaSuccess) return asim_cuda(s->ctx, e, "allocate step results");
+    st = asim_search_evaluate(s, 0, C, s->d_good_all.as<int64_t>(), cuda_stream);
+    if (st) return st;
+    st = asim_search_apply(s, s->d_good_all.as<int64_t>(), cuda_stream);
+    if (st) return st;
+  }
+}
+
+asim_status asim_search_result_get(const asim_search* s, asim_search_result* out) {
+  if (!s || !out) return ASIM_EINVAL;
+  int32_t best = -1;
+  int64_t best_good = 0;
+  for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r)
+    if (s->runs[r].best_good > best_good) {  // Alg. 2: strict '>' keeps the first best run
+      best_good = s->runs[r].best_good;
+      best = r;
+    }
+  out->best_run = best;
+  out->best_good = best_good;
+  out->num_groups = best >= 0 ? s->runs[best].G : 0;
+  if (out->group_cfg) {
+    for (int32_t g = 0; g < ASIM_MAX_GROUPS; ++g)
+      out->group_cfg[g] = (best >= 0 && g < s->runs[best].G) ? s->runs[best].cfg[g] : -1;
+  }
+  if (out->host_mask)
+    for (int32_t m = 0; m < s->ctx->hp.M; ++m)
+      out->host_mask[m] = best >= 0 ? s->runs[best].best[m] : 0;
+  out->steps = s->steps;
+  out->candidates = s->candidates;
+  out->evaluated = s->evaluated;
+  out->request_evals = s->evaluated * s->ctx->n;
+  return ASIM_OK;
+}
+
+asim_status asim_search_run_info(const asim_search* s, int32_t run, int32_t* num_groups,
+                                 int32_t* group_cfg, uint64_t* host_mask, int64_t* best_good,
+                                 int64_t* steps) {
+  if (!s || run < 0 || run >= (int32_t)s->runs.size()) return ASIM_EINVAL;
+  const Run& r = s->runs[run];
+  if (num_groups) *num_groups = r.G;
+  if (group_cfg)
+    for (int32_t g = 0; g < r.G; ++g) group_cfg[g] = r.cfg[g];
+  if (host_mask)
+    for (int32_t m = 0; m < s->ctx->hp.M; ++m) host_mask[m] = r.best[m];
+  if (best_good) *best_good = r.best_good;
+  if (steps) *steps = r.steps;
+  return ASIM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+"""GPU parity of the whole placement search: libasim.so's lockstep Alg. 2 /
+Alg. 1 driver (with and without exact de-duplication) must pick the same
+placement as the oracle's plain step-by-step search, run by run."""
+
+import numpy as np
+import pytest
+
+from oracle import search as osearch
+from workloads import configs, traces
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sim():
+    from paper_2302_11665_b200 import Simulator
+    s = Simulator(0)
+    yield s
+    s.close()
+
+
+def _compare(sim, prob, tr, dedup_modes=(False, True)):
+    ref = osearch.alg2(prob, tr)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    for dedup in dedup_modes:
+        res = sim.search(dedup=dedup)
+        assert len(res.runs) == len(ref["runs"])
+        for r_gpu, r_ref in zip(res.runs, ref["runs"]):
+            assert r_gpu["best_good"] == r_ref["good"]
+            np.testing.assert_array_equal(r_gpu["host_mask"], r_ref["placement"].host_mask)
+            np.testing.assert_array_equal(r_gpu["group_cfg"], r_ref["placement"].group_cfg)
+        assert res.best_good == ref["good"]
+        assert res.best_run == ref["run"]
+        if ref["run"] >= 0:
+            np.testing.assert_array_equal(res.host_mask, ref["placement"].host_mask)
+    return ref
+
+
+def test_search_motivating(sim):
+    for scale in (1.0, 1.5, 3.0, 5.0):
+        prob = configs.motivating_problem(slo_scale=scale)
+        tr = configs.motivating_trace(seed=2, n_requests=1000)
+        _compare(sim, prob, tr)
+
+
+def test_search_s1_shaped_small(sim):
+    names = [f"BERT-1.3B#{i}" for i in range(8)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=2.0)
+    tr = traces.independent_gamma(3, [3.0] * 8, 4.0, 120.0)
+    _compare(sim, prob, tr)
+
+
+def test_search_s3_shaped_small(sim):
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "BERT-6.7B", "MoE-1.3B",
+                                  "MoE-2.4B", "MoE-5.3B") for i in range(2)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=5.0)
+    tr = traces.maf2_shaped(4, len(names), 20.0, 300.0)
+    _compare(sim, prob, tr)
+
+
+def test_search_s4_shaped(sim):
+    prob, tr = configs.s4(duration=1800.0)
+    ref = _compare(sim, prob, tr)
+    assert ref["good"] > 0

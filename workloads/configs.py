@@ -45,7 +45,7 @@ def build_problem(model_names, num_devices, budget, slo_scale=5.0, num_layers=24
         if per_model and name in per_model:
             specs.append(per_model[name])
         else:
-            b, lat = table1.MODELS[name]
+            b, lat = table1.MODELS[name.split("#")[0]]
             specs.append((b, lat, None, None))
     maxK = max((k or num_layers) for _, _, k, _ in specs)
     if configs is None:

@@ -98,10 +98,20 @@ typedef struct {
   double sim_ms;
   int64_t stage_updates;
   int64_t request_evals;
+  int64_t chunk_reruns;  /* fix-up re-runs of chunks whose trajectories never met */
 } asim_stats;
 asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
 asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);
 asim_status asim_reset_stats(asim_ctx* ctx);
+/* Kernel selection (testing): 0 = automatic (default), 1 = general
+ * lane-per-candidate kernel over the whole trace, 2 = chunked kernel with
+ * speculative time chunks and exact fix-up whenever the batch allows it.
+ * Results are identical for every choice. */
+asim_status asim_set_path(asim_ctx* ctx, int32_t path);
+/* Minimum time-chunk length in requests for the chunked kernel (default
+ * 4096; small values exercise the fix-up in tests).  Results do not depend
+ * on it. */
+asim_status asim_set_chunk_size(asim_ctx* ctx, int64_t min_requests);
 
 /* ---------------------------------------------------------------- problem */
 /* "a set of models" + "a cluster resource specification".  All

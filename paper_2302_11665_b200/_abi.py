@@ -48,7 +48,7 @@ class asim_results(ctypes.Structure):
 
 class asim_stats(ctypes.Structure):
     _fields_ = [("launches", i64), ("sim_launches", i64), ("sim_ms", ctypes.c_double),
-                ("stage_updates", i64), ("request_evals", i64)]
+                ("stage_updates", i64), ("request_evals", i64), ("chunk_reruns", i64)]
 
 
 class asim_search_spec(ctypes.Structure):
@@ -86,6 +86,8 @@ asim_launch_count = _bind("asim_launch_count", i64, [vp])
 asim_set_profiling = _bind("asim_set_profiling", i32, [vp, i32])
 asim_get_stats = _bind("asim_get_stats", i32, [vp, _P(asim_stats)])
 asim_reset_stats = _bind("asim_reset_stats", i32, [vp])
+asim_set_path = _bind("asim_set_path", i32, [vp, i32])
+asim_set_chunk_size = _bind("asim_set_chunk_size", i32, [vp, i64])
 asim_set_problem = _bind("asim_set_problem", i32, [vp, _P(asim_problem)])
 asim_set_trace = _bind("asim_set_trace", i32, [vp, i64, vp, vp, i32, vp])
 asim_evaluate = _bind("asim_evaluate", i32, [vp, _P(asim_candidates), _P(asim_results), vp])

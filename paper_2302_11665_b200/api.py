@@ -109,7 +109,15 @@ class Simulator:
         s = A.asim_stats()
         self._check(A.asim_get_stats(self.h, ctypes.byref(s)))
         return dict(launches=s.launches, sim_launches=s.sim_launches, sim_ms=s.sim_ms,
-                    stage_updates=s.stage_updates, request_evals=s.request_evals)
+                    stage_updates=s.stage_updates, request_evals=s.request_evals,
+                    chunk_reruns=s.chunk_reruns)
+
+    def set_chunk_size(self, min_requests: int) -> None:
+        self._check(A.asim_set_chunk_size(self.h, int(min_requests)))
+
+    def set_path(self, path: int) -> None:
+        """0 auto, 1 general kernel, 2 chunked kernel (identical results)."""
+        self._check(A.asim_set_path(self.h, int(path)))
 
     # ------------------------------------------------------------- inputs
     def set_problem(self, prob) -> None:

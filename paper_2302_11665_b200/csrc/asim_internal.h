@@ -58,3 +58,54 @@ cudaError_t launch_argmax(const int64_t* good, int64_t C, int64_t* argmax_out,
                           cudaStream_t stream, int64_t* launches);
 
 }  // namespace asim
+
+namespace asim {
+
+// ---- chunked throughput path (chunk.cu) ----------------------------------
+// Work item: up to 32 consecutive candidates sharing one base placement.
+struct ItemDesc {
+  int32_t base;    // base index in the batch
+  int32_t first;   // first candidate (batch index)
+  int32_t count;   // 1..32
+  int32_t S;       // compile-time stage class: 1,2,4,8,16 (uniform config) or 0 (dynamic)
+  int32_t cfg;     // the base's uniform config id, -1 if groups differ
+  int32_t stages;  // stages of `cfg` (uniform case)
+  int32_t slots;   // sum of stages over the base's groups
+  int32_t pad;
+};
+
+struct ChunkUnit {  // fix-up work unit
+  int32_t item, chunk, src;  // src: start state from 0 = spec_end, 1 = fix_end of chunk-1
+  int32_t pad;
+};
+
+struct ChunkParams {
+  DevProblem pr;
+  DevTrace tr;
+  DevBatch bt;
+  const ItemDesc* items;
+  int32_t num_items;
+  int32_t J;                   // chunks
+  const int64_t* chunk_begin;  // [J+1] request index boundaries
+  int64_t theta;               // uint32 epoch threshold (see chunk.cu)
+  int32_t slots_max;
+  int32_t num_units;
+  const ChunkUnit* units;      // fix-up passes only
+  uint32_t* counter;           // dynamic work counter
+  int32_t* spec_good;          // [J][items*32]
+  int64_t* spec_sum;
+  void* spec_end;              // [J][items][slots_max][32] of T
+  int64_t* spec_epoch;         // [J][items]
+  int32_t* fix_good;
+  int64_t* fix_sum;
+  void* fix_end;
+  int64_t* fix_epoch;
+  uint8_t* fix_flag;           // [J][items] 1 = not coalesced within the chunk
+};
+
+cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStream_t st, int sms,
+                              int64_t* launches);
+cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
+                                int64_t* launches);
+
+}  // namespace asim

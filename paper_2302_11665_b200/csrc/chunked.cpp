@@ -1,0 +1,189 @@
+// chunked.cpp -- host orchestration of the chunked throughput path
+// (chunk.cu): work-item construction, chunk sizing, the speculative pass,
+// the fix-up passes with exact re-run chains, and the final reduction.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "ctx.h"
+
+namespace {
+
+constexpr int kSTab = 16;
+
+int stage_class(int s) { return (s == 1 || s == 2 || s == 4 || s == 8 || s == 16) ? s : 0; }
+
+}  // namespace
+
+bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out) {
+  if (out.good_per_model) return false;  // per-model counts: general kernel (sim.cu)
+  if (hb.slots > ASIM_MAX_SLOTS) return false;
+  const size_t M = (size_t)ctx->hp.M;
+  const size_t per_warp = (size_t)hb.slots * 32 * 8 * 2 + M * (8 + 8 * (kSTab + 2)) + 256;
+  return 4 * per_warp <= 220 * 1024;
+}
+
+// uint32 relative time is exact when 2^32 - 1 - max slo - max service > 0
+// (chunk.cu header); require some headroom so epochs move rarely.
+static int64_t theta_for(const asim_ctx* ctx) {
+  int64_t slo_max = 0;
+  for (int64_t s : ctx->hp.slo) slo_max = std::max(slo_max, s);
+  const __int128 th = (__int128)0xFFFFFFFFll - slo_max - ctx->hp.max_service;
+  if (th < 100000000) return -1;  // < 0.1 s of headroom: use int64
+  return (int64_t)th;
+}
+
+asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
+                             const asim::DevOut& out, cudaStream_t st) {
+  const int64_t N = ctx->n;
+  const HostProblem& hp = ctx->hp;
+  // ---- work items: <= 32 consecutive candidates of one base
+  std::vector<asim::ItemDesc> items;
+  std::vector<int32_t> base_cfg_uniform, base_slots;
+  const int32_t B = hb.G ? (int32_t)(hb.base_cfg.size() / hb.G) : (int32_t)(hb.base_mask.size() / hp.M);
+  base_cfg_uniform.assign(B, -1);
+  base_slots.assign(B, 0);
+  for (int32_t b = 0; b < B; ++b) {
+    int32_t u = -2, slots = 0;
+    for (int32_t g = 0; g < hb.G; ++g) {
+      const int32_t c = hb.base_cfg[(int64_t)b * hb.G + g];
+      if (c < 0) continue;
+      slots += hp.cfg_stages[c];
+      u = (u == -2 || u == c) ? c : -1;
+    }
+    base_cfg_uniform[b] = u >= 0 ? u : -1;
+    base_slots[b] = slots;
+  }
+  int32_t slots_max = 1;
+  for (int64_t c = begin; c < end;) {
+    const int32_t b = hb.cand_base[c];
+    int32_t cnt = 1;
+    while (c + cnt < end && cnt < 32 && hb.cand_base[c + cnt] == b) ++cnt;
+    asim::ItemDesc it{};
+    it.base = b;
+    it.first = (int32_t)c;
+    it.count = cnt;
+    it.cfg = base_cfg_uniform[b];
+    it.stages = it.cfg >= 0 ? hp.cfg_stages[it.cfg] : 0;
+    it.S = it.cfg >= 0 ? stage_class(it.stages) : 0;
+    if (it.S == 0) it.cfg = -1;
+    it.slots = base_slots[b];
+    slots_max = std::max(slots_max, it.slots);
+    items.push_back(it);
+    c += cnt;
+  }
+  const int32_t I = (int32_t)items.size();
+  if (I == 0) return ASIM_OK;
+  // ---- chunks: enough (item, chunk) units to fill the GPU, chunks >= kMinChunk
+  const int64_t target_units = (int64_t)ctx->sms * 16 * 4;
+  int64_t J = (target_units + I - 1) / I;
+  J = std::min<int64_t>(J, std::max<int64_t>(1, N / std::max<int64_t>(1, ctx->min_chunk)));
+  J = std::max<int64_t>(1, std::min<int64_t>(J, 1 << 16));
+  if (N == 0) J = 1;
+  std::vector<int64_t> cb(J + 1);
+  for (int64_t j = 0; j <= J; ++j) cb[j] = N * j / J;
+  const int64_t theta = theta_for(ctx);
+  const bool u32 = theta > 0;
+  const size_t tsz = u32 ? 4 : 8;
+
+  // ---- device buffers (grow-only)
+  const int64_t per_chunk = (int64_t)I * 32;
+  cudaError_t e = upload(ctx->c_items, items, st);
+  if (e == cudaSuccess) e = upload(ctx->c_begin, cb, st);
+  if (e == cudaSuccess) e = ctx->c_spec_good.ensure(J * per_chunk * 4);
+  if (e == cudaSuccess) e = ctx->c_spec_sum.ensure(J * per_chunk * 8);
+  if (e == cudaSuccess) e = ctx->c_fix_good.ensure(J * per_chunk * 4);
+  if (e == cudaSuccess) e = ctx->c_fix_sum.ensure(J * per_chunk * 8);
+  if (e == cudaSuccess) e = ctx->c_spec_end.ensure(J * I * (int64_t)slots_max * 32 * tsz);
+  if (e == cudaSuccess) e = ctx->c_fix_end.ensure(J * I * (int64_t)slots_max * 32 * tsz);
+  if (e == cudaSuccess) e = ctx->c_spec_epoch.ensure(J * I * 8);
+  if (e == cudaSuccess) e = ctx->c_fix_epoch.ensure(J * I * 8);
+  if (e == cudaSuccess) e = ctx->c_flag.ensure(J * I);
+  if (e == cudaSuccess) e = ctx->c_counter.ensure(16);
+  if (e == cudaSuccess && J > 1) e = ctx->c_units.ensure(J * I * sizeof(asim::ChunkUnit));
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk buffers");
+
+  asim::ChunkParams P{};
+  P.pr = ctx->dev_problem();
+  P.tr = ctx->dev_trace();
+  P.bt.G = hb.G;
+  P.bt.base_cfg = ctx->d_base_cfg.as<int32_t>();
+  P.bt.base_mask = ctx->d_base_mask.as<uint64_t>();
+  P.bt.cand_base = ctx->d_cand_base.as<int32_t>();
+  P.bt.cand_model = ctx->d_cand_model.as<int32_t>();
+  P.bt.cand_group = ctx->d_cand_group.as<int32_t>();
+  P.bt.cand_ok = ctx->d_cand_ok.as<uint8_t>();
+  P.bt.C = (int64_t)hb.cand_base.size();
+  P.items = ctx->c_items.as<asim::ItemDesc>();
+  P.num_items = I;
+  P.J = (int32_t)J;
+  P.chunk_begin = ctx->c_begin.as<int64_t>();
+  P.theta = theta;
+  P.slots_max = slots_max;
+  P.counter = ctx->c_counter.as<uint32_t>();
+  P.spec_good = ctx->c_spec_good.as<int32_t>();
+  P.spec_sum = ctx->c_spec_sum.as<int64_t>();
+  P.spec_end = ctx->c_spec_end.p;
+  P.spec_epoch = ctx->c_spec_epoch.as<int64_t>();
+  P.fix_good = ctx->c_fix_good.as<int32_t>();
+  P.fix_sum = ctx->c_fix_sum.as<int64_t>();
+  P.fix_end = ctx->c_fix_end.p;
+  P.fix_epoch = ctx->c_fix_epoch.as<int64_t>();
+  P.fix_flag = ctx->c_flag.as<uint8_t>();
+
+  // ---- pass 1: every (item, chunk) from the idle state
+  P.num_units = (int32_t)(J * I);
+  P.units = nullptr;
+  e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
+
+  if (J > 1) {
+    // ---- pass 2: fix-up of every chunk j >= 1 from chunk j-1's speculative end
+    std::vector<asim::ChunkUnit> units;
+    units.reserve((J - 1) * I);
+    for (int32_t i = 0; i < I; ++i)
+      for (int32_t j = 1; j < J; ++j) units.push_back(asim::ChunkUnit{i, j, 0, 0});
+    e = upload(ctx->c_units, units, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "upload units");
+    P.units = ctx->c_units.as<asim::ChunkUnit>();
+    P.num_units = (int32_t)units.size();
+    e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 2");
+    // ---- exact re-run chains: a chunk whose trajectories never met publishes
+    // its true end state; the next chunk is re-run from it, and so on.
+    std::vector<uint8_t> flag(J * I);
+    std::vector<uint8_t> computed_src(J * I, 0);  // start source used by unit (item, j)
+    std::vector<int32_t> pos(I, 1);
+    std::vector<uint8_t> prev_src(I, 0);
+    for (;;) {
+      e = cudaMemcpyAsync(flag.data(), P.fix_flag, J * I, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk flags");
+      std::vector<asim::ChunkUnit> redo;
+      for (int32_t i = 0; i < I; ++i) {
+        while (pos[i] < J) {
+          const int64_t u = (int64_t)pos[i] * I + i;
+          if (computed_src[u] == prev_src[i]) {
+            prev_src[i] = flag[u] ? 1 : 0;
+            ++pos[i];
+          } else {
+            redo.push_back(asim::ChunkUnit{i, pos[i], 1, 0});
+            computed_src[u] = 1;
+            break;
+          }
+        }
+      }
+      if (redo.empty()) break;
+      ctx->chunk_reruns += (int64_t)redo.size();
+      e = upload(ctx->c_units, redo, st);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "upload redo units");
+      P.num_units = (int32_t)redo.size();
+      e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk re-run");
+    }
+  }
+  e = asim::launch_chunk_reduce(P, out, st, &ctx->launches);
+  return asim_cuda(ctx, e, "chunk reduce");
+}

@@ -151,6 +151,31 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
   if (e == cudaSuccess) e = upload(ctx->d_cand_group, hb.cand_group, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_ok, hb.cand_ok, st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload batch");
+  // Throughput path: candidates sharing a base placement, no per-model
+  // counts -> chunked kernel (chunk.cu); otherwise the general kernel below.
+  const bool shared_bases = (int64_t)(hb.base_cfg.size() / std::max<int32_t>(hb.G, 1)) < C ||
+                            hb.G == 0;
+  bool chunked = ctx->force_path == 2 ||
+                 (ctx->force_path == 0 && shared_bases && asim_chunked_eligible(ctx, hb, out));
+  if (ctx->force_path == 2 && !asim_chunked_eligible(ctx, hb, out)) chunked = false;
+  if (chunked) {
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (ctx->profiling) {
+      if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
+        return asim_cuda(ctx, cudaGetLastError(), "event create");
+      cudaEventRecord(ev0, st);
+    }
+    asim_status s = asim_run_chunked(ctx, hb, begin, end, out, st);
+    if (ctx->profiling) {
+      cudaEventRecord(ev1, st);
+      ctx->events.emplace_back(ev0, ev1);
+      ++ctx->sim_launches;
+      int64_t ok = 0;
+      for (int64_t i = begin; i < end; ++i) ok += hb.cand_ok[i];
+      ctx->request_evals += ok * ctx->n;
+    }
+    return s;
+  }
   // warp items: 32 consecutive candidates, cut where the base changes so a
   // warp shares one base placement (uniform hosting lists)
   std::vector<asim::WarpItem> items;
@@ -223,6 +248,7 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   asim_ctx* ctx = new (std::nothrow) asim_ctx();
   if (!ctx) return asim_fail(nullptr, ASIM_ENOMEM, "host allocation failed");
   ctx->device = cuda_device;
+  ctx->sms = prop.multiProcessorCount;
   *out = ctx;
   return ASIM_OK;
 }
@@ -236,7 +262,10 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->d_arrival, &ctx->d_model, &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group,
                     &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm,
-                    &ctx->d_argmax, &ctx->d_counter};
+                    &ctx->d_argmax, &ctx->d_counter, &ctx->c_items, &ctx->c_begin,
+                    &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
+                    &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
+                    &ctx->c_flag, &ctx->c_counter, &ctx->c_units};
     for (DBuf* b : bufs) b->release();
   }
   delete ctx;
@@ -260,11 +289,26 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   ctx->sim_launches = 0;
   ctx->sim_ms = 0.0;
   ctx->request_evals = 0;
+  ctx->chunk_reruns = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 8);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return asim_cuda(ctx, e, "reset stats");
   }
+  return ASIM_OK;
+}
+
+asim_status asim_set_path(asim_ctx* ctx, int32_t path) {
+  if (!ctx) return ASIM_EINVAL;
+  if (path < 0 || path > 2) return asim_fail(ctx, ASIM_EINVAL, "path must be 0, 1 or 2");
+  ctx->force_path = path;
+  return ASIM_OK;
+}
+
+asim_status asim_set_chunk_size(asim_ctx* ctx, int64_t min_requests) {
+  if (!ctx) return ASIM_EINVAL;
+  if (min_requests < 1) return asim_fail(ctx, ASIM_ERANGE, "min_requests must be >= 1");
+  ctx->min_chunk = min_requests;
   return ASIM_OK;
 }
 
@@ -303,6 +347,7 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->sim_ms = ctx->sim_ms;
   out->stage_updates = (int64_t)upd;
   out->request_evals = ctx->request_evals;
+  out->chunk_reruns = ctx->chunk_reruns;
   return ASIM_OK;
 }
 

@@ -67,6 +67,14 @@ struct asim_ctx {
   int64_t request_evals = 0;
   DBuf d_counter;  // unsigned long long stage-update counter
 
+  int sms = 148;
+  int64_t chunk_reruns = 0;
+  // chunked path buffers (chunked.cpp)
+  DBuf c_items, c_begin, c_spec_good, c_spec_sum, c_fix_good, c_fix_sum, c_spec_end, c_fix_end,
+      c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_units;
+  int32_t force_path = 0;  // 0 auto, 1 general kernel, 2 chunked kernel (tests)
+  int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
+
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;
   DBuf d_good, d_sum, d_pm, d_argmax;
@@ -105,6 +113,7 @@ cudaError_t upload(DBuf& buf, const std::vector<T>& v, cudaStream_t st) {
 }
 
 // Batch encoding shared by evaluate, evaluate_deltas and the search.
+struct HostBatch;
 struct HostBatch {
   int32_t G = 0;
   std::vector<int32_t> base_cfg;   // [B][G]
@@ -117,3 +126,7 @@ struct HostBatch {
 // good/sum/per-model at out (device pointers, indexed by candidate).
 asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                            const asim::DevOut& out, cudaStream_t st);
+
+bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out);
+asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
+                             const asim::DevOut& out, cudaStream_t st);

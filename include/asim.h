@@ -105,7 +105,8 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);
 asim_status asim_reset_stats(asim_ctx* ctx);
 /* Kernel selection (testing): 0 = automatic (default), 1 = general
  * lane-per-candidate kernel over the whole trace, 2 = chunked kernel with
- * speculative time chunks and exact fix-up whenever the batch allows it.
+ * speculative time chunks and exact fix-up whenever the batch allows it,
+ * 3 = as 2 with int64 absolute times forced.
  * Results are identical for every choice. */
 asim_status asim_set_path(asim_ctx* ctx, int32_t path);
 /* Minimum time-chunk length in requests for the chunked kernel (default

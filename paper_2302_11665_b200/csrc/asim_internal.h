@@ -101,6 +101,7 @@ struct ChunkParams {
   void* fix_end;
   int64_t* fix_epoch;
   uint8_t* fix_flag;           // [J][items] 1 = not coalesced within the chunk
+  unsigned long long* stage_updates;  // nullable statistics counter
 };
 
 cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStream_t st, int sms,

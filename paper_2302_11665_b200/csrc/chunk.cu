@@ -192,12 +192,14 @@ __device__ __forceinline__ void commit(const ChunkParams& P, const WarpMem<T>& w
 // index on ties), admission at receipt, commit.  Returns latency or -1.
 template <typename T, int S>
 __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& w, T* st, int lane,
-                                        uint64_t mask, int m, T ar, const T* dv, T tl, T sl) {
+                                        uint64_t mask, int m, T ar, const T* dv, T tl, T sl,
+                                        unsigned long long& upd) {
   T best_f = TT<T>::maxv();
   int best_g = -1;
   while (mask) {  // ascending g, strict '<': lowest index wins ties (C1)
     const int g = __ffsll((long long)mask) - 1;
     mask &= mask - 1;
+    if (S > 0) upd += S; else upd += (w.gt[g] >> 24);
     const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
     if (f < best_f) {
       best_f = f;
@@ -255,6 +257,7 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
   __syncwarp();
 
   int64_t good0 = 0, sum0 = 0, good1 = 0, sum1 = 0;
+  unsigned long long upd = 0;
   bool coalesced = false;
   T dv[S > 0 ? S : 1];
   for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
@@ -266,7 +269,9 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
       const int m = __shfl_sync(FULL, mi, jj);
       if constexpr (TT<T>::kRel) {
         if (a - E > P.theta) {  // warp-uniform epoch move (exact, see header)
-          const T delta = (T)(a - E);
+          // every stored value is < 2^32 - 1, so a longer gap clears them all
+          const int64_t gap = a - E;
+          const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
           rebase<T>(w.st0, slots, lane, delta);
           if constexpr (DUAL) rebase<T>(w.st1, slots, lane, delta);
           E = a;
@@ -294,13 +299,13 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
         tl = w.tail[m];
       }
       const T sl = w.slo[m];
-      const int64_t l0 = step<T, S>(P, w, w.st0, lane, mask, m, ar, dv, tl, sl);
+      const int64_t l0 = step<T, S>(P, w, w.st0, lane, mask, m, ar, dv, tl, sl, upd);
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
       }
       if constexpr (DUAL) {
-        const int64_t l1 = step<T, S>(P, w, w.st1, lane, mask, m, ar, dv, tl, sl);
+        const int64_t l1 = step<T, S>(P, w, w.st1, lane, mask, m, ar, dv, tl, sl, upd);
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;
@@ -310,6 +315,10 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
     if (DUAL && coalesced) break;
   }
 
+  if (P.stage_updates) {
+    for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(FULL, upd, o);
+    if (lane == 0) atomicAdd(P.stage_updates, upd);
+  }
   const int64_t unit = (int64_t)j * P.num_items + item;
   if constexpr (!DUAL) {
     P.spec_good[(int64_t)j * P.num_items * 32 + slot_id] = (int32_t)good0;

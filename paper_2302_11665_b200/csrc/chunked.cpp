@@ -84,7 +84,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   if (N == 0) J = 1;
   std::vector<int64_t> cb(J + 1);
   for (int64_t j = 0; j <= J; ++j) cb[j] = N * j / J;
-  const int64_t theta = theta_for(ctx);
+  const int64_t theta = ctx->force_path == 3 ? -1 : theta_for(ctx);
   const bool u32 = theta > 0;
   const size_t tsz = u32 ? 4 : 8;
 
@@ -132,6 +132,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.fix_end = ctx->c_fix_end.p;
   P.fix_epoch = ctx->c_fix_epoch.as<int64_t>();
   P.fix_flag = ctx->c_flag.as<uint8_t>();
+  P.stage_updates = out.stage_updates;
 
   // ---- pass 1: every (item, chunk) from the idle state
   P.num_units = (int32_t)(J * I);

@@ -155,9 +155,9 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
   // counts -> chunked kernel (chunk.cu); otherwise the general kernel below.
   const bool shared_bases = (int64_t)(hb.base_cfg.size() / std::max<int32_t>(hb.G, 1)) < C ||
                             hb.G == 0;
-  bool chunked = ctx->force_path == 2 ||
+  bool chunked = ctx->force_path >= 2 ||
                  (ctx->force_path == 0 && shared_bases && asim_chunked_eligible(ctx, hb, out));
-  if (ctx->force_path == 2 && !asim_chunked_eligible(ctx, hb, out)) chunked = false;
+  if (ctx->force_path >= 2 && !asim_chunked_eligible(ctx, hb, out)) chunked = false;
   if (chunked) {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (ctx->profiling) {
@@ -165,7 +165,9 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
         return asim_cuda(ctx, cudaGetLastError(), "event create");
       cudaEventRecord(ev0, st);
     }
-    asim_status s = asim_run_chunked(ctx, hb, begin, end, out, st);
+    asim::DevOut o2 = out;
+    o2.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
+    asim_status s = asim_run_chunked(ctx, hb, begin, end, o2, st);
     if (ctx->profiling) {
       cudaEventRecord(ev1, st);
       ctx->events.emplace_back(ev0, ev1);
@@ -300,7 +302,7 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
 
 asim_status asim_set_path(asim_ctx* ctx, int32_t path) {
   if (!ctx) return ASIM_EINVAL;
-  if (path < 0 || path > 2) return asim_fail(ctx, ASIM_EINVAL, "path must be 0, 1 or 2");
+  if (path < 0 || path > 3) return asim_fail(ctx, ASIM_EINVAL, "path must be 0..3");
   ctx->force_path = path;
   return ASIM_OK;
 }

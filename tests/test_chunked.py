@@ -166,3 +166,17 @@ def test_search_same_on_both_paths(sim):
     sim.set_chunk_size(4096)
     vals = list(res.values())
     assert all(v == vals[0] for v in vals)
+
+
+@pytest.mark.parametrize("scale", [1.0, 2.0, 5.0])
+def test_epoch_rebase_long_gaps(sim, scale):
+    """uint32 epochs with gaps longer than 2^32 - theta (sparse, bursty
+    arrivals): the epoch move must clear every stored free time."""
+    prob = configs.motivating_problem(slo_scale=scale)
+    rng = np.random.default_rng(int(scale * 10))
+    gaps = rng.gamma(1 / 16.0, 16.0 * 1.2e9, size=4000)  # mean 1.2 s, CV 4
+    a = np.floor(np.cumsum(gaps)).astype(np.int64)
+    tr = Trace(a, rng.integers(0, 2, size=4000).astype(np.int32))
+    bases = [Placement.from_lists([0, 0], [[0], [1]], 2), Placement.from_lists([2], [[0]], 2),
+             Placement.from_lists([1], [[1]], 2)]
+    _check(sim, prob, tr, bases, rng, chunk_sizes=(37, 4096), per_base=12)

@@ -102,7 +102,23 @@ struct ChunkParams {
   int64_t* fix_epoch;
   uint8_t* fix_flag;           // [J][items] 1 = not coalesced within the chunk
   unsigned long long* stage_updates;  // nullable statistics counter
+  // Speculation source (nullable = idle): absolute int64 free times of the
+  // base placement's TRUE trajectory at every chunk boundary,
+  // spec_state[(spec_row[b] * J + j) * slots_max + k].  Any start state is
+  // exact (the fix-up corrects it); the base's own trajectory is the one the
+  // candidates (base + one replica) stay closest to.
+  const int64_t* spec_state;
+  const int32_t* spec_row;     // [B] row of base b in spec_state
+  int32_t state_stride;        // slots per boundary row of spec_state / published states
 };
+
+// Publish the true state at every chunk boundary of lane 0 of each item:
+// out[(out_row[item] * J + j) * state_stride + k] (absolute int64),
+// j = 0 is the idle state.  end_src[j * I + i] = 0 if the true end of chunk
+// j is spec_end, 1 if fix_end.
+cudaError_t launch_publish_states(const ChunkParams& P, const uint8_t* end_src, bool u32,
+                                  const int32_t* out_row, int64_t* out, cudaStream_t st,
+                                  int64_t* launches);
 
 cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStream_t st, int sms,
                               int64_t* launches);

@@ -235,11 +235,26 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
   const int slots = it.slots;
   const int64_t slot_id = (int64_t)item * 32 + lane;
 
-  // initial state and epoch
+  // initial state and epoch.  The speculative trajectory starts from the
+  // base's true boundary state (or idle); the fix-up's true trajectory from
+  // the previous chunk's true end state.
   int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
-  for (int k = 0; k < slots; ++k) w.st0[k * 32 + lane] = (T)0;
+  T* spec_st = DUAL ? w.st1 : w.st0;
+  if (P.spec_state != nullptr && j > 0) {
+    const int64_t* ss = P.spec_state + ((int64_t)P.spec_row[it.base] * P.J + j) * P.state_stride;
+    for (int k = 0; k < slots; ++k) {
+      const int64_t v = ss[k];
+      if constexpr (TT<T>::kRel) {
+        const int64_t r = v - E;
+        spec_st[k * 32 + lane] = r > 0 ? (T)r : (T)0;
+      } else {
+        spec_st[k * 32 + lane] = (T)v;
+      }
+    }
+  } else {
+    for (int k = 0; k < slots; ++k) spec_st[k * 32 + lane] = (T)0;
+  }
   if constexpr (DUAL) {
-    for (int k = 0; k < slots; ++k) w.st1[k * 32 + lane] = (T)0;
     const int64_t prev = (int64_t)(j - 1) * P.num_items + item;
     const T* src_st = reinterpret_cast<const T*>(src ? P.fix_end : P.spec_end) +
                       prev * P.slots_max * 32;
@@ -402,6 +417,30 @@ __global__ void chunk_reduce_kernel(ChunkParams P, DevOut out) {
   if (out.sum_latency) out.sum_latency[c - out.out_offset] = ok ? s : 0;
 }
 
+template <typename T>
+__global__ void publish_kernel(ChunkParams P, const uint8_t* __restrict__ end_src,
+                               const int32_t* __restrict__ out_row, int64_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)P.num_items * P.J * P.state_stride;
+  if (t >= total) return;
+  const int k = (int)(t % P.state_stride);
+  const int j = (int)((t / P.state_stride) % P.J);
+  const int item = (int)(t / ((int64_t)P.state_stride * P.J));
+  int64_t v = 0;  // j == 0: idle; slots beyond the item's: unused
+  if (j > 0 && k < P.items[item].slots) {
+    const int64_t u = (int64_t)(j - 1) * P.num_items + item;  // end of chunk j-1
+    const bool fix = end_src[u] != 0;
+    const T* st = reinterpret_cast<const T*>(fix ? P.fix_end : P.spec_end) + u * P.slots_max * 32;
+    const T x = st[k * 32 + 0];  // lane 0 of the item
+    if constexpr (TT<T>::kRel) {
+      v = (fix ? P.fix_epoch : P.spec_epoch)[u] + (int64_t)x;
+    } else {
+      v = (int64_t)x;
+    }
+  }
+  out[((int64_t)out_row[item] * P.J + j) * P.state_stride + k] = v;
+}
+
 template <typename T, bool DUAL>
 cudaError_t launch_t(const ChunkParams& P, cudaStream_t st, int sms) {
   const size_t per_warp = (size_t)P.slots_max * 32 * sizeof(T) * (DUAL ? 2 : 1) +
@@ -437,6 +476,20 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
     e = dual ? launch_t<int64_t, true>(P, st, sms) : launch_t<int64_t, false>(P, st, sms);
   if (launches) ++*launches;
   return e;
+}
+
+cudaError_t launch_publish_states(const ChunkParams& P, const uint8_t* end_src, bool u32,
+                                  const int32_t* out_row, int64_t* out, cudaStream_t st,
+                                  int64_t* launches) {
+  const int64_t total = (int64_t)P.num_items * P.J * P.state_stride;
+  if (total == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  if (u32)
+    publish_kernel<uint32_t><<<blocks, 256, 0, st>>>(P, end_src, out_row, out);
+  else
+    publish_kernel<int64_t><<<blocks, 256, 0, st>>>(P, end_src, out_row, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,

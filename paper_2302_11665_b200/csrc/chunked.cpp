@@ -36,7 +36,7 @@ static int64_t theta_for(const asim_ctx* ctx) {
 }
 
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
-                             const asim::DevOut& out, cudaStream_t st) {
+                             const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
   const int64_t N = ctx->n;
   const HostProblem& hp = ctx->hp;
   // ---- work items: <= 32 consecutive candidates of one base
@@ -82,6 +82,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   J = std::min<int64_t>(J, std::max<int64_t>(1, N / std::max<int64_t>(1, ctx->min_chunk)));
   J = std::max<int64_t>(1, std::min<int64_t>(J, 1 << 16));
   if (N == 0) J = 1;
+  if (opt && opt->J > 0) J = opt->J;  // the search keeps one chunking for all its steps
   std::vector<int64_t> cb(J + 1);
   for (int64_t j = 0; j <= J; ++j) cb[j] = N * j / J;
   const int64_t theta = ctx->force_path == 3 ? -1 : theta_for(ctx);
@@ -133,6 +134,11 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.fix_epoch = ctx->c_fix_epoch.as<int64_t>();
   P.fix_flag = ctx->c_flag.as<uint8_t>();
   P.stage_updates = out.stage_updates;
+  P.spec_state = opt ? opt->spec_state : nullptr;
+  P.spec_row = opt ? opt->spec_row : nullptr;
+  P.state_stride = (opt && opt->state_stride > 0) ? opt->state_stride : slots_max;
+  if (P.spec_state && P.state_stride < slots_max)
+    return asim_fail(ctx, ASIM_ERANGE, "internal: state stride below slots");
 
   // ---- pass 1: every (item, chunk) from the idle state
   P.num_units = (int32_t)(J * I);
@@ -140,6 +146,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
 
+  std::vector<uint8_t> end_src(J * I, 0);
   if (J > 1) {
     // ---- pass 2: fix-up of every chunk j >= 1 from chunk j-1's speculative end
     std::vector<asim::ChunkUnit> units;
@@ -158,6 +165,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     std::vector<uint8_t> computed_src(J * I, 0);  // start source used by unit (item, j)
     std::vector<int32_t> pos(I, 1);
     std::vector<uint8_t> prev_src(I, 0);
+    end_src.assign(J * I, 0);  // chunk 0 is exact: its true end is spec_end
     for (;;) {
       e = cudaMemcpyAsync(flag.data(), P.fix_flag, J * I, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -168,6 +176,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
           const int64_t u = (int64_t)pos[i] * I + i;
           if (computed_src[u] == prev_src[i]) {
             prev_src[i] = flag[u] ? 1 : 0;
+            end_src[u] = prev_src[i];
             ++pos[i];
           } else {
             redo.push_back(asim::ChunkUnit{i, pos[i], 1, 0});
@@ -186,5 +195,13 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     }
   }
   e = asim::launch_chunk_reduce(P, out, st, &ctx->launches);
-  return asim_cuda(ctx, e, "chunk reduce");
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk reduce");
+  if (opt && opt->publish_out) {  // true boundary states of lane 0 of every item
+    e = upload(ctx->c_end_src, end_src, st);
+    if (e == cudaSuccess)
+      e = asim::launch_publish_states(P, ctx->c_end_src.as<uint8_t>(), u32, opt->publish_row,
+                                      opt->publish_out, st, &ctx->launches);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "publish states");
+  }
+  return ASIM_OK;
 }

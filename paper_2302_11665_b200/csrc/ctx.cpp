@@ -140,7 +140,7 @@ asim_status asim_ready(asim_ctx* ctx) {
 }
 
 asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
-                           const asim::DevOut& out, cudaStream_t st) {
+                           const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
   const int64_t C = (int64_t)hb.cand_base.size();
   if (end <= begin) return ASIM_OK;
   if (begin < 0 || end > C) return asim_fail(ctx, ASIM_ERANGE, "candidate range");
@@ -167,7 +167,7 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
     }
     asim::DevOut o2 = out;
     o2.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
-    asim_status s = asim_run_chunked(ctx, hb, begin, end, o2, st);
+    asim_status s = asim_run_chunked(ctx, hb, begin, end, o2, st, opt);
     if (ctx->profiling) {
       cudaEventRecord(ev1, st);
       ctx->events.emplace_back(ev0, ev1);
@@ -267,7 +267,7 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->d_argmax, &ctx->d_counter, &ctx->c_items, &ctx->c_begin,
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
-                    &ctx->c_flag, &ctx->c_counter, &ctx->c_units};
+                    &ctx->c_flag, &ctx->c_counter, &ctx->c_units, &ctx->c_end_src};
     for (DBuf* b : bufs) b->release();
   }
   delete ctx;

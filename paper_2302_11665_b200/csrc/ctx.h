@@ -71,7 +71,7 @@ struct asim_ctx {
   int64_t chunk_reruns = 0;
   // chunked path buffers (chunked.cpp)
   DBuf c_items, c_begin, c_spec_good, c_spec_sum, c_fix_good, c_fix_sum, c_spec_end, c_fix_end,
-      c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_units;
+      c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_units, c_end_src;
   int32_t force_path = 0;  // 0 auto, 1 general kernel, 2 chunked kernel (tests)
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
 
@@ -124,9 +124,21 @@ struct HostBatch {
 };
 // Upload a batch and launch the simulation of candidates [0, C) writing
 // good/sum/per-model at out (device pointers, indexed by candidate).
+struct ChunkOptions;
 asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
-                           const asim::DevOut& out, cudaStream_t st);
+                           const asim::DevOut& out, cudaStream_t st,
+                           const ChunkOptions* opt = nullptr);
 
+// Options of the chunked path used by the search (all optional).
+struct ChunkOptions {
+  int64_t J = 0;                         // fixed chunk count (0 = automatic)
+  const int64_t* spec_state = nullptr;   // speculation source (device), see ChunkParams
+  const int32_t* spec_row = nullptr;     // [B] device
+  int32_t state_stride = 0;
+  int64_t* publish_out = nullptr;        // true boundary states of lane 0 of each item
+  const int32_t* publish_row = nullptr;  // [items] device
+};
 bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out);
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
-                             const asim::DevOut& out, cudaStream_t st);
+                             const asim::DevOut& out, cudaStream_t st,
+                             const ChunkOptions* opt = nullptr);

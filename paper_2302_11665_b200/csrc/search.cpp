@@ -56,6 +56,14 @@ struct asim_search {
   std::vector<int64_t> seg;       // [bases + 1] candidate offsets per base
   DBuf d_good_all;
   std::vector<int64_t> h_good;
+  // Speculation from the base placement's true trajectory (chunk.cu): per run
+  // the absolute free times at every chunk boundary of the current base.
+  bool use_states = false;
+  int64_t J = 1;
+  int32_t stride = 1;       // slots per boundary row
+  DBuf state_prev, state_cur, d_rows, d_base_good;
+  bool base_ready = false;
+  HostBatch hb_base;        // one candidate per base: the base itself
   // statistics
   int64_t steps = 0, candidates = 0, evaluated = 0;
 };
@@ -122,6 +130,28 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     s->G = std::max(s->G, r.G);
     s->runs.push_back(std::move(r));
   }
+  // one chunking for the whole search; rows of idle boundary states per run
+  int32_t stride = 1;
+  for (auto& cfg : groups) {
+    int32_t sl = 0;
+    for (int32_t c : cfg) sl += hp.cfg_stages[c];
+    stride = std::max(stride, sl);
+  }
+  s->stride = stride;
+  s->J = std::max<int64_t>(1, std::min<int64_t>(1024, ctx->n / std::max<int64_t>(1, ctx->min_chunk)));
+  s->use_states = ctx->force_path != 1;  // the general kernel has no time chunks
+  if (s->use_states && !s->runs.empty()) {
+    const size_t bytes = s->runs.size() * (size_t)s->J * stride * 8;
+    cudaError_t e = s->state_prev.ensure(bytes);
+    if (e == cudaSuccess) e = s->state_cur.ensure(bytes);
+    if (e == cudaSuccess) e = cudaMemset(s->state_prev.p, 0, bytes);
+    if (e == cudaSuccess) e = cudaMemset(s->state_cur.p, 0, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      asim_search_destroy(s);
+      return asim_cuda(ctx, e, "search state buffers");
+    }
+  }
   *out = s;
   return ASIM_OK;
 }
@@ -129,6 +159,10 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
 void asim_search_destroy(asim_search* s) {
   if (!s) return;
   s->d_good_all.release();
+  s->state_prev.release();
+  s->state_cur.release();
+  s->d_rows.release();
+  s->d_base_good.release();
   delete s;
 }
 
@@ -188,6 +222,19 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
     hb.slots = std::max(hb.slots, slots);
     s->seg.push_back((int64_t)hb.cand_base.size());
   }
+  // the bases themselves (true boundary states for speculation)
+  s->base_ready = false;
+  s->hb_base = HostBatch();
+  s->hb_base.G = G;
+  s->hb_base.base_cfg = hb.base_cfg;
+  s->hb_base.base_mask = hb.base_mask;
+  s->hb_base.slots = hb.slots;
+  for (int32_t b = 0; b < (int32_t)s->base_run.size(); ++b) {
+    s->hb_base.cand_base.push_back(b);
+    s->hb_base.cand_model.push_back(-1);
+    s->hb_base.cand_group.push_back(0);
+    s->hb_base.cand_ok.push_back(1);
+  }
   s->prepared = true;
   *num_candidates = (int64_t)hb.cand_base.size();
   if (*num_candidates == 0) s->prepared = false;  // search finished
@@ -208,14 +255,50 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
   int prev = -1;
   cudaGetDevice(&prev);
   if (prev != s->ctx->device) cudaSetDevice(s->ctx->device);
+  cudaStream_t strm = static_cast<cudaStream_t>(cuda_stream);
+  asim_status st = ASIM_OK;
+  ChunkOptions opt;
+  ChunkOptions* popt = nullptr;
+  asim::DevOut probe{};
+  if (s->use_states && asim_chunked_eligible(s->ctx, s->hb, probe)) {
+    const int32_t B = (int32_t)s->base_run.size();
+    opt.J = s->J;
+    opt.state_stride = s->stride;
+    if (!s->base_ready) {
+      // true boundary states of every base: simulate each base (one lane)
+      // speculating from the previous base's states, publish into state_cur
+      cudaError_t e = upload(s->d_rows, s->base_run, strm);
+      if (e == cudaSuccess) e = s->d_base_good.ensure(B * 8 + 8);
+      if (e != cudaSuccess) {
+        if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
+        return asim_cuda(s->ctx, e, "base pass buffers");
+      }
+      ChunkOptions ob = opt;
+      ob.spec_state = s->state_prev.as<int64_t>();
+      ob.spec_row = s->d_rows.as<int32_t>();
+      ob.publish_out = s->state_cur.as<int64_t>();
+      ob.publish_row = s->d_rows.as<int32_t>();
+      asim::DevOut bo{};
+      bo.good = s->d_base_good.as<int64_t>();
+      bo.out_offset = 0;
+      st = asim_run_chunked(s->ctx, s->hb_base, 0, B, bo, strm, &ob);
+      if (st) {
+        if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
+        return st;
+      }
+      s->base_ready = true;
+    }
+    opt.spec_state = s->state_cur.as<int64_t>();
+    opt.spec_row = s->d_rows.as<int32_t>();
+    popt = &opt;
+  }
   asim::DevOut out;
   out.good = good_dev;
   out.sum_latency = nullptr;
   out.good_per_model = nullptr;
   out.out_offset = begin;
   out.stage_updates = nullptr;
-  asim_status st = asim_run_batch(s->ctx, s->hb, begin, end, out,
-                                  static_cast<cudaStream_t>(cuda_stream));
+  st = asim_run_batch(s->ctx, s->hb, begin, end, out, strm, popt);
   if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
   return st;
 }
@@ -249,6 +332,7 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
       run.best = run.sel;
     }
   }
+  if (s->base_ready) std::swap(s->state_prev, s->state_cur);  // next step speculates from it
   s->prepared = false;
   return ASIM_OK;
 }

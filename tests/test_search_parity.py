@@ -63,3 +63,17 @@ def test_search_s4_shaped(sim):
     prob, tr = configs.s4(duration=1800.0)
     ref = _compare(sim, prob, tr)
     assert ref["good"] > 0
+
+
+@pytest.mark.parametrize("chunk", [40, 257])
+def test_search_small_chunks_base_speculation(sim, chunk):
+    """Many time chunks per step: candidates speculate from the base
+    placement's true boundary states (search.cpp); still oracle-exact."""
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "MoE-5.3B") for i in range(2)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=3.0)
+    tr = traces.maf2_shaped(11, len(names), 12.0, 900.0)
+    sim.set_chunk_size(chunk)
+    try:
+        _compare(sim, prob, tr)
+    finally:
+        sim.set_chunk_size(4096)

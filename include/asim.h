@@ -98,7 +98,7 @@ typedef struct {
   double sim_ms;
   int64_t stage_updates;
   int64_t request_evals;
-  int64_t chunk_reruns;  /* fix-up re-runs of chunks whose trajectories never met */
+  int64_t chunk_reruns;  /* chunks re-simulated because their start state was wrong */
 } asim_stats;
 asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
 asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);

@@ -74,10 +74,6 @@ struct ItemDesc {
   int32_t pad;
 };
 
-struct ChunkUnit {  // fix-up work unit
-  int32_t item, chunk, src;  // src: start state from 0 = spec_end, 1 = fix_end of chunk-1
-  int32_t pad;
-};
 
 struct ChunkParams {
   DevProblem pr;
@@ -90,7 +86,6 @@ struct ChunkParams {
   int64_t theta;               // uint32 epoch threshold (see chunk.cu)
   int32_t slots_max;
   int32_t num_units;
-  const ChunkUnit* units;      // fix-up passes only
   uint32_t* counter;           // dynamic work counter
   int32_t* spec_good;          // [J][items*32]
   int64_t* spec_sum;
@@ -110,6 +105,7 @@ struct ChunkParams {
   const int64_t* spec_state;
   const int32_t* spec_row;     // [B] row of base b in spec_state
   int32_t state_stride;        // slots per boundary row of spec_state / published states
+  unsigned long long* walked;  // nullable statistics: chunks re-simulated by the walk pass
 };
 
 // Publish the true state at every chunk boundary of lane 0 of each item:
@@ -124,5 +120,10 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
                               int64_t* launches);
 cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
                                 int64_t* launches);
+// Pass 3: per item, re-simulate the chunks whose start state was wrong and
+// record for every (j, item) whether chunk j's true end is spec_end (0) or
+// fix_end (1) in end_src[j * items + item].
+cudaError_t launch_chunk_walk(const ChunkParams& P, uint8_t* end_src, bool u32, cudaStream_t st,
+                              int sms, int64_t* launches);
 
 }  // namespace asim

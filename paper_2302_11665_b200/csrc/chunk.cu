@@ -2,39 +2,46 @@
 // lane-per-candidate over (item, time-chunk) work units with exact
 // speculative-chunk fix-up.
 //
-//   pass 1 (spec)   every unit (32 candidates of one base placement x one
-//                   chunk of the trace) is simulated from the idle state;
-//                   per-lane counts and the end state are stored.
-//   pass 2 (fix)    for chunk j >= 1 the TRUE trajectory (started from the
-//                   true end state of chunk j-1) and the SPECULATIVE one
-//                   (started idle) are run in lockstep until every lane's
-//                   states are equivalent -- for every stage slot k,
-//                   max(true_k, a) == max(spec_k, a) at the next arrival a
-//                   (a free time earlier than the arrival acts exactly like
-//                   the arrival, since every later stage start is >= it).
-//                   From there on both trajectories take identical decisions,
-//                   so the difference of their counts is the exact correction.
-//                   A unit whose trajectories never meet runs to the chunk
-//                   end and publishes its true end state; the host re-runs
-//                   the next chunk from it (rare chains; exact in all cases).
+//   pass 1 (SPEC)   every unit (<= 32 candidates sharing one base placement x
+//                   one chunk of the trace) is simulated from a speculative
+//                   start state: the base placement's true state at the chunk
+//                   boundary when the search provides it, else idle.  Counts
+//                   and the end state are stored.
+//   pass 2 (DUAL)   for chunk j >= 1 the TRUE trajectory (from chunk j-1's
+//                   speculative end, assumed true) and the SPECULATIVE one are
+//                   run in lockstep until every lane's states are equivalent:
+//                   for every stage slot k, max(true_k, a) == max(spec_k, a) at
+//                   the next arrival a (a free time earlier than an arrival acts
+//                   exactly like it, since every later stage start is >= it).
+//                   From there both trajectories take identical decisions, so
+//                   the difference of their counts is the exact correction.  A
+//                   unit whose trajectories never meet runs to the chunk end
+//                   and publishes its true end state.
+//   pass 3 (WALK)   one warp per item scans its chunks in order; wherever a
+//                   chunk's start state turned out wrong (the previous chunk
+//                   never met its speculation) it re-simulates that chunk from
+//                   the true start, single trajectory, until the true end state
+//                   is again equivalent to the stored speculative one.  Exact in
+//                   every case; the walked length is the inherently sequential
+//                   part (sustained overload never forgets its start state).
 //
 // Time representation (template T):
 //   int64_t   absolute nanoseconds (any SLO).
 //   uint32_t  nanoseconds relative to a warp-uniform epoch E <= arrival.
-//             Free times are stored as max(free - E, 0): a free time below
-//             the current arrival is equivalent to the arrival, so clamping
-//             at the epoch is exact.  E is moved to the current arrival a
-//             whenever a - E > theta = 2^32 - 1 - max_slo - max_service,
+//             Free times are stored as max(free - E, 0): clamping at the epoch
+//             is exact by the same equivalence.  E moves to the current arrival
+//             a whenever a - E > theta = 2^32 - 1 - max_slo - max_service,
 //             which keeps every stored or predicted value below 2^32
 //             (accepted finishes are <= a + slo; predictions add at most
-//             max_service to a stored value).  Chosen by the host only when
-//             theta is positive.
+//             max_service to a stored value).  Chosen only when theta > 0.1 s.
 //
 // Per request (§4.3; C1-C6), exactly as sim.cu:
 //   f_g = pipeline recurrence on group g's free times; g* = argmin (f_g, g);
 //   accept iff f_g* - a <= slo[m]; on accept store the stage departures.
-// State lives in shared memory as [slot][lane]; all per-model tables of the
-// unit's base placement are staged in shared memory per warp.
+// State lives in shared memory as [slot][lane]; the unit's per-model tables
+// (hosting masks, stage latencies of the base's uniform config, tail, SLO,
+// relevance flags) are staged in shared memory per warp.  Requests whose
+// model no lane hosts are skipped 32 at a time with one ballot.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,9 +51,10 @@ namespace asim {
 namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr int kWarps = 4;  // warps per block; each warp takes units independently
-constexpr int kSTab = 16;  // stage entries per model in the uniform-config table
+constexpr int kWarps = 4;        // warps per block; each warp takes units independently
+constexpr int kSTab = 16;        // stage entries per model in the uniform-config table
 constexpr int kCheckEvery = 64;  // coalescence test period (requests) in the fix-up
+enum Mode { SPEC = 0, DUAL = 1, WALK = 2 };
 
 template <typename T>
 struct TT;
@@ -73,20 +81,19 @@ __device__ __forceinline__ T tmax(T a, T b) {
 // Per-warp shared-memory region.
 template <typename T>
 struct WarpMem {
-  T* st0;          // [slots][32] true / speculative trajectory
-  T* st1;          // [slots][32] speculative trajectory (fix-up only)
+  T* st0;          // [slots][32] speculative (SPEC) / true (DUAL, WALK) trajectory
+  T* st1;          // [slots][32] speculative trajectory (DUAL only)
   uint64_t* mask;  // [M]   hosting groups of model m in the base placement
   T* d;            // [M][kSTab] stage latencies under the base's uniform config
   T* tail;         // [M]
   T* slo;          // [M]   (clipped to T's range: exact, see header)
-  uint32_t* gt;    // [64]  dynamic-config group table: cfg | off<<16 | s<<24
+  uint32_t* gt;    // [64]  group table: cfg | off<<16 | s<<24
+  uint8_t* rel;    // [M]   some lane of the unit hosts model m
 };
 
-template <typename T>
-__device__ __forceinline__ size_t warp_bytes(const ChunkParams& P, bool dual) {
-  const size_t slots = (size_t)P.slots_max;
-  size_t b = slots * 32 * sizeof(T) * (dual ? 2 : 1);
-  b += (size_t)P.pr.M * (8 + sizeof(T) * (kSTab + 2)) + 64 * 4;
+__host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, bool dual) {
+  size_t b = (size_t)slots_max * 32 * tsz * (dual ? 2 : 1);
+  b += (size_t)M * (8 + tsz * (kSTab + 2)) + 64 * 4 + ((M + 15) & ~15);
   return (b + 15) & ~size_t(15);
 }
 
@@ -108,6 +115,7 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   w.slo = q;
   q += P.pr.M;
   w.gt = reinterpret_cast<uint32_t*>(q);
+  w.rel = reinterpret_cast<uint8_t*>(w.gt + 64);
   return w;
 }
 
@@ -121,11 +129,12 @@ __device__ void load_base(const ChunkParams& P, const ItemDesc& it, WarpMem<T>& 
     w.slo[m] = TT<T>::clip(P.pr.slo[m]);
     if (it.cfg >= 0) {
       const int64_t* d = P.pr.stage + ((int64_t)m * PP + it.cfg) * SS;
-      for (int k = 0; k < kSTab; ++k) w.d[m * kSTab + k] = (k < SS && k < it.stages) ? (T)d[k] : (T)0;
+      for (int k = 0; k < kSTab; ++k)
+        w.d[m * kSTab + k] = (k < SS && k < it.stages) ? (T)d[k] : (T)0;
       w.tail[m] = (T)P.pr.tail[(int64_t)m * PP + it.cfg];
     }
   }
-  if (lane == 0) {  // group table (also used by the dynamic-config path)
+  if (lane == 0) {
     int off = 0;
     for (int g = 0; g < 64; ++g) {
       uint32_t e = 0xFFFFFFFFu;
@@ -143,9 +152,8 @@ __device__ void load_base(const ChunkParams& P, const ItemDesc& it, WarpMem<T>& 
   __syncwarp();
 }
 
-// Predicted finish of the request (relative arrival ar) on group g of this
-// lane's trajectory `st`; S > 0: uniform config with S stages (slot = g*S+k);
-// S == 0: dynamic (group table + global stage table).
+// Predicted finish on group g of trajectory `st`; S > 0: uniform config with
+// S stages (slot = g*S + k); S == 0: group table + global stage table.
 template <typename T, int S>
 __device__ __forceinline__ T predict(const ChunkParams& P, const WarpMem<T>& w, const T* st,
                                      int lane, int g, int m, T ar, const T* dv, T tl) {
@@ -199,7 +207,8 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
   while (mask) {  // ascending g, strict '<': lowest index wins ties (C1)
     const int g = __ffsll((long long)mask) - 1;
     mask &= mask - 1;
-    if (S > 0) upd += S; else upd += (w.gt[g] >> 24);
+    if (S > 0) upd += S;
+    else upd += (w.gt[g] >> 24);
     const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
     if (f < best_f) {
       best_f = f;
@@ -221,9 +230,41 @@ __device__ __forceinline__ void rebase(T* st, int slots, int lane, T delta) {
   }
 }
 
-// Simulate one unit.  DUAL = fix-up (st0 = true trajectory, st1 = speculative).
-template <typename T, int S, bool DUAL>
-__device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it, int item, int j,
+// Move the epoch to arrival a if a - E > theta (uint32 only; warp-uniform).
+template <typename T, int MODE>
+__device__ __forceinline__ void maybe_rebase(const ChunkParams& P, WarpMem<T>& w, int slots,
+                                             int lane, int64_t a, int64_t& E) {
+  if constexpr (TT<T>::kRel) {
+    if (a - E > P.theta) {
+      // every stored value is < 2^32 - 1, so a longer gap clears them all
+      const int64_t gap = a - E;
+      const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+      rebase<T>(w.st0, slots, lane, delta);
+      if constexpr (MODE == DUAL) rebase<T>(w.st1, slots, lane, delta);
+      E = a;
+    }
+  }
+}
+
+// Load a stored state (relative to epoch Ep, or absolute) into `dst` at epoch E.
+template <typename T>
+__device__ __forceinline__ void load_state(T* dst, const T* src, int64_t Ep, int64_t E, int slots,
+                                           int lane) {
+  for (int k = 0; k < slots; ++k) {
+    const T v = src[k * 32 + lane];
+    if constexpr (TT<T>::kRel) {
+      const int64_t r = (int64_t)v - (E - Ep);
+      dst[k * 32 + lane] = r > 0 ? (T)r : (T)0;
+    } else {
+      dst[k * 32 + lane] = v;
+    }
+  }
+}
+
+// Simulate one unit (item, chunk j) in MODE.  Returns (WALK) whether the true
+// end state is equivalent to the stored speculative end state of chunk j.
+template <typename T, int S, int MODE>
+__device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it, int item, int j,
                          int lane, int src) {
   const int64_t i_begin = P.chunk_begin[j], i_end = P.chunk_begin[j + 1];
   const bool in_item = lane < it.count;
@@ -231,43 +272,40 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
   const int my_m = in_item ? P.bt.cand_model[c] : -1;
   const int my_g = in_item ? P.bt.cand_group[c] : 0;
   const bool active = in_item && P.bt.cand_ok[c];
-  const uint64_t my_bit = (my_m >= 0) ? (1ull << my_g) : 0ull;
+  const uint64_t my_bit = (my_m >= 0 && active) ? (1ull << my_g) : 0ull;
   const int slots = it.slots;
+  const int M = P.pr.M;
   const int64_t slot_id = (int64_t)item * 32 + lane;
+  const int64_t unit = (int64_t)j * P.num_items + item;
 
-  // initial state and epoch.  The speculative trajectory starts from the
-  // base's true boundary state (or idle); the fix-up's true trajectory from
-  // the previous chunk's true end state.
+  // relevance: models hosted by the base or added by some active lane
+  for (int m = lane; m < M; m += 32) w.rel[m] = w.mask[m] != 0ull;
+  __syncwarp();
+  if (my_bit) w.rel[my_m] = 1;
+
+  // initial states
   int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
-  T* spec_st = DUAL ? w.st1 : w.st0;
-  if (P.spec_state != nullptr && j > 0) {
-    const int64_t* ss = P.spec_state + ((int64_t)P.spec_row[it.base] * P.J + j) * P.state_stride;
-    for (int k = 0; k < slots; ++k) {
-      const int64_t v = ss[k];
-      if constexpr (TT<T>::kRel) {
-        const int64_t r = v - E;
-        spec_st[k * 32 + lane] = r > 0 ? (T)r : (T)0;
-      } else {
-        spec_st[k * 32 + lane] = (T)v;
+  if constexpr (MODE != WALK) {  // the speculative trajectory
+    T* spec_st = (MODE == DUAL) ? w.st1 : w.st0;
+    if (P.spec_state != nullptr && j > 0) {
+      const int64_t* ss = P.spec_state + ((int64_t)P.spec_row[it.base] * P.J + j) * P.state_stride;
+      for (int k = 0; k < slots; ++k) {
+        const int64_t v = ss[k];
+        if constexpr (TT<T>::kRel) {
+          const int64_t r = v - E;
+          spec_st[k * 32 + lane] = r > 0 ? (T)r : (T)0;
+        } else {
+          spec_st[k * 32 + lane] = (T)v;
+        }
       }
+    } else {
+      for (int k = 0; k < slots; ++k) spec_st[k * 32 + lane] = (T)0;
     }
-  } else {
-    for (int k = 0; k < slots; ++k) spec_st[k * 32 + lane] = (T)0;
   }
-  if constexpr (DUAL) {
-    const int64_t prev = (int64_t)(j - 1) * P.num_items + item;
-    const T* src_st = reinterpret_cast<const T*>(src ? P.fix_end : P.spec_end) +
-                      prev * P.slots_max * 32;
-    const int64_t Ep = (src ? P.fix_epoch : P.spec_epoch)[prev];
-    for (int k = 0; k < slots; ++k) {
-      const T v = src_st[k * 32 + lane];
-      if constexpr (TT<T>::kRel) {
-        const int64_t r = (int64_t)v - (E - Ep);
-        w.st0[k * 32 + lane] = r > 0 ? (T)r : (T)0;
-      } else {
-        w.st0[k * 32 + lane] = v;
-      }
-    }
+  if constexpr (MODE != SPEC) {  // the true trajectory: true end of chunk j-1
+    const int64_t prev = unit - P.num_items;
+    const T* s0 = reinterpret_cast<const T*>(src ? P.fix_end : P.spec_end) + prev * P.slots_max * 32;
+    load_state<T>(w.st0, s0, (src ? P.fix_epoch : P.spec_epoch)[prev], E, slots, lane);
   }
   __syncwarp();
 
@@ -276,37 +314,33 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
   bool coalesced = false;
   T dv[S > 0 ? S : 1];
   for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
-    const int64_t ai = (i0 + lane < i_end) ? P.tr.arrival[i0 + lane] : 0;
-    const int mi = (i0 + lane < i_end) ? (int)P.tr.model[i0 + lane] : 0;
-    const int nj = (int)min((int64_t)32, i_end - i0);
-    for (int jj = 0; jj < nj; ++jj) {
+    const bool valid = i0 + lane < i_end;
+    const int64_t ai = valid ? P.tr.arrival[i0 + lane] : 0;
+    const int mi = valid ? (int)P.tr.model[i0 + lane] : 0;
+    if constexpr (MODE == DUAL) {
+      if (((i0 - i_begin) % kCheckEvery) == 0) {
+        const int64_t a0 = __shfl_sync(FULL, ai, 0);
+        maybe_rebase<T, MODE>(P, w, slots, lane, a0, E);
+        const T ar = (T)(a0 - E);
+        bool eq = true;
+        for (int k = 0; k < slots; ++k)
+          eq &= tmax(w.st0[k * 32 + lane], ar) == tmax(w.st1[k * 32 + lane], ar);
+        if (__all_sync(FULL, eq || !active)) {
+          coalesced = true;
+          break;
+        }
+      }
+    }
+    unsigned todo = __ballot_sync(FULL, valid && w.rel[mi]);
+    while (todo) {  // requests some lane hosts, in trace order
+      const int jj = __ffs(todo) - 1;
+      todo &= todo - 1;
       const int64_t a = __shfl_sync(FULL, ai, jj);
       const int m = __shfl_sync(FULL, mi, jj);
-      if constexpr (TT<T>::kRel) {
-        if (a - E > P.theta) {  // warp-uniform epoch move (exact, see header)
-          // every stored value is < 2^32 - 1, so a longer gap clears them all
-          const int64_t gap = a - E;
-          const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
-          rebase<T>(w.st0, slots, lane, delta);
-          if constexpr (DUAL) rebase<T>(w.st1, slots, lane, delta);
-          E = a;
-        }
-      }
+      maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
       const T ar = (T)(a - E);
-      if constexpr (DUAL) {
-        if (((i0 + jj - i_begin) % kCheckEvery) == 0) {
-          bool eq = true;
-          for (int k = 0; k < slots; ++k)
-            eq &= tmax(w.st0[k * 32 + lane], ar) == tmax(w.st1[k * 32 + lane], ar);
-          if (__all_sync(FULL, eq || !active)) {
-            coalesced = true;
-            break;
-          }
-        }
-      }
       uint64_t mask = w.mask[m] | ((m == my_m) ? my_bit : 0ull);
       if (!active) mask = 0ull;
-      if (__ballot_sync(FULL, mask != 0ull) == 0u) continue;  // hosted nowhere: rejected
       T tl = 0;
       if constexpr (S > 0) {
 #pragma unroll
@@ -319,7 +353,7 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
         ++good0;
         sum0 += l0;
       }
-      if constexpr (DUAL) {
+      if constexpr (MODE == DUAL) {
         const int64_t l1 = step<T, S>(P, w, w.st1, lane, mask, m, ar, dv, tl, sl, upd);
         if (l1 >= 0) {
           ++good1;
@@ -327,70 +361,133 @@ __device__ void run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
         }
       }
     }
-    if (DUAL && coalesced) break;
   }
 
   if (P.stage_updates) {
     for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(FULL, upd, o);
     if (lane == 0) atomicAdd(P.stage_updates, upd);
   }
-  const int64_t unit = (int64_t)j * P.num_items + item;
-  if constexpr (!DUAL) {
-    P.spec_good[(int64_t)j * P.num_items * 32 + slot_id] = (int32_t)good0;
-    P.spec_sum[(int64_t)j * P.num_items * 32 + slot_id] = sum0;
+  const int64_t cstride = (int64_t)P.num_items * 32;
+  bool equivalent = true;
+  if constexpr (MODE == SPEC) {
+    P.spec_good[j * cstride + slot_id] = (int32_t)good0;
+    P.spec_sum[j * cstride + slot_id] = sum0;
     if (j + 1 < P.J) {  // end state for the next chunk's fix-up
       T* out = reinterpret_cast<T*>(P.spec_end) + unit * P.slots_max * 32;
       for (int k = 0; k < slots; ++k) out[k * 32 + lane] = w.st0[k * 32 + lane];
       if (lane == 0) P.spec_epoch[unit] = E;
     }
-  } else {
-    P.fix_good[(int64_t)j * P.num_items * 32 + slot_id] = (int32_t)(good0 - good1);
-    P.fix_sum[(int64_t)j * P.num_items * 32 + slot_id] = sum0 - sum1;
+  } else if constexpr (MODE == DUAL) {
+    P.fix_good[j * cstride + slot_id] = (int32_t)(good0 - good1);
+    P.fix_sum[j * cstride + slot_id] = sum0 - sum1;
     if (lane == 0) P.fix_flag[unit] = coalesced ? 0 : 1;
     if (!coalesced && j + 1 < P.J) {  // publish the true end state
       T* out = reinterpret_cast<T*>(P.fix_end) + unit * P.slots_max * 32;
       for (int k = 0; k < slots; ++k) out[k * 32 + lane] = w.st0[k * 32 + lane];
       if (lane == 0) P.fix_epoch[unit] = E;
     }
+  } else {  // WALK: exact correction of the whole chunk
+    P.fix_good[j * cstride + slot_id] = (int32_t)(good0 - P.spec_good[j * cstride + slot_id]);
+    P.fix_sum[j * cstride + slot_id] = sum0 - P.spec_sum[j * cstride + slot_id];
+    if (j + 1 < P.J) {
+      // equivalent to the speculative end at the next arrival?  (absolute times)
+      const int64_t a_next = P.tr.arrival[i_end];
+      const T* se = reinterpret_cast<const T*>(P.spec_end) + unit * P.slots_max * 32;
+      const int64_t Es = P.spec_epoch[unit];
+      bool eq = true;
+      for (int k = 0; k < slots; ++k) {
+        const int64_t t0 = (TT<T>::kRel ? E : 0) + (int64_t)w.st0[k * 32 + lane];
+        const int64_t t1 = (TT<T>::kRel ? Es : 0) + (int64_t)se[k * 32 + lane];
+        eq &= (t0 > a_next ? t0 : a_next) == (t1 > a_next ? t1 : a_next);
+      }
+      equivalent = __all_sync(FULL, eq || !active);
+      if (!equivalent) {
+        T* out = reinterpret_cast<T*>(P.fix_end) + unit * P.slots_max * 32;
+        for (int k = 0; k < slots; ++k) out[k * 32 + lane] = w.st0[k * 32 + lane];
+        if (lane == 0) P.fix_epoch[unit] = E;
+      }
+    }
+  }
+  return equivalent;
+}
+
+template <typename T, int MODE>
+__device__ __forceinline__ bool dispatch_unit(const ChunkParams& P, WarpMem<T>& w,
+                                              const ItemDesc& it, int item, int j, int lane,
+                                              int src) {
+  switch (it.S) {
+    case 1: return run_unit<T, 1, MODE>(P, w, it, item, j, lane, src);
+    case 2: return run_unit<T, 2, MODE>(P, w, it, item, j, lane, src);
+    case 4: return run_unit<T, 4, MODE>(P, w, it, item, j, lane, src);
+    case 8: return run_unit<T, 8, MODE>(P, w, it, item, j, lane, src);
+    case 16: return run_unit<T, 16, MODE>(P, w, it, item, j, lane, src);
+    default: return run_unit<T, 0, MODE>(P, w, it, item, j, lane, src);
   }
 }
 
-template <typename T, bool DUAL>
+__device__ __forceinline__ int next_unit(const ChunkParams& P, int lane) {
+  int u = 0;
+  if (lane == 0) u = (int)atomicAdd(P.counter, 1u);
+  return __shfl_sync(FULL, u, 0);
+}
+
+// Passes 1 and 2: persistent warps pulling (item, chunk) units.
+template <typename T, int MODE>
 __global__ void __launch_bounds__(kWarps * 32) chunk_kernel(ChunkParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpMem<T> w = carve<T>(smem + warp * warp_bytes<T>(P, DUAL), P, DUAL);
-  int cur_base = -1, cur_cfg = -2;
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), MODE == DUAL);
+  WarpMem<T> w = carve<T>(smem + warp * wb, P, MODE == DUAL);
+  int cur_base = -1;
   for (;;) {
-    int u = 0;
-    if (lane == 0) u = (int)atomicAdd(P.counter, 1u);
-    u = __shfl_sync(FULL, u, 0);
+    const int u = next_unit(P, lane);
     if (u >= P.num_units) break;
-    int item, j, src = 0;
-    if constexpr (DUAL) {
-      const ChunkUnit cu = P.units[u];
-      item = cu.item;
-      j = cu.chunk;
-      src = cu.src;
-    } else {  // pass 1 enumerates every (item, chunk), chunk-major
-      item = u % P.num_items;
-      j = u / P.num_items;
-    }
+    const int item = u % P.num_items;
+    const int j = (MODE == DUAL ? 1 : 0) + u / P.num_items;  // chunk-major
     const ItemDesc it = P.items[item];
-    if (it.base != cur_base || it.cfg != cur_cfg) {
+    if (it.base != cur_base) {
       load_base<T>(P, it, w, lane);
       cur_base = it.base;
-      cur_cfg = it.cfg;
     }
-    switch (it.S) {
-      case 1: run_unit<T, 1, DUAL>(P, w, it, item, j, lane, src); break;
-      case 2: run_unit<T, 2, DUAL>(P, w, it, item, j, lane, src); break;
-      case 4: run_unit<T, 4, DUAL>(P, w, it, item, j, lane, src); break;
-      case 8: run_unit<T, 8, DUAL>(P, w, it, item, j, lane, src); break;
-      case 16: run_unit<T, 16, DUAL>(P, w, it, item, j, lane, src); break;
-      default: run_unit<T, 0, DUAL>(P, w, it, item, j, lane, src); break;
-    }
+    dispatch_unit<T, MODE>(P, w, it, item, j, lane, 0);
     __syncwarp();
+  }
+}
+
+// Pass 3: one warp per item walks the chunks whose start state was wrong.
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) walk_kernel(ChunkParams P, uint8_t* end_src) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  WarpMem<T> w = carve<T>(smem + warp * wb, P, false);
+  int cur_base = -1;
+  for (;;) {
+    const int item = next_unit(P, lane);
+    if (item >= P.num_items) break;
+    const ItemDesc it = P.items[item];
+    if (lane == 0) end_src[item] = 0;  // chunk 0 starts idle: exact
+    bool start_ok = true;  // pass 2 started chunk j from its true start state
+    unsigned long long walked = 0;
+    for (int j = 1; j < P.J; ++j) {
+      const int64_t u = (int64_t)j * P.num_items + item;
+      if (start_ok) {
+        const bool met = P.fix_flag[u] == 0;  // pass 2's correction is exact
+        if (lane == 0) end_src[u] = met ? 0 : 1;
+        start_ok = met;  // else the true end of chunk j is pass 2's fix_end
+        continue;
+      }
+      if (it.base != cur_base) {
+        load_base<T>(P, it, w, lane);
+        cur_base = it.base;
+      }
+      ++walked;
+      const bool eq = dispatch_unit<T, WALK>(P, w, it, item, j, lane, 1);
+      if (lane == 0) end_src[u] = eq ? 0 : 1;
+      start_ok = eq;
+      __syncwarp();
+    }
+    if (P.walked && lane == 0 && walked) atomicAdd(P.walked, walked);
   }
 }
 
@@ -432,34 +529,45 @@ __global__ void publish_kernel(ChunkParams P, const uint8_t* __restrict__ end_sr
     const bool fix = end_src[u] != 0;
     const T* st = reinterpret_cast<const T*>(fix ? P.fix_end : P.spec_end) + u * P.slots_max * 32;
     const T x = st[k * 32 + 0];  // lane 0 of the item
-    if constexpr (TT<T>::kRel) {
-      v = (fix ? P.fix_epoch : P.spec_epoch)[u] + (int64_t)x;
-    } else {
-      v = (int64_t)x;
-    }
+    v = (TT<T>::kRel ? (fix ? P.fix_epoch : P.spec_epoch)[u] : 0) + (int64_t)x;
   }
   out[((int64_t)out_row[item] * P.J + j) * P.state_stride + k] = v;
 }
 
-template <typename T, bool DUAL>
-cudaError_t launch_t(const ChunkParams& P, cudaStream_t st, int sms) {
-  const size_t per_warp = (size_t)P.slots_max * 32 * sizeof(T) * (DUAL ? 2 : 1) +
-                          (size_t)P.pr.M * (8 + sizeof(T) * (kSTab + 2)) + 64 * 4;
-  const size_t smem = kWarps * ((per_warp + 15) & ~size_t(15));
+template <typename K>
+cudaError_t grid_for(K kernel, size_t smem, int64_t units, int sms, int64_t* blocks) {
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(chunk_kernel<T, DUAL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_kernel<T, DUAL>, kWarps * 32,
-                                                    smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  int64_t blocks = (int64_t)per_sm * sms;  // persistent: warps pull units from a counter
-  const int64_t need = ((int64_t)P.num_units + kWarps - 1) / kWarps;
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  chunk_kernel<T, DUAL><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P);
+  int64_t b = (int64_t)per_sm * sms;  // persistent: warps pull units from a counter
+  const int64_t need = (units + kWarps - 1) / kWarps;
+  if (b > need) b = need;
+  *blocks = b < 1 ? 1 : b;
+  return cudaSuccess;
+}
+
+template <typename T, int MODE>
+cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
+  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, sizeof(T), MODE == DUAL);
+  int64_t blocks = 1;
+  cudaError_t e = grid_for(chunk_kernel<T, MODE>, smem, P.num_units, sms, &blocks);
+  if (e != cudaSuccess) return e;
+  chunk_kernel<T, MODE><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_walk_t(const ChunkParams& P, uint8_t* end_src, cudaStream_t st, int sms) {
+  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  int64_t blocks = 1;
+  cudaError_t e = grid_for(walk_kernel<T>, smem, P.num_items, sms, &blocks);
+  if (e != cudaSuccess) return e;
+  walk_kernel<T><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
   return cudaGetLastError();
 }
 
@@ -471,9 +579,18 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
   cudaError_t e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
   if (u32)
-    e = dual ? launch_t<uint32_t, true>(P, st, sms) : launch_t<uint32_t, false>(P, st, sms);
+    e = dual ? launch_pass_t<uint32_t, DUAL>(P, st, sms) : launch_pass_t<uint32_t, SPEC>(P, st, sms);
   else
-    e = dual ? launch_t<int64_t, true>(P, st, sms) : launch_t<int64_t, false>(P, st, sms);
+    e = dual ? launch_pass_t<int64_t, DUAL>(P, st, sms) : launch_pass_t<int64_t, SPEC>(P, st, sms);
+  if (launches) ++*launches;
+  return e;
+}
+
+cudaError_t launch_chunk_walk(const ChunkParams& P, uint8_t* end_src, bool u32, cudaStream_t st,
+                              int sms, int64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  e = u32 ? launch_walk_t<uint32_t>(P, end_src, st, sms) : launch_walk_t<int64_t>(P, end_src, st, sms);
   if (launches) ++*launches;
   return e;
 }

@@ -103,7 +103,6 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   if (e == cudaSuccess) e = ctx->c_fix_epoch.ensure(J * I * 8);
   if (e == cudaSuccess) e = ctx->c_flag.ensure(J * I);
   if (e == cudaSuccess) e = ctx->c_counter.ensure(16);
-  if (e == cudaSuccess && J > 1) e = ctx->c_units.ensure(J * I * sizeof(asim::ChunkUnit));
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk buffers");
 
   asim::ChunkParams P{};
@@ -134,6 +133,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.fix_epoch = ctx->c_fix_epoch.as<int64_t>();
   P.fix_flag = ctx->c_flag.as<uint8_t>();
   P.stage_updates = out.stage_updates;
+  P.walked = ctx->profiling ? ctx->d_walked.as<unsigned long long>() : nullptr;
   P.spec_state = opt ? opt->spec_state : nullptr;
   P.spec_row = opt ? opt->spec_row : nullptr;
   P.state_stride = (opt && opt->state_stride > 0) ? opt->state_stride : slots_max;
@@ -142,65 +142,29 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
 
   // ---- pass 1: every (item, chunk) from the idle state
   P.num_units = (int32_t)(J * I);
-  P.units = nullptr;
   e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
 
-  std::vector<uint8_t> end_src(J * I, 0);
+  e = ctx->c_end_src.ensure(J * I + 8);
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src buffer");
+  uint8_t* end_src = ctx->c_end_src.as<uint8_t>();
   if (J > 1) {
     // ---- pass 2: fix-up of every chunk j >= 1 from chunk j-1's speculative end
-    std::vector<asim::ChunkUnit> units;
-    units.reserve((J - 1) * I);
-    for (int32_t i = 0; i < I; ++i)
-      for (int32_t j = 1; j < J; ++j) units.push_back(asim::ChunkUnit{i, j, 0, 0});
-    e = upload(ctx->c_units, units, st);
-    if (e != cudaSuccess) return asim_cuda(ctx, e, "upload units");
-    P.units = ctx->c_units.as<asim::ChunkUnit>();
-    P.num_units = (int32_t)units.size();
+    P.num_units = (int32_t)((J - 1) * I);
     e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 2");
-    // ---- exact re-run chains: a chunk whose trajectories never met publishes
-    // its true end state; the next chunk is re-run from it, and so on.
-    std::vector<uint8_t> flag(J * I);
-    std::vector<uint8_t> computed_src(J * I, 0);  // start source used by unit (item, j)
-    std::vector<int32_t> pos(I, 1);
-    std::vector<uint8_t> prev_src(I, 0);
-    end_src.assign(J * I, 0);  // chunk 0 is exact: its true end is spec_end
-    for (;;) {
-      e = cudaMemcpyAsync(flag.data(), P.fix_flag, J * I, cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk flags");
-      std::vector<asim::ChunkUnit> redo;
-      for (int32_t i = 0; i < I; ++i) {
-        while (pos[i] < J) {
-          const int64_t u = (int64_t)pos[i] * I + i;
-          if (computed_src[u] == prev_src[i]) {
-            prev_src[i] = flag[u] ? 1 : 0;
-            end_src[u] = prev_src[i];
-            ++pos[i];
-          } else {
-            redo.push_back(asim::ChunkUnit{i, pos[i], 1, 0});
-            computed_src[u] = 1;
-            break;
-          }
-        }
-      }
-      if (redo.empty()) break;
-      ctx->chunk_reruns += (int64_t)redo.size();
-      e = upload(ctx->c_units, redo, st);
-      if (e != cudaSuccess) return asim_cuda(ctx, e, "upload redo units");
-      P.num_units = (int32_t)redo.size();
-      e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
-      if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk re-run");
-    }
+    // ---- pass 3: walk the chunks whose start state was wrong (exact chains)
+    e = asim::launch_chunk_walk(P, end_src, u32, st, ctx->sms, &ctx->launches);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk walk");
+  } else {
+    e = cudaMemsetAsync(end_src, 0, J * I, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src");
   }
   e = asim::launch_chunk_reduce(P, out, st, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk reduce");
   if (opt && opt->publish_out) {  // true boundary states of lane 0 of every item
-    e = upload(ctx->c_end_src, end_src, st);
-    if (e == cudaSuccess)
-      e = asim::launch_publish_states(P, ctx->c_end_src.as<uint8_t>(), u32, opt->publish_row,
-                                      opt->publish_out, st, &ctx->launches);
+    e = asim::launch_publish_states(P, end_src, u32, opt->publish_row, opt->publish_out, st,
+                                    &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "publish states");
   }
   return ASIM_OK;

@@ -139,18 +139,24 @@ asim_status asim_ready(asim_ctx* ctx) {
   return ASIM_OK;
 }
 
-asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
-                           const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
-  const int64_t C = (int64_t)hb.cand_base.size();
-  if (end <= begin) return ASIM_OK;
-  if (begin < 0 || end > C) return asim_fail(ctx, ASIM_ERANGE, "candidate range");
+asim_status asim_upload_batch(asim_ctx* ctx, const HostBatch& hb, cudaStream_t st) {
   cudaError_t e = upload(ctx->d_base_cfg, hb.base_cfg, st);
   if (e == cudaSuccess) e = upload(ctx->d_base_mask, hb.base_mask, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_base, hb.cand_base, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_model, hb.cand_model, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_group, hb.cand_group, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_ok, hb.cand_ok, st);
-  if (e != cudaSuccess) return asim_cuda(ctx, e, "upload batch");
+  return asim_cuda(ctx, e, "upload batch");
+}
+
+asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
+                           const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
+  const int64_t C = (int64_t)hb.cand_base.size();
+  if (end <= begin) return ASIM_OK;
+  if (begin < 0 || end > C) return asim_fail(ctx, ASIM_ERANGE, "candidate range");
+  asim_status us = asim_upload_batch(ctx, hb, st);
+  if (us) return us;
+  cudaError_t e = cudaSuccess;
   // Throughput path: candidates sharing a base placement, no per-model
   // counts -> chunked kernel (chunk.cu); otherwise the general kernel below.
   const bool shared_bases = (int64_t)(hb.base_cfg.size() / std::max<int32_t>(hb.G, 1)) < C ||
@@ -264,10 +270,10 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->d_arrival, &ctx->d_model, &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group,
                     &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm,
-                    &ctx->d_argmax, &ctx->d_counter, &ctx->c_items, &ctx->c_begin,
+                    &ctx->d_argmax, &ctx->d_counter, &ctx->d_walked, &ctx->c_items, &ctx->c_begin,
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
-                    &ctx->c_flag, &ctx->c_counter, &ctx->c_units, &ctx->c_end_src};
+                    &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src};
     for (DBuf* b : bufs) b->release();
   }
   delete ctx;
@@ -291,9 +297,9 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   ctx->sim_launches = 0;
   ctx->sim_ms = 0.0;
   ctx->request_evals = 0;
-  ctx->chunk_reruns = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 8);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 8);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return asim_cuda(ctx, e, "reset stats");
   }
@@ -319,7 +325,9 @@ asim_status asim_set_profiling(asim_ctx* ctx, int32_t on) {
   DeviceGuard dg(ctx->device);
   if (on && !ctx->d_counter.p) {
     cudaError_t e = ctx->d_counter.ensure(8);
+    if (e == cudaSuccess) e = ctx->d_walked.ensure(8);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 8);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 8);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "profiling counter");
   }
   ctx->profiling = on != 0;
@@ -339,9 +347,10 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
     cudaEventDestroy(ev.second);
   }
   ctx->events.clear();
-  unsigned long long upd = 0;
+  unsigned long long upd = 0, walked = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemcpy(&upd, ctx->d_counter.p, 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(&walked, ctx->d_walked.p, 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "stats counter");
   }
   out->launches = ctx->launches;
@@ -349,7 +358,7 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->sim_ms = ctx->sim_ms;
   out->stage_updates = (int64_t)upd;
   out->request_evals = ctx->request_evals;
-  out->chunk_reruns = ctx->chunk_reruns;
+  out->chunk_reruns = (int64_t)walked;
   return ASIM_OK;
 }
 

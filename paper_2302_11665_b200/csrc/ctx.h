@@ -66,12 +66,12 @@ struct asim_ctx {
   double sim_ms = 0.0;
   int64_t request_evals = 0;
   DBuf d_counter;  // unsigned long long stage-update counter
+  DBuf d_walked;   // unsigned long long walked-chunk counter
 
   int sms = 148;
-  int64_t chunk_reruns = 0;
   // chunked path buffers (chunked.cpp)
   DBuf c_items, c_begin, c_spec_good, c_spec_sum, c_fix_good, c_fix_sum, c_spec_end, c_fix_end,
-      c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_units, c_end_src;
+      c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_end_src;
   int32_t force_path = 0;  // 0 auto, 1 general kernel, 2 chunked kernel (tests)
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
 
@@ -125,6 +125,8 @@ struct HostBatch {
 // Upload a batch and launch the simulation of candidates [0, C) writing
 // good/sum/per-model at out (device pointers, indexed by candidate).
 struct ChunkOptions;
+// Copy a batch's bases and candidates into the context's device buffers.
+asim_status asim_upload_batch(asim_ctx* ctx, const HostBatch& hb, cudaStream_t st);
 asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                            const asim::DevOut& out, cudaStream_t st,
                            const ChunkOptions* opt = nullptr);

@@ -281,7 +281,8 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
       asim::DevOut bo{};
       bo.good = s->d_base_good.as<int64_t>();
       bo.out_offset = 0;
-      st = asim_run_chunked(s->ctx, s->hb_base, 0, B, bo, strm, &ob);
+      st = asim_upload_batch(s->ctx, s->hb_base, strm);
+      if (!st) st = asim_run_chunked(s->ctx, s->hb_base, 0, B, bo, strm, &ob);
       if (st) {
         if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
         return st;

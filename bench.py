@@ -329,7 +329,8 @@ def main():
             config=dict(workload=name, trace_requests=N, models=prob.num_models,
                         devices=prob.num_devices, runs=len(res.runs), search_steps=res.steps,
                         candidates_per_search=res.candidates,
-                        simulated_per_search=res.evaluated, dedup=bool(args.dedup),
+                        simulated_per_search=res.evaluated, memo_hits=res.memo_hits,
+                        dedup=bool(args.dedup),
                         best_run=res.best_run, best_attainment=res.best_good / max(N, 1),
                         l2="flushed between timed steps (256 MB write)",
                         parallelism=f"candidate-sharded x{world}"),

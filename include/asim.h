@@ -224,12 +224,19 @@ double asim_attainment(int64_t good, int64_t n);
  * num_devices/size groups of config p.  Otherwise run r has run_num_groups[r]
  * groups with configs run_group_cfg[sum_{r'<r} G_r' ...] (host arrays).
  *
+ * Exactness-preserving reuse: a candidate whose connected component of the
+ * (group, model) hosting graph is untouched by the previous step's winner
+ * keeps its previous good shifted by the base's change (components are
+ * simulated independently by construction); only the others are simulated.
+ *
  * Stepwise protocol (for candidate sharding across GPUs):
- *   asim_search_prepare  -> *num_candidates = C of this step (0 = finished)
+ *   asim_search_prepare  -> *num_candidates = C candidates of this step that
+ *                           need simulation (may be 0); -1 = search finished
  *   asim_search_evaluate -> good of global candidates [begin, end) into
  *                           good_dev[0 .. end-begin) (device, stream-ordered)
  *   (all-gather the shards into one device array of C int64)
- *   asim_search_apply    -> per-run argmax over good_all_dev[C]; apply
+ *   asim_search_apply    -> per-run argmax over good_all_dev[C] (NULL if C == 0)
+ *                           and the memo values; apply
  * asim_search_run does the whole loop on this context's GPU.
  * The search borrows ctx (problem and trace must stay set while it lives). */
 typedef struct {
@@ -250,6 +257,7 @@ typedef struct {
   int64_t candidates;      /* sum over steps of C (simulate() calls)          */
   int64_t evaluated;       /* candidates actually simulated (after dedup)     */
   int64_t request_evals;   /* sum over evaluated candidates of n (requests)   */
+  int64_t memo_hits;       /* candidates whose good came from the component memo */
 } asim_search_result;
 
 asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim_search** out);

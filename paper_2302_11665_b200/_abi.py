@@ -59,7 +59,7 @@ class asim_search_spec(ctypes.Structure):
 class asim_search_result(ctypes.Structure):
     _fields_ = [("best_run", i32), ("best_good", i64), ("num_groups", i32), ("group_cfg", vp),
                 ("host_mask", vp), ("steps", i64), ("candidates", i64), ("evaluated", i64),
-                ("request_evals", i64)]
+                ("request_evals", i64), ("memo_hits", i64)]
 
 
 if not os.path.exists(LIB_PATH):

@@ -60,6 +60,7 @@ class SearchResult:
     candidates: int
     evaluated: int
     request_evals: int
+    memo_hits: int
     runs: list
 
 
@@ -220,6 +221,7 @@ class SearchHandle:
         self.close()
 
     def prepare(self) -> int:
+        """Candidates of this step needing simulation (>= 0), or -1 when finished."""
         c = ctypes.c_int64()
         self.sim._check(A.asim_search_prepare(self.h, ctypes.byref(c)))
         return int(c.value)
@@ -230,7 +232,8 @@ class SearchHandle:
                                                _stream_ptr(stream)))
 
     def apply(self, good_all_dev, stream=None) -> None:
-        self.sim._check(A.asim_search_apply(self.h, _ptr(good_all_dev), _stream_ptr(stream)))
+        self.sim._check(A.asim_search_apply(self.h, _ptr(good_all_dev) if good_all_dev is not None
+                                            else None, _stream_ptr(stream)))
 
     def run(self, stream=None) -> None:
         self.sim._check(A.asim_search_run(self.h, _stream_ptr(stream)))
@@ -239,7 +242,7 @@ class SearchHandle:
         M = self.sim.M
         cfg = np.full(A.ASIM_MAX_GROUPS, -1, np.int32)
         mask = np.zeros(M, np.uint64)
-        r = A.asim_search_result(0, 0, 0, _ptr(cfg), _ptr(mask), 0, 0, 0, 0)
+        r = A.asim_search_result(0, 0, 0, _ptr(cfg), _ptr(mask), 0, 0, 0, 0, 0)
         self.sim._check(A.asim_search_result_get(self.h, ctypes.byref(r)))
         runs = []
         for i in range(A.asim_search_num_runs(self.h)):
@@ -253,4 +256,5 @@ class SearchHandle:
             runs.append(dict(num_groups=ng.value, group_cfg=rc[:ng.value].copy(), host_mask=rm,
                              best_good=bg.value, steps=stp.value))
         return SearchResult(r.best_run, r.best_good, r.num_groups, cfg[:r.num_groups].copy(),
-                            mask, r.steps, r.candidates, r.evaluated, r.request_evals, runs)
+                            mask, r.steps, r.candidates, r.evaluated, r.request_evals,
+                            r.memo_hits, runs)

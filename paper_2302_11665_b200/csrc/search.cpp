@@ -13,6 +13,15 @@
 //   apply     a7: per run, argmax (ties -> lowest index, "pick_highest",
 //             P:722) and sel <- sel + (m*, g*); best_sel on strict '>'.
 //
+// Exact component memo (always on): a placement's simulation splits into
+// independent connected components of the bipartite (group, model) hosting
+// graph -- a request is only ever dispatched among its model's hosts, and a
+// group's stages only see requests of the models it hosts.  Candidate (m, g)
+// of step t whose component K = comp(g) u comp(m) u {m} in base(t-1) is
+// disjoint from the two components the step-(t-1) winner (m*, g*) merged has
+// good_t(m, g) = good_{t-1}(m, g) + good(base(t)) - good(base(t-1)) exactly,
+// so only the other candidates are simulated.
+//
 // Exact de-duplication (spec->dedup): adding model m to either of two EMPTY
 // groups g1 < g2 with the same config gives the same simulation whenever g1
 // and g2 sit between the same pair of m's hosting groups in index order
@@ -40,6 +49,34 @@ struct Run {
   int64_t best_good = 0;
   bool active = true;
   int64_t steps = 0;
+  int64_t base_good = 0;  // good of the current selection (the last winner)
+  // this step's full candidate list, in (m, g) order
+  struct Cand {
+    int32_t m, g;
+    int8_t kind;    // 0 simulated (ref = batch index), 1 memo (value), 2 duplicate (ref = rep)
+    int64_t ref;
+    int64_t good;
+  };
+  std::vector<Cand> cands;
+  // memo carried to the next step: (m, g) -> good, valid when the winner is elsewhere
+  std::map<std::pair<int32_t, int32_t>, int64_t> memo;
+  std::vector<std::pair<int32_t, int32_t>> history;  // winners in order
+};
+
+// union-find over G groups + M models (node G + m) of one selection
+struct Components {
+  std::vector<int32_t> p;
+  Components(int32_t G, int32_t M, const std::vector<uint64_t>& sel) : p(G + M) {
+    for (size_t i = 0; i < p.size(); ++i) p[i] = (int32_t)i;
+    for (int32_t m = 0; m < M; ++m)
+      for (int32_t g = 0; g < G; ++g)
+        if ((sel[m] >> g) & 1ULL) unite(g, G + m);
+  }
+  int32_t find(int32_t x) {
+    while (p[x] != x) x = p[x] = p[p[x]];
+    return x;
+  }
+  void unite(int32_t a, int32_t b) { p[find(a)] = find(b); }
 };
 
 }  // namespace
@@ -65,7 +102,8 @@ struct asim_search {
   bool base_ready = false;
   HostBatch hb_base;        // one candidate per base: the base itself
   // statistics
-  int64_t steps = 0, candidates = 0, evaluated = 0;
+  int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0;
+  bool finished = false;
 };
 
 static asim_status sfail(asim_search* s, asim_status code, const std::string& m) {
@@ -189,28 +227,42 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
     for (int32_t m = 0; m < M; ++m)
       for (int32_t g = 0; g < run.G; ++g)
         if ((run.sel[m] >> g) & 1ULL) empty[g] = 0;
-    int64_t n_run = 0;
+    run.cands.clear();
     for (int32_t m = 0; m < M; ++m) {
-      std::map<std::pair<int32_t, int32_t>, bool> seen;  // (cfg, rank among hosts) of empty groups
+      std::map<std::pair<int32_t, int32_t>, int64_t> seen;  // (cfg, rank among hosts) -> rep
       for (int32_t g = 0; g < run.G; ++g) {
         if ((run.sel[m] >> g) & 1ULL) continue;  // a model at most once per group (C11)
         const int64_t mb = hp.mem_at(m, run.cfg[g]);
         if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
         ++full;
-        ++n_run;
-        if (s->dedup && empty[g]) {
+        Run::Cand c{m, g, 0, 0, 0};
+        auto it = run.memo.find(std::make_pair(m, g));
+        if (it != run.memo.end()) {  // component untouched by the last winner
+          c.kind = 1;
+          c.good = it->second;
+          ++s->memo_hits;
+        } else if (s->dedup && empty[g]) {
           const uint64_t below = g ? (run.sel[m] & ((1ULL << g) - 1)) : 0ULL;
           auto key = std::make_pair(run.cfg[g], (int32_t)__builtin_popcountll(below));
-          if (seen.count(key)) continue;
-          seen[key] = true;
+          auto sit = seen.find(key);
+          if (sit != seen.end()) {
+            c.kind = 2;
+            c.ref = sit->second;
+          } else {
+            seen[key] = (int64_t)run.cands.size();
+          }
         }
-        hb.cand_base.push_back(b);
-        hb.cand_model.push_back(m);
-        hb.cand_group.push_back(g);
-        hb.cand_ok.push_back(1);
+        if (c.kind == 0) {
+          c.ref = (int64_t)hb.cand_base.size();
+          hb.cand_base.push_back(b);
+          hb.cand_model.push_back(m);
+          hb.cand_group.push_back(g);
+          hb.cand_ok.push_back(1);
+        }
+        run.cands.push_back(c);
       }
     }
-    if (n_run == 0) {  // no feasible addition: this run's Alg. 1 loop ends
+    if (run.cands.empty()) {  // no feasible addition: this run's Alg. 1 loop ends
       run.active = false;
       continue;
     }
@@ -235,12 +287,17 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
     s->hb_base.cand_group.push_back(0);
     s->hb_base.cand_ok.push_back(1);
   }
+  if (s->base_run.empty()) {  // every run has ended: the search is finished
+    s->finished = true;
+    s->prepared = false;
+    *num_candidates = -1;
+    return ASIM_OK;
+  }
   s->prepared = true;
   *num_candidates = (int64_t)hb.cand_base.size();
-  if (*num_candidates == 0) s->prepared = false;  // search finished
   s->candidates += full;
   s->evaluated += *num_candidates;
-  if (*num_candidates) ++s->steps;
+  ++s->steps;
   return ASIM_OK;
 }
 
@@ -307,26 +364,48 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
 asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void* cuda_stream) {
   if (!s) return ASIM_EINVAL;
   if (!s->prepared) return sfail(s, ASIM_ESTATE, "apply before prepare");
-  if (!good_all_dev) return sfail(s, ASIM_EINVAL, "null good_all_dev");
   const int64_t C = (int64_t)s->hb.cand_base.size();
+  if (C > 0 && !good_all_dev) return sfail(s, ASIM_EINVAL, "null good_all_dev");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   s->h_good.resize(C);
-  cudaError_t e = cudaMemcpyAsync(s->h_good.data(), good_all_dev, C * 8, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return asim_cuda(s->ctx, e, "copy step results");
+  if (C > 0) {
+    cudaError_t e =
+        cudaMemcpyAsync(s->h_good.data(), good_all_dev, C * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return asim_cuda(s->ctx, e, "copy step results");
+  }
   const HostProblem& hp = s->ctx->hp;
+  const int32_t M = hp.M;
   for (size_t b = 0; b < s->base_run.size(); ++b) {
     Run& run = s->runs[s->base_run[b]];
+    // every candidate's good: simulated, memo, or its duplicate's representative
     int64_t bi = -1, bg = -1;
-    for (int64_t c = s->seg[b]; c < s->seg[b + 1]; ++c)
-      if (s->h_good[c] > bg) {  // first maximum: lowest index on ties (C12)
-        bg = s->h_good[c];
-        bi = c;
+    for (size_t i = 0; i < run.cands.size(); ++i) {
+      Run::Cand& c = run.cands[i];
+      if (c.kind == 0) c.good = s->h_good[c.ref];
+      else if (c.kind == 2) c.good = run.cands[c.ref].good;
+      if (c.good > bg) {  // first maximum in (m, g) order: lowest index on ties (C12)
+        bg = c.good;
+        bi = (int64_t)i;
       }
+    }
     if (bi < 0) return sfail(s, ASIM_ERANGE, "step results contain no feasible candidate");
-    const int32_t m = s->hb.cand_model[bi], g = s->hb.cand_group[bi];
-    run.sel[m] |= 1ULL << g;
-    run.used[g] += hp.mem_at(m, run.cfg[g]);
+    const int32_t ms = run.cands[bi].m, gs = run.cands[bi].g;
+    // memo for the next step: candidates whose component avoids the two
+    // components the winner merges keep their good shifted by the base's change
+    Components comp(run.G, M, run.sel);
+    const int32_t w1 = comp.find(gs), w2 = comp.find(run.G + ms);
+    const int64_t shift = bg - run.base_good;
+    run.memo.clear();
+    for (const Run::Cand& c : run.cands) {
+      const int32_t a1 = comp.find(c.g), a2 = comp.find(run.G + c.m);
+      if (a1 != w1 && a1 != w2 && a2 != w1 && a2 != w2)
+        run.memo.emplace(std::make_pair(c.m, c.g), c.good + shift);
+    }
+    run.sel[ms] |= 1ULL << gs;
+    run.used[gs] += hp.mem_at(ms, run.cfg[gs]);
+    run.base_good = bg;
+    run.history.emplace_back(ms, gs);
     ++run.steps;
     if (bg > run.best_good) {  // "if sel*.slo_att > best_sel.slo_att"
       run.best_good = bg;
@@ -344,7 +423,7 @@ asim_status asim_search_run(asim_search* s, void* cuda_stream) {
     int64_t C = 0;
     asim_status st = asim_search_prepare(s, &C);
     if (st) return st;
-    if (C == 0) return ASIM_OK;
+    if (C < 0) return ASIM_OK;
     cudaError_t e = s->d_good_all.ensure(C * 8 + 8);
     if (e != cudaSuccess) return asim_cuda(s->ctx, e, "allocate step results");
     st = asim_search_evaluate(s, 0, C, s->d_good_all.as<int64_t>(), cuda_stream);
@@ -377,6 +456,7 @@ asim_status asim_search_result_get(const asim_search* s, asim_search_result* out
   out->candidates = s->candidates;
   out->evaluated = s->evaluated;
   out->request_evals = s->evaluated * s->ctx->n;
+  out->memo_hits = s->memo_hits;
   return ASIM_OK;
 }
 

@@ -8,9 +8,10 @@ all-gather of the int64 good counts (NCCL over NVLink on B200s); every rank
 then applies the same per-run argmax (lowest global index on ties), so the
 search state stays identical on all ranks without any further broadcast.
 
-`engine` is anything with prepare() -> C, evaluate(begin, end, out, stream)
-and apply(good_all, stream): api.SearchHandle on the GPU; tests inject a CPU
-engine to exercise this logic under gloo.
+`engine` is anything with prepare() -> C (-1 = finished; 0 = nothing to
+simulate this step), evaluate(begin, end, out, stream) and apply(good_all,
+stream): api.SearchHandle on the GPU; tests inject a CPU engine to exercise
+this logic under gloo.
 """
 
 from __future__ import annotations
@@ -48,8 +49,12 @@ def run_search(engine, pg=None, stream=None, device=None, on_step=None) -> int:
     local = torch.empty(0, dtype=torch.int64, device=device)
     while True:
         C = engine.prepare()
-        if C == 0:
+        if C < 0:
             return steps
+        if C == 0:
+            engine.apply(None, stream)
+            steps += 1
+            continue
         pad = -(-C // world)
         if local.numel() < pad:
             local = torch.zeros(max(pad, 2 * local.numel()), dtype=torch.int64, device=device)

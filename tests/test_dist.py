@@ -49,7 +49,7 @@ class OracleEngine:
                         n += 1
             if n == 0:
                 run["active"] = False
-        return len(self.cands)
+        return len(self.cands) if self.cands else -1
 
     def evaluate(self, b, e, out, stream=None):
         if e <= b:

@@ -216,7 +216,11 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
     }
   }
   if (best_g >= 0 && (T)(best_f - ar) <= sl) {  // reject at receipt if the SLO is missed (C2, C3)
-    commit<T, S>(P, w, st, lane, best_g, m, ar, dv);
+    if constexpr (S == 1) {
+      st[best_g * 32 + lane] = best_f - tl;  // one stage: its departure is f - tail
+    } else {
+      commit<T, S>(P, w, st, lane, best_g, m, ar, dv);
+    }
     return (int64_t)(best_f - ar);
   }
   return -1;
@@ -313,10 +317,25 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
   unsigned long long upd = 0;
   bool coalesced = false;
   T dv[S > 0 ? S : 1];
+  // 4-deep ring of trace tiles in registers: a lone warp (the walk) would
+  // otherwise stall on the L2 latency of every tile.  The trace is padded
+  // by >= 160 records (asim_set_trace), so the look-ahead stays in bounds.
+  int64_t pa0 = P.tr.arrival[i_begin + lane], pa1 = P.tr.arrival[i_begin + 32 + lane];
+  int64_t pa2 = P.tr.arrival[i_begin + 64 + lane], pa3 = P.tr.arrival[i_begin + 96 + lane];
+  int pm0 = P.tr.model[i_begin + lane], pm1 = P.tr.model[i_begin + 32 + lane];
+  int pm2 = P.tr.model[i_begin + 64 + lane], pm3 = P.tr.model[i_begin + 96 + lane];
   for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
     const bool valid = i0 + lane < i_end;
-    const int64_t ai = valid ? P.tr.arrival[i0 + lane] : 0;
-    const int mi = valid ? (int)P.tr.model[i0 + lane] : 0;
+    const int64_t ai = valid ? pa0 : 0;
+    const int mi = valid ? pm0 : 0;
+    pa0 = pa1;
+    pa1 = pa2;
+    pa2 = pa3;
+    pm0 = pm1;
+    pm1 = pm2;
+    pm2 = pm3;
+    pa3 = P.tr.arrival[i0 + 128 + lane];
+    pm3 = P.tr.model[i0 + 128 + lane];
     if constexpr (MODE == DUAL) {
       if (((i0 - i_begin) % kCheckEvery) == 0) {
         const int64_t a0 = __shfl_sync(FULL, ai, 0);

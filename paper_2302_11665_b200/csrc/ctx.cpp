@@ -450,8 +450,9 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
     if (m[i] < 0 || m[i] >= ctx->hp.M) return asim_fail(ctx, ASIM_ERANGE, "model id out of range");
   }
   if (n && a[n - 1] > kMaxTime) return asim_fail(ctx, ASIM_ERANGE, "arrival > 2^62");
-  // pad to a multiple of 32 requests (never-hosted sentinel model 0xFFFF)
-  const int64_t npad = std::max<int64_t>(32, (n + 31) / 32 * 32);
+  // pad to a multiple of 32 requests plus a look-ahead margin of 256 records
+  // (chunk.cu prefetches 4 tiles ahead); sentinel model 0xFFFF is never hosted
+  const int64_t npad = (n + 31) / 32 * 32 + 256;
   std::vector<int64_t> ap(npad, n ? a[n - 1] : 0);
   std::vector<uint16_t> mp(npad, 0xFFFF);
   for (int64_t i = 0; i < n; ++i) {

@@ -83,17 +83,20 @@ template <typename T>
 struct WarpMem {
   T* st0;          // [slots][32] speculative (SPEC) / true (DUAL, WALK) trajectory
   T* st1;          // [slots][32] speculative trajectory (DUAL only)
-  uint64_t* mask;  // [M]   hosting groups of model m in the base placement
   T* d;            // [M][kSTab] stage latencies under the base's uniform config
   T* tail;         // [M]
   T* slo;          // [M]   (clipped to T's range: exact, see header)
   uint32_t* gt;    // [64]  group table: cfg | off<<16 | s<<24
+  uint16_t* hoff;  // [M+1] hosting list of model m in the base: hid[hoff[m] .. hoff[m+1])
+  uint8_t* hid;    // [M*64] group ids, ascending
   uint8_t* rel;    // [M]   some lane of the unit hosts model m
 };
 
 __host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, bool dual) {
   size_t b = (size_t)slots_max * 32 * tsz * (dual ? 2 : 1);
-  b += (size_t)M * (8 + tsz * (kSTab + 2)) + 64 * 4 + ((M + 15) & ~15);
+  b += (size_t)M * tsz * (kSTab + 2) + 64 * 4 + 2 * (size_t)(M + 1);
+  b = (b + 15) & ~size_t(15);
+  b += (size_t)M * 64 + ((M + 15) & ~15);
   return (b + 15) & ~size_t(15);
 }
 
@@ -106,8 +109,7 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   p += slots * 32;
   w.st1 = dual ? p : nullptr;
   if (dual) p += slots * 32;
-  w.mask = reinterpret_cast<uint64_t*>(p);
-  T* q = reinterpret_cast<T*>(w.mask + P.pr.M);
+  T* q = p;
   w.d = q;
   q += P.pr.M * kSTab;
   w.tail = q;
@@ -115,7 +117,11 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   w.slo = q;
   q += P.pr.M;
   w.gt = reinterpret_cast<uint32_t*>(q);
-  w.rel = reinterpret_cast<uint8_t*>(w.gt + 64);
+  w.hoff = reinterpret_cast<uint16_t*>(w.gt + 64);
+  unsigned char* r = reinterpret_cast<unsigned char*>(w.hoff + P.pr.M + 1);
+  r = base + ((r - base + 15) & ~(ptrdiff_t)15);
+  w.hid = r;
+  w.rel = r + (size_t)P.pr.M * 64;
   return w;
 }
 
@@ -124,8 +130,30 @@ template <typename T>
 __device__ void load_base(const ChunkParams& P, const ItemDesc& it, WarpMem<T>& w, int lane) {
   const int M = P.pr.M, PP = P.pr.P, SS = P.pr.S;
   const uint64_t* bm = P.bt.base_mask + (int64_t)it.base * M;
+  // hosting lists: prefix sum of popcounts, then every lane fills its models
+  int base_off = 0;
+  for (int m0 = 0; m0 < M; m0 += 32) {
+    const int m = m0 + lane;
+    const uint64_t bits = m < M ? bm[m] : 0ull;
+    const int cnt = __popcll(bits);
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int start = base_off + incl - cnt;
+    if (m < M) {
+      w.hoff[m] = (uint16_t)start;
+      uint64_t b = bits;
+      for (int r = start; b; ++r) {
+        w.hid[r] = (uint8_t)(__ffsll((long long)b) - 1);
+        b &= b - 1;
+      }
+    }
+    base_off += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+  if (lane == 0) w.hoff[M] = (uint16_t)base_off;
   for (int m = lane; m < M; m += 32) {
-    w.mask[m] = bm[m];
     w.slo[m] = TT<T>::clip(P.pr.slo[m]);
     if (it.cfg >= 0) {
       const int64_t* d = P.pr.stage + ((int64_t)m * PP + it.cfg) * SS;
@@ -200,13 +228,13 @@ __device__ __forceinline__ void commit(const ChunkParams& P, const WarpMem<T>& w
 // index on ties), admission at receipt, commit.  Returns latency or -1.
 template <typename T, int S>
 __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& w, T* st, int lane,
-                                        uint64_t mask, int m, T ar, const T* dv, T tl, T sl,
-                                        unsigned long long& upd) {
+                                        int m, bool mine, int my_g, bool active, T ar,
+                                        const T* dv, T tl, T sl, unsigned long long& upd) {
   T best_f = TT<T>::maxv();
-  int best_g = -1;
-  while (mask) {  // ascending g, strict '<': lowest index wins ties (C1)
-    const int g = __ffsll((long long)mask) - 1;
-    mask &= mask - 1;
+  int best_g = 64;
+  const int h0 = w.hoff[m], h1 = w.hoff[m + 1];
+  for (int h = h0; h < h1; ++h) {  // the base's hosts, ascending: strict '<' keeps the lowest (C1)
+    const int g = w.hid[h];
     if (S > 0) upd += S;
     else upd += (w.gt[g] >> 24);
     const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
@@ -215,7 +243,16 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
       best_g = g;
     }
   }
-  if (best_g >= 0 && (T)(best_f - ar) <= sl) {  // reject at receipt if the SLO is missed (C2, C3)
+  if (mine) {  // this lane's added replica; ties resolved by group index
+    if (S > 0) upd += S;
+    else upd += (w.gt[my_g] >> 24);
+    const T f = predict<T, S>(P, w, st, lane, my_g, m, ar, dv, tl);
+    if (f < best_f || (f == best_f && my_g < best_g)) {
+      best_f = f;
+      best_g = my_g;
+    }
+  }
+  if (active && best_g < 64 && (T)(best_f - ar) <= sl) {  // reject at receipt if the SLO is missed (C2, C3)
     if constexpr (S == 1) {
       st[best_g * 32 + lane] = best_f - tl;  // one stage: its departure is f - tail
     } else {
@@ -276,16 +313,15 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
   const int my_m = in_item ? P.bt.cand_model[c] : -1;
   const int my_g = in_item ? P.bt.cand_group[c] : 0;
   const bool active = in_item && P.bt.cand_ok[c];
-  const uint64_t my_bit = (my_m >= 0 && active) ? (1ull << my_g) : 0ull;
   const int slots = it.slots;
   const int M = P.pr.M;
   const int64_t slot_id = (int64_t)item * 32 + lane;
   const int64_t unit = (int64_t)j * P.num_items + item;
 
   // relevance: models hosted by the base or added by some active lane
-  for (int m = lane; m < M; m += 32) w.rel[m] = w.mask[m] != 0ull;
+  for (int m = lane; m < M; m += 32) w.rel[m] = w.hoff[m + 1] != w.hoff[m];
   __syncwarp();
-  if (my_bit) w.rel[my_m] = 1;
+  if (active && my_m >= 0) w.rel[my_m] = 1;
 
   // initial states
   int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
@@ -358,8 +394,7 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
       const int m = __shfl_sync(FULL, mi, jj);
       maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
       const T ar = (T)(a - E);
-      uint64_t mask = w.mask[m] | ((m == my_m) ? my_bit : 0ull);
-      if (!active) mask = 0ull;
+      const bool mine = active && m == my_m;
       T tl = 0;
       if constexpr (S > 0) {
 #pragma unroll
@@ -367,13 +402,15 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
         tl = w.tail[m];
       }
       const T sl = w.slo[m];
-      const int64_t l0 = step<T, S>(P, w, w.st0, lane, mask, m, ar, dv, tl, sl, upd);
+      const int64_t l0 =
+          step<T, S>(P, w, w.st0, lane, m, mine, my_g, active, ar, dv, tl, sl, upd);
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
       }
       if constexpr (MODE == DUAL) {
-        const int64_t l1 = step<T, S>(P, w, w.st1, lane, mask, m, ar, dv, tl, sl, upd);
+        const int64_t l1 =
+            step<T, S>(P, w, w.st1, lane, m, mine, my_g, active, ar, dv, tl, sl, upd);
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;

@@ -34,6 +34,13 @@ struct DevBatch {
   const int32_t* cand_model;    // [C]  -1 = none
   const int32_t* cand_group;    // [C]
   const uint8_t* cand_ok;       // [C]  0 = infeasible (good = -1)
+  // Component restriction (chunked path, nullable = simulate everything):
+  // lane c only simulates requests of the models in cand_kmask[c] and only
+  // compares the stage slots of the groups in cand_gmask[c] -- the candidate's
+  // own connected component; every other component evolves exactly like the
+  // base placement's (search.cpp).  Requires M <= 64.
+  const uint64_t* cand_kmask;   // [C]
+  const uint64_t* cand_gmask;   // [C]
   int64_t C;
 };
 
@@ -106,7 +113,15 @@ struct ChunkParams {
   const int32_t* spec_row;     // [B] row of base b in spec_state
   int32_t state_stride;        // slots per boundary row of spec_state / published states
   unsigned long long* walked;  // nullable statistics: chunks re-simulated by the walk pass
+  // Per-model good counts (nullable; one-lane items such as the search's base
+  // pass): spec_pm / fix_pm [J][items][M] int32, like spec_good / fix_good.
+  int32_t* spec_pm;
+  int32_t* fix_pm;
 };
+
+// Per-model totals of lane 0 of each item: pm_out[item][m] (int64).
+cudaError_t launch_pm_reduce(const ChunkParams& P, int64_t* pm_out, cudaStream_t st,
+                             int64_t* launches);
 
 // Publish the true state at every chunk boundary of lane 0 of each item:
 // out[(out_row[item] * J + j) * state_stride + k] (absolute int64),

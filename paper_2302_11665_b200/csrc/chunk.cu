@@ -90,13 +90,14 @@ struct WarpMem {
   uint16_t* hoff;  // [M+1] hosting list of model m in the base: hid[hoff[m] .. hoff[m+1])
   uint8_t* hid;    // [M*64] group ids, ascending
   uint8_t* rel;    // [M]   some lane of the unit hosts model m
+  uint8_t* sgrp;   // [128] group of each stage slot
 };
 
 __host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, bool dual) {
   size_t b = (size_t)slots_max * 32 * tsz * (dual ? 2 : 1);
   b += (size_t)M * tsz * (kSTab + 2) + 64 * 4 + 2 * (size_t)(M + 1);
   b = (b + 15) & ~size_t(15);
-  b += (size_t)M * 64 + ((M + 15) & ~15);
+  b += (size_t)M * 64 + ((M + 15) & ~15) + 128;
   return (b + 15) & ~size_t(15);
 }
 
@@ -122,6 +123,7 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   r = base + ((r - base + 15) & ~(ptrdiff_t)15);
   w.hid = r;
   w.rel = r + (size_t)P.pr.M * 64;
+  w.sgrp = w.rel + ((P.pr.M + 15) & ~15);
   return w;
 }
 
@@ -171,6 +173,7 @@ __device__ void load_base(const ChunkParams& P, const ItemDesc& it, WarpMem<T>& 
         if (cfg >= 0) {
           const int s = P.pr.cfg_stages[cfg];
           e = (uint32_t)cfg | ((uint32_t)off << 16) | ((uint32_t)s << 24);
+          for (int k = 0; k < s && off + k < 128; ++k) w.sgrp[off + k] = (uint8_t)g;
           off += s;
         }
       }
@@ -317,11 +320,29 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
   const int M = P.pr.M;
   const int64_t slot_id = (int64_t)item * 32 + lane;
   const int64_t unit = (int64_t)j * P.num_items + item;
+  // the lane's own component (models simulated, groups compared); all else
+  // evolves exactly like the base placement
+  const bool restrict_k = P.bt.cand_kmask != nullptr;
+  const uint64_t kmask = (restrict_k && in_item) ? P.bt.cand_kmask[c] : ~0ull;
+  const uint64_t gmask = (P.bt.cand_gmask && in_item) ? P.bt.cand_gmask[c] : ~0ull;
+  int32_t* pm_row = nullptr;  // per-model counts (one-lane items, e.g. the search's base pass)
+  if (P.spec_pm) pm_row = (MODE == SPEC ? P.spec_pm : P.fix_pm) + unit * M;
 
-  // relevance: models hosted by the base or added by some active lane
-  for (int m = lane; m < M; m += 32) w.rel[m] = w.hoff[m + 1] != w.hoff[m];
-  __syncwarp();
-  if (active && my_m >= 0) w.rel[my_m] = 1;
+  // relevance: models some active lane simulates
+  if (restrict_k) {
+    const uint64_t km = active ? kmask : 0ull;
+    const uint64_t un = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(km >> 32)) << 32) |
+                        __reduce_or_sync(FULL, (uint32_t)km);
+    for (int m = lane; m < M; m += 32) w.rel[m] = (m < 64) && ((un >> m) & 1ull);
+  } else {
+    for (int m = lane; m < M; m += 32) w.rel[m] = w.hoff[m + 1] != w.hoff[m];
+    __syncwarp();
+    if (active && my_m >= 0) w.rel[my_m] = 1;
+  }
+  if constexpr (MODE == WALK) {  // this chunk's per-model correction restarts from -spec
+    if (pm_row)
+      for (int m = lane; m < M; m += 32) pm_row[m] = -P.spec_pm[unit * M + m];
+  }
 
   // initial states
   int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
@@ -379,7 +400,8 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
         const T ar = (T)(a0 - E);
         bool eq = true;
         for (int k = 0; k < slots; ++k)
-          eq &= tmax(w.st0[k * 32 + lane], ar) == tmax(w.st1[k * 32 + lane], ar);
+          if ((gmask >> w.sgrp[k]) & 1ull)
+            eq &= tmax(w.st0[k * 32 + lane], ar) == tmax(w.st1[k * 32 + lane], ar);
         if (__all_sync(FULL, eq || !active)) {
           coalesced = true;
           break;
@@ -394,7 +416,8 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
       const int m = __shfl_sync(FULL, mi, jj);
       maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
       const T ar = (T)(a - E);
-      const bool mine = active && m == my_m;
+      const bool live = active && ((kmask >> (m & 63)) & 1ull);
+      const bool mine = live && m == my_m;
       T tl = 0;
       if constexpr (S > 0) {
 #pragma unroll
@@ -403,17 +426,19 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
       }
       const T sl = w.slo[m];
       const int64_t l0 =
-          step<T, S>(P, w, w.st0, lane, m, mine, my_g, active, ar, dv, tl, sl, upd);
+          step<T, S>(P, w, w.st0, lane, m, mine, my_g, live, ar, dv, tl, sl, upd);
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
+        if (pm_row) atomicAdd(pm_row + m, 1);
       }
       if constexpr (MODE == DUAL) {
         const int64_t l1 =
-            step<T, S>(P, w, w.st1, lane, m, mine, my_g, active, ar, dv, tl, sl, upd);
+            step<T, S>(P, w, w.st1, lane, m, mine, my_g, live, ar, dv, tl, sl, upd);
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;
+          if (pm_row) atomicAdd(pm_row + m, -1);
         }
       }
     }
@@ -452,6 +477,7 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
       const int64_t Es = P.spec_epoch[unit];
       bool eq = true;
       for (int k = 0; k < slots; ++k) {
+        if (!((gmask >> w.sgrp[k]) & 1ull)) continue;
         const int64_t t0 = (TT<T>::kRel ? E : 0) + (int64_t)w.st0[k * 32 + lane];
         const int64_t t1 = (TT<T>::kRel ? Es : 0) + (int64_t)se[k * 32 + lane];
         eq &= (t0 > a_next ? t0 : a_next) == (t1 > a_next ? t1 : a_next);
@@ -570,6 +596,20 @@ __global__ void chunk_reduce_kernel(ChunkParams P, DevOut out) {
   if (out.sum_latency) out.sum_latency[c - out.out_offset] = ok ? s : 0;
 }
 
+__global__ void pm_reduce_kernel(ChunkParams P, int64_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int M = P.pr.M;
+  if (t >= (int64_t)P.num_items * M) return;
+  const int item = (int)(t / M), m = (int)(t % M);
+  int64_t v = 0;
+  for (int j = 0; j < P.J; ++j) {
+    const int64_t row = ((int64_t)j * P.num_items + item) * M + m;
+    v += P.spec_pm[row];
+    if (j > 0) v += P.fix_pm[row];
+  }
+  out[t] = v;
+}
+
 template <typename T>
 __global__ void publish_kernel(ChunkParams P, const uint8_t* __restrict__ end_src,
                                const int32_t* __restrict__ out_row, int64_t* __restrict__ out) {
@@ -661,6 +701,15 @@ cudaError_t launch_publish_states(const ChunkParams& P, const uint8_t* end_src, 
     publish_kernel<uint32_t><<<blocks, 256, 0, st>>>(P, end_src, out_row, out);
   else
     publish_kernel<int64_t><<<blocks, 256, 0, st>>>(P, end_src, out_row, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pm_reduce(const ChunkParams& P, int64_t* pm_out, cudaStream_t st,
+                             int64_t* launches) {
+  const int64_t n = (int64_t)P.num_items * P.pr.M;
+  if (n == 0 || !P.spec_pm) return cudaSuccess;
+  pm_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P, pm_out);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

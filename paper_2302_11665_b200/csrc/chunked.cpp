@@ -115,6 +115,8 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.bt.cand_model = ctx->d_cand_model.as<int32_t>();
   P.bt.cand_group = ctx->d_cand_group.as<int32_t>();
   P.bt.cand_ok = ctx->d_cand_ok.as<uint8_t>();
+  P.bt.cand_kmask = hb.cand_kmask.empty() ? nullptr : ctx->d_cand_kmask.as<uint64_t>();
+  P.bt.cand_gmask = hb.cand_gmask.empty() ? nullptr : ctx->d_cand_gmask.as<uint64_t>();
   P.bt.C = (int64_t)hb.cand_base.size();
   P.items = ctx->c_items.as<asim::ItemDesc>();
   P.num_items = I;
@@ -140,7 +142,19 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   if (P.spec_state && P.state_stride < slots_max)
     return asim_fail(ctx, ASIM_ERANGE, "internal: state stride below slots");
 
-  // ---- pass 1: every (item, chunk) from the idle state
+  // ---- per-model counts of one-lane items (the search's base pass)
+  P.spec_pm = P.fix_pm = nullptr;
+  if (opt && opt->pm_out) {
+    const size_t bytes = (size_t)J * I * hp.M * 4;
+    e = ctx->c_spec_pm.ensure(bytes + 8);
+    if (e == cudaSuccess) e = ctx->c_fix_pm.ensure(bytes + 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_spec_pm.p, 0, bytes, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_fix_pm.p, 0, bytes, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "per-model buffers");
+    P.spec_pm = ctx->c_spec_pm.as<int32_t>();
+    P.fix_pm = ctx->c_fix_pm.as<int32_t>();
+  }
+  // ---- pass 1: every (item, chunk) from the speculative start
   P.num_units = (int32_t)(J * I);
   e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
@@ -161,6 +175,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src");
   }
   e = asim::launch_chunk_reduce(P, out, st, &ctx->launches);
+  if (e == cudaSuccess && P.spec_pm) e = asim::launch_pm_reduce(P, opt->pm_out, st, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk reduce");
   if (opt && opt->publish_out) {  // true boundary states of lane 0 of every item
     e = asim::launch_publish_states(P, end_src, u32, opt->publish_row, opt->publish_out, st,

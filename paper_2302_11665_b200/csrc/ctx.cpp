@@ -146,6 +146,8 @@ asim_status asim_upload_batch(asim_ctx* ctx, const HostBatch& hb, cudaStream_t s
   if (e == cudaSuccess) e = upload(ctx->d_cand_model, hb.cand_model, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_group, hb.cand_group, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_ok, hb.cand_ok, st);
+  if (e == cudaSuccess && !hb.cand_kmask.empty()) e = upload(ctx->d_cand_kmask, hb.cand_kmask, st);
+  if (e == cudaSuccess && !hb.cand_gmask.empty()) e = upload(ctx->d_cand_gmask, hb.cand_gmask, st);
   return asim_cuda(ctx, e, "upload batch");
 }
 
@@ -164,6 +166,11 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
   bool chunked = ctx->force_path >= 2 ||
                  (ctx->force_path == 0 && shared_bases && asim_chunked_eligible(ctx, hb, out));
   if (ctx->force_path >= 2 && !asim_chunked_eligible(ctx, hb, out)) chunked = false;
+  if (!hb.cand_kmask.empty()) {  // component-restricted batches only exist on the chunked path
+    if (!asim_chunked_eligible(ctx, hb, out))
+      return asim_fail(ctx, ASIM_ESTATE, "internal: restricted batch not chunk-eligible");
+    chunked = true;
+  }
   if (chunked) {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (ctx->profiling) {
@@ -208,6 +215,8 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
   b.cand_model = ctx->d_cand_model.as<int32_t>();
   b.cand_group = ctx->d_cand_group.as<int32_t>();
   b.cand_ok = ctx->d_cand_ok.as<uint8_t>();
+  b.cand_kmask = nullptr;  // the general kernel simulates whole placements
+  b.cand_gmask = nullptr;
   b.C = C;
   asim::DevOut o = out;
   o.stage_updates = nullptr;
@@ -273,7 +282,8 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->d_argmax, &ctx->d_counter, &ctx->d_walked, &ctx->c_items, &ctx->c_begin,
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
-                    &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src};
+                    &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src, &ctx->d_cand_kmask,
+                    &ctx->d_cand_gmask, &ctx->c_spec_pm, &ctx->c_fix_pm};
     for (DBuf* b : bufs) b->release();
   }
   delete ctx;

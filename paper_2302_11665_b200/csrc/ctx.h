@@ -77,6 +77,7 @@ struct asim_ctx {
 
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;
+  DBuf d_cand_kmask, d_cand_gmask, c_spec_pm, c_fix_pm;
   DBuf d_good, d_sum, d_pm, d_argmax;
 
   asim::DevProblem dev_problem() const {
@@ -120,6 +121,7 @@ struct HostBatch {
   std::vector<uint64_t> base_mask; // [B][M]
   std::vector<int32_t> cand_base, cand_model, cand_group;
   std::vector<uint8_t> cand_ok;
+  std::vector<uint64_t> cand_kmask, cand_gmask;  // optional component restriction
   int32_t slots = 1;               // max over bases of sum of stages
 };
 // Upload a batch and launch the simulation of candidates [0, C) writing
@@ -139,6 +141,7 @@ struct ChunkOptions {
   int32_t state_stride = 0;
   int64_t* publish_out = nullptr;        // true boundary states of lane 0 of each item
   const int32_t* publish_row = nullptr;  // [items] device
+  int64_t* pm_out = nullptr;             // per-model good of lane 0 of each item [items][M]
 };
 bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out);
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,

@@ -101,6 +101,11 @@ struct asim_search {
   DBuf state_prev, state_cur, d_rows, d_base_good;
   bool base_ready = false;
   HostBatch hb_base;        // one candidate per base: the base itself
+  // Component restriction: simulated candidates only replay their own
+  // component; good = good(base) - good_base(K_c) + good_c(K_c).
+  bool restrict_k = false;
+  DBuf d_base_pm;                // [B][M] per-model good of every base (base pass)
+  std::vector<int64_t> h_base_pm;
   // statistics
   int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0;
   bool finished = false;
@@ -178,6 +183,12 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
   s->stride = stride;
   s->J = std::max<int64_t>(1, std::min<int64_t>(1024, ctx->n / std::max<int64_t>(1, ctx->min_chunk)));
   s->use_states = ctx->force_path != 1;  // the general kernel has no time chunks
+  {
+    HostBatch probe_hb;
+    probe_hb.slots = stride;
+    asim::DevOut probe{};
+    s->restrict_k = s->use_states && hp.M <= 64 && asim_chunked_eligible(ctx, probe_hb, probe);
+  }
   if (s->use_states && !s->runs.empty()) {
     const size_t bytes = s->runs.size() * (size_t)s->J * stride * 8;
     cudaError_t e = s->state_prev.ensure(bytes);
@@ -197,6 +208,7 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
 void asim_search_destroy(asim_search* s) {
   if (!s) return;
   s->d_good_all.release();
+  s->d_base_pm.release();
   s->state_prev.release();
   s->state_cur.release();
   s->d_rows.release();
@@ -228,6 +240,15 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
       for (int32_t g = 0; g < run.G; ++g)
         if ((run.sel[m] >> g) & 1ULL) empty[g] = 0;
     run.cands.clear();
+    // components of the base: models / groups per root (restriction masks)
+    std::vector<uint64_t> rootK, rootG;
+    Components comp(run.G, M, run.sel);
+    if (s->restrict_k) {
+      rootK.assign(run.G + M, 0);
+      rootG.assign(run.G + M, 0);
+      for (int32_t g = 0; g < run.G; ++g) rootG[comp.find(g)] |= 1ULL << g;
+      for (int32_t m = 0; m < M; ++m) rootK[comp.find(run.G + m)] |= 1ULL << m;
+    }
     for (int32_t m = 0; m < M; ++m) {
       std::map<std::pair<int32_t, int32_t>, int64_t> seen;  // (cfg, rank among hosts) -> rep
       for (int32_t g = 0; g < run.G; ++g) {
@@ -258,6 +279,11 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
           hb.cand_model.push_back(m);
           hb.cand_group.push_back(g);
           hb.cand_ok.push_back(1);
+          if (s->restrict_k) {  // K_c = comp(g) u comp(m) in the base, plus m
+            const int32_t r1 = comp.find(g), r2 = comp.find(run.G + m);
+            hb.cand_kmask.push_back(rootK[r1] | rootK[r2] | (1ULL << m));
+            hb.cand_gmask.push_back(rootG[r1] | rootG[r2] | (1ULL << g));
+          }
         }
         run.cands.push_back(c);
       }
@@ -330,7 +356,15 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
         if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
         return asim_cuda(s->ctx, e, "base pass buffers");
       }
+      if (s->restrict_k) {
+        e = s->d_base_pm.ensure((size_t)B * s->ctx->hp.M * 8 + 8);
+        if (e != cudaSuccess) {
+          if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
+          return asim_cuda(s->ctx, e, "base per-model buffer");
+        }
+      }
       ChunkOptions ob = opt;
+      ob.pm_out = s->restrict_k ? s->d_base_pm.as<int64_t>() : nullptr;
       ob.spec_state = s->state_prev.as<int64_t>();
       ob.spec_row = s->d_rows.as<int32_t>();
       ob.publish_out = s->state_cur.as<int64_t>();
@@ -376,14 +410,40 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
   }
   const HostProblem& hp = s->ctx->hp;
   const int32_t M = hp.M;
+  const bool restricted = !s->hb.cand_kmask.empty();
+  if (restricted) {  // per-model good of every base (from the base pass)
+    if (!s->base_ready) return sfail(s, ASIM_ESTATE, "internal: base pass missing");
+    const size_t n = s->base_run.size() * (size_t)M;
+    s->h_base_pm.resize(n);
+    cudaError_t e = cudaMemcpyAsync(s->h_base_pm.data(), s->d_base_pm.p, n * 8,
+                                    cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return asim_cuda(s->ctx, e, "copy base per-model good");
+  }
   for (size_t b = 0; b < s->base_run.size(); ++b) {
     Run& run = s->runs[s->base_run[b]];
+    if (restricted) {  // internal consistency: the base pass reproduces the base's good
+      int64_t tot = 0;
+      for (int32_t m = 0; m < M; ++m) tot += s->h_base_pm[b * M + m];
+      if (tot != run.base_good)
+        return sfail(s, ASIM_ERANGE, "internal: base pass disagrees with the last winner");
+    }
     // every candidate's good: simulated, memo, or its duplicate's representative
     int64_t bi = -1, bg = -1;
     for (size_t i = 0; i < run.cands.size(); ++i) {
       Run::Cand& c = run.cands[i];
-      if (c.kind == 0) c.good = s->h_good[c.ref];
-      else if (c.kind == 2) c.good = run.cands[c.ref].good;
+      if (c.kind == 0) {
+        c.good = s->h_good[c.ref];
+        if (restricted) {  // good(base) - good_base(K_c) + good_c(K_c)
+          const uint64_t km = s->hb.cand_kmask[c.ref];
+          int64_t gk = 0;
+          for (int32_t m = 0; m < M; ++m)
+            if ((km >> m) & 1ULL) gk += s->h_base_pm[b * M + m];
+          c.good += run.base_good - gk;
+        }
+      } else if (c.kind == 2) {
+        c.good = run.cands[c.ref].good;
+      }
       if (c.good > bg) {  // first maximum in (m, g) order: lowest index on ties (C12)
         bg = c.good;
         bi = (int64_t)i;

@@ -231,19 +231,47 @@ __device__ __forceinline__ void commit(const ChunkParams& P, const WarpMem<T>& w
 // index on ties), admission at receipt, commit.  Returns latency or -1.
 template <typename T, int S>
 __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& w, T* st, int lane,
-                                        int m, bool mine, int my_g, bool active, T ar,
-                                        const T* dv, T tl, T sl, unsigned long long& upd) {
+                                        int m, int h0, int h1, bool mine, int my_g, bool active,
+                                        T ar, const T* dv, T tl, T sl, unsigned long long& upd) {
   T best_f = TT<T>::maxv();
   int best_g = 64;
-  const int h0 = w.hoff[m], h1 = w.hoff[m + 1];
-  for (int h = h0; h < h1; ++h) {  // the base's hosts, ascending: strict '<' keeps the lowest (C1)
-    const int g = w.hid[h];
-    if (S > 0) upd += S;
-    else upd += (w.gt[g] >> 24);
-    const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
-    if (f < best_f) {
-      best_f = f;
-      best_g = g;
+  // the base's hosts, ascending: strict '<' keeps the lowest index (C1)
+  if constexpr (S > 0) {
+    // batches of RB hosts: every id and state load of a batch is issued before
+    // the max-plus chains consume them (one shared-memory latency per batch)
+    constexpr int RB = S >= 8 ? 1 : 8 / S;
+    for (int hb = h0; hb < h1; hb += RB) {
+      int g[RB];
+      T v[RB][S];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) g[r] = (hb + r < h1) ? (int)w.hid[hb + r] : -1;
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int k = 0; k < S; ++k) v[r][k] = g[r] >= 0 ? st[(g[r] * S + k) * 32 + lane] : (T)0;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        if (g[r] < 0) break;  // warp-uniform
+        T x = ar;
+#pragma unroll
+        for (int k = 0; k < S; ++k) x = tmax(x, v[r][k]) + dv[k];
+        const T f = x + tl;
+        if (f < best_f) {
+          best_f = f;
+          best_g = g[r];
+        }
+      }
+    }
+    upd += (unsigned long long)(h1 - h0) * S;
+  } else {
+    for (int h = h0; h < h1; ++h) {
+      const int g = w.hid[h];
+      upd += (w.gt[g] >> 24);
+      const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
+      if (f < best_f) {
+        best_f = f;
+        best_g = g;
+      }
     }
   }
   if (mine) {  // this lane's added replica; ties resolved by group index
@@ -271,6 +299,21 @@ __device__ __forceinline__ void rebase(T* st, int slots, int lane, T delta) {
   for (int k = 0; k < slots; ++k) {
     const T v = st[k * 32 + lane];
     st[k * 32 + lane] = v > delta ? v - delta : (T)0;
+  }
+}
+
+// Move the epoch to E_new >= E unconditionally (uint32 only; warp-uniform).
+template <typename T, int MODE>
+__device__ __forceinline__ void rebase_to(WarpMem<T>& w, int slots, int lane, int64_t E_new,
+                                          int64_t& E) {
+  if constexpr (TT<T>::kRel) {
+    if (E_new > E) {
+      const int64_t gap = E_new - E;
+      const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+      rebase<T>(w.st0, slots, lane, delta);
+      if constexpr (MODE == DUAL) rebase<T>(w.st1, slots, lane, delta);
+      E = E_new;
+    }
   }
 }
 
@@ -409,24 +452,51 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
       }
     }
     unsigned todo = __ballot_sync(FULL, valid && w.rel[mi]);
+    if (!todo) continue;  // no lane hosts any of these 32 requests
+    // one epoch for the whole tile when its relevant arrivals fit under theta
+    // (moving the epoch early is exact: any E <= the next arrival works)
+    bool per_req = false;
+    if constexpr (TT<T>::kRel) {
+      const int64_t a_last = __shfl_sync(FULL, ai, 31 - __clz(todo));
+      if (a_last - E > P.theta) {
+        const int64_t a_first = __shfl_sync(FULL, ai, __ffs(todo) - 1);
+        rebase_to<T, MODE>(w, slots, lane, a_first, E);
+        per_req = a_last - E > P.theta;  // a sparse tile: fall back to per-request epochs
+      }
+    }
+    // lane-parallel per-request fields, broadcast below by independent shuffles
+    const T ar_l = (T)(ai - E);
+    const int h0_l = w.hoff[mi], h1_l = w.hoff[mi + 1];
+    const T sl_l = w.slo[mi];
+    T tl_l = 0, d0_l = 0;
+    if constexpr (S > 0) tl_l = w.tail[mi];
+    if constexpr (S == 1) d0_l = w.d[mi * kSTab];
     while (todo) {  // requests some lane hosts, in trace order
       const int jj = __ffs(todo) - 1;
       todo &= todo - 1;
-      const int64_t a = __shfl_sync(FULL, ai, jj);
       const int m = __shfl_sync(FULL, mi, jj);
-      maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
-      const T ar = (T)(a - E);
-      const bool live = active && ((kmask >> (m & 63)) & 1ull);
-      const bool mine = live && m == my_m;
+      T ar = __shfl_sync(FULL, ar_l, jj);
+      const int h0 = __shfl_sync(FULL, h0_l, jj), h1 = __shfl_sync(FULL, h1_l, jj);
+      const T sl = __shfl_sync(FULL, sl_l, jj);
       T tl = 0;
-      if constexpr (S > 0) {
+      if constexpr (S > 0) tl = __shfl_sync(FULL, tl_l, jj);
+      if constexpr (S == 1) {
+        dv[0] = __shfl_sync(FULL, d0_l, jj);
+      } else if constexpr (S > 1) {
 #pragma unroll
         for (int k = 0; k < S; ++k) dv[k] = w.d[m * kSTab + k];
-        tl = w.tail[m];
       }
-      const T sl = w.slo[m];
+      if constexpr (TT<T>::kRel) {
+        if (per_req) {
+          const int64_t a = __shfl_sync(FULL, ai, jj);
+          maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
+          ar = (T)(a - E);
+        }
+      }
+      const bool live = active && ((kmask >> (m & 63)) & 1ull);
+      const bool mine = live && m == my_m;
       const int64_t l0 =
-          step<T, S>(P, w, w.st0, lane, m, mine, my_g, live, ar, dv, tl, sl, upd);
+          step<T, S>(P, w, w.st0, lane, m, h0, h1, mine, my_g, live, ar, dv, tl, sl, upd);
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
@@ -434,7 +504,7 @@ __device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it
       }
       if constexpr (MODE == DUAL) {
         const int64_t l1 =
-            step<T, S>(P, w, w.st1, lane, m, mine, my_g, live, ar, dv, tl, sl, upd);
+            step<T, S>(P, w, w.st1, lane, m, h0, h1, mine, my_g, live, ar, dv, tl, sl, upd);
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;

@@ -103,33 +103,38 @@ __host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, b
 
 template <typename T>
 __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkParams& P, bool dual) {
+  // integer offsets from the shared-memory base only: pointer differences
+  // would hide the address space and turn every LDS into a generic access
   WarpMem<T> w;
-  const int slots = P.slots_max;
-  T* p = reinterpret_cast<T*>(base);
-  w.st0 = p;
-  p += slots * 32;
-  w.st1 = dual ? p : nullptr;
-  if (dual) p += slots * 32;
-  T* q = p;
-  w.d = q;
-  q += P.pr.M * kSTab;
-  w.tail = q;
-  q += P.pr.M;
-  w.slo = q;
-  q += P.pr.M;
-  w.gt = reinterpret_cast<uint32_t*>(q);
-  w.hoff = reinterpret_cast<uint16_t*>(w.gt + 64);
-  unsigned char* r = reinterpret_cast<unsigned char*>(w.hoff + P.pr.M + 1);
-  r = base + ((r - base + 15) & ~(ptrdiff_t)15);
-  w.hid = r;
-  w.rel = r + (size_t)P.pr.M * 64;
-  w.sgrp = w.rel + ((P.pr.M + 15) & ~15);
+  const size_t M = (size_t)P.pr.M;
+  const size_t st_bytes = (size_t)P.slots_max * 32 * sizeof(T);
+  size_t off = 0;
+  w.st0 = reinterpret_cast<T*>(base + off);
+  off += st_bytes;
+  w.st1 = dual ? reinterpret_cast<T*>(base + off) : nullptr;
+  if (dual) off += st_bytes;
+  w.d = reinterpret_cast<T*>(base + off);
+  off += M * kSTab * sizeof(T);
+  w.tail = reinterpret_cast<T*>(base + off);
+  off += M * sizeof(T);
+  w.slo = reinterpret_cast<T*>(base + off);
+  off += M * sizeof(T);
+  w.gt = reinterpret_cast<uint32_t*>(base + off);
+  off += 64 * 4;
+  w.hoff = reinterpret_cast<uint16_t*>(base + off);
+  off += 2 * (M + 1);
+  off = (off + 15) & ~size_t(15);
+  w.hid = base + off;
+  off += M * 64;
+  w.rel = base + off;
+  off += (M + 15) & ~size_t(15);
+  w.sgrp = base + off;
   return w;
 }
 
 // Stage the base placement's tables (lane-parallel).
 template <typename T>
-__device__ void load_base(const ChunkParams& P, const ItemDesc& it, WarpMem<T>& w, int lane) {
+__device__ __forceinline__ void load_base(const ChunkParams& P, const ItemDesc& it, WarpMem<T>& w, int lane) {
   const int M = P.pr.M, PP = P.pr.P, SS = P.pr.S;
   const uint64_t* bm = P.bt.base_mask + (int64_t)it.base * M;
   // hosting lists: prefix sum of popcounts, then every lane fills its models
@@ -239,7 +244,7 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
   if constexpr (S > 0) {
     // batches of RB hosts: every id and state load of a batch is issued before
     // the max-plus chains consume them (one shared-memory latency per batch)
-    constexpr int RB = S >= 8 ? 1 : 8 / S;
+    constexpr int RB = S == 1 ? 2 : 1;  // most models have 1-2 hosts
     for (int hb = h0; hb < h1; hb += RB) {
       int g[RB];
       T v[RB][S];
@@ -351,7 +356,7 @@ __device__ __forceinline__ void load_state(T* dst, const T* src, int64_t Ep, int
 // Simulate one unit (item, chunk j) in MODE.  Returns (WALK) whether the true
 // end state is equivalent to the stored speculative end state of chunk j.
 template <typename T, int S, int MODE>
-__device__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it, int item, int j,
+__device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it, int item, int j,
                          int lane, int src) {
   const int64_t i_begin = P.chunk_begin[j], i_end = P.chunk_begin[j + 1];
   const bool in_item = lane < it.count;

@@ -113,23 +113,18 @@ struct ChunkParams {
   const int32_t* spec_row;     // [B] row of base b in spec_state
   int32_t state_stride;        // slots per boundary row of spec_state / published states
   unsigned long long* walked;  // nullable statistics: chunks re-simulated by the walk pass
-  // Per-model good counts (nullable; one-lane items such as the search's base
-  // pass): spec_pm / fix_pm [J][items][M] int32, like spec_good / fix_good.
-  int32_t* spec_pm;
-  int32_t* fix_pm;
 };
 
-// Per-model totals of lane 0 of each item: pm_out[item][m] (int64).
-cudaError_t launch_pm_reduce(const ChunkParams& P, int64_t* pm_out, cudaStream_t st,
-                             int64_t* launches);
-
-// Publish the true state at every chunk boundary of lane 0 of each item:
-// out[(out_row[item] * J + j) * state_stride + k] (absolute int64),
-// j = 0 is the idle state.  end_src[j * I + i] = 0 if the true end of chunk
-// j is spec_end, 1 if fix_end.
+// Publish the true state at every chunk boundary of chosen lanes (item, lane)
+// into out[(row * J + j) * state_stride + k] (absolute int64; j = 0 idle).
+// end_src[j * items + i] = 0 if the true end of chunk j is spec_end, 1 if
+// fix_end.  Slots outside the lane's component mask come from spec_state.
+struct PublishItem {
+  int32_t item, lane, row;
+};
 cudaError_t launch_publish_states(const ChunkParams& P, const uint8_t* end_src, bool u32,
-                                  const int32_t* out_row, int64_t* out, cudaStream_t st,
-                                  int64_t* launches);
+                                  const PublishItem* pub, int32_t npub, int64_t* out,
+                                  cudaStream_t st, int64_t* launches);
 
 cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStream_t st, int sms,
                               int64_t* launches);

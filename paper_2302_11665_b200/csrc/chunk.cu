@@ -373,8 +373,6 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
   const bool restrict_k = P.bt.cand_kmask != nullptr;
   const uint64_t kmask = (restrict_k && in_item) ? P.bt.cand_kmask[c] : ~0ull;
   const uint64_t gmask = (P.bt.cand_gmask && in_item) ? P.bt.cand_gmask[c] : ~0ull;
-  int32_t* pm_row = nullptr;  // per-model counts (one-lane items, e.g. the search's base pass)
-  if (P.spec_pm) pm_row = (MODE == SPEC ? P.spec_pm : P.fix_pm) + unit * M;
 
   // relevance: models some active lane simulates
   if (restrict_k) {
@@ -386,10 +384,6 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
     for (int m = lane; m < M; m += 32) w.rel[m] = w.hoff[m + 1] != w.hoff[m];
     __syncwarp();
     if (active && my_m >= 0) w.rel[my_m] = 1;
-  }
-  if constexpr (MODE == WALK) {  // this chunk's per-model correction restarts from -spec
-    if (pm_row)
-      for (int m = lane; m < M; m += 32) pm_row[m] = -P.spec_pm[unit * M + m];
   }
 
   // initial states
@@ -505,7 +499,6 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
-        if (pm_row) atomicAdd(pm_row + m, 1);
       }
       if constexpr (MODE == DUAL) {
         const int64_t l1 =
@@ -513,7 +506,6 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;
-          if (pm_row) atomicAdd(pm_row + m, -1);
         }
       }
     }
@@ -671,38 +663,48 @@ __global__ void chunk_reduce_kernel(ChunkParams P, DevOut out) {
   if (out.sum_latency) out.sum_latency[c - out.out_offset] = ok ? s : 0;
 }
 
-__global__ void pm_reduce_kernel(ChunkParams P, int64_t* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int M = P.pr.M;
-  if (t >= (int64_t)P.num_items * M) return;
-  const int item = (int)(t / M), m = (int)(t % M);
-  int64_t v = 0;
-  for (int j = 0; j < P.J; ++j) {
-    const int64_t row = ((int64_t)j * P.num_items + item) * M + m;
-    v += P.spec_pm[row];
-    if (j > 0) v += P.fix_pm[row];
-  }
-  out[t] = v;
-}
-
+// True state at every chunk boundary of chosen lanes: for each PublishItem
+// (item, lane, row), out[(row * J + j) * state_stride + k] (absolute int64).
+// j = 0 is idle.  Slots outside the lane's component mask (cand_gmask) were
+// never simulated by that lane: they evolve exactly like the speculation
+// source (the base placement), whose state at boundary j is copied instead.
 template <typename T>
 __global__ void publish_kernel(ChunkParams P, const uint8_t* __restrict__ end_src,
-                               const int32_t* __restrict__ out_row, int64_t* __restrict__ out) {
+                               const PublishItem* __restrict__ pub, int32_t npub,
+                               int64_t* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)P.num_items * P.J * P.state_stride;
+  const int64_t total = (int64_t)npub * P.J * P.state_stride;
   if (t >= total) return;
   const int k = (int)(t % P.state_stride);
   const int j = (int)((t / P.state_stride) % P.J);
-  const int item = (int)(t / ((int64_t)P.state_stride * P.J));
+  const PublishItem pi = pub[t / ((int64_t)P.state_stride * P.J)];
+  const ItemDesc it = P.items[pi.item];
   int64_t v = 0;  // j == 0: idle; slots beyond the item's: unused
-  if (j > 0 && k < P.items[item].slots) {
-    const int64_t u = (int64_t)(j - 1) * P.num_items + item;  // end of chunk j-1
-    const bool fix = end_src[u] != 0;
-    const T* st = reinterpret_cast<const T*>(fix ? P.fix_end : P.spec_end) + u * P.slots_max * 32;
-    const T x = st[k * 32 + 0];  // lane 0 of the item
-    v = (TT<T>::kRel ? (fix ? P.fix_epoch : P.spec_epoch)[u] : 0) + (int64_t)x;
+  if (j > 0 && k < it.slots) {
+    const int64_t c = (int64_t)it.first + pi.lane;
+    bool own = true;
+    if (P.bt.cand_gmask) {  // group of slot k under the base's group table
+      int g = 0, off = 0;
+      for (; g < P.bt.G; ++g) {
+        const int cfg = P.bt.base_cfg[(int64_t)it.base * P.bt.G + g];
+        if (cfg < 0) continue;
+        const int s = P.pr.cfg_stages[cfg];
+        if (k < off + s) break;
+        off += s;
+      }
+      own = (P.bt.cand_gmask[c] >> g) & 1ull;
+    }
+    if (own || P.spec_state == nullptr) {
+      const int64_t u = (int64_t)(j - 1) * P.num_items + pi.item;  // end of chunk j-1
+      const bool fix = end_src[u] != 0;
+      const T* st = reinterpret_cast<const T*>(fix ? P.fix_end : P.spec_end) + u * P.slots_max * 32;
+      const T x = st[k * 32 + pi.lane];
+      v = (TT<T>::kRel ? (fix ? P.fix_epoch : P.spec_epoch)[u] : 0) + (int64_t)x;
+    } else {
+      v = P.spec_state[((int64_t)P.spec_row[it.base] * P.J + j) * P.state_stride + k];
+    }
   }
-  out[((int64_t)out_row[item] * P.J + j) * P.state_stride + k] = v;
+  out[((int64_t)pi.row * P.J + j) * P.state_stride + k] = v;
 }
 
 template <typename K>
@@ -767,24 +769,15 @@ cudaError_t launch_chunk_walk(const ChunkParams& P, uint8_t* end_src, bool u32, 
 }
 
 cudaError_t launch_publish_states(const ChunkParams& P, const uint8_t* end_src, bool u32,
-                                  const int32_t* out_row, int64_t* out, cudaStream_t st,
-                                  int64_t* launches) {
-  const int64_t total = (int64_t)P.num_items * P.J * P.state_stride;
+                                  const PublishItem* pub, int32_t npub, int64_t* out,
+                                  cudaStream_t st, int64_t* launches) {
+  const int64_t total = (int64_t)npub * P.J * P.state_stride;
   if (total == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((total + 255) / 256);
   if (u32)
-    publish_kernel<uint32_t><<<blocks, 256, 0, st>>>(P, end_src, out_row, out);
+    publish_kernel<uint32_t><<<blocks, 256, 0, st>>>(P, end_src, pub, npub, out);
   else
-    publish_kernel<int64_t><<<blocks, 256, 0, st>>>(P, end_src, out_row, out);
-  if (launches) ++*launches;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pm_reduce(const ChunkParams& P, int64_t* pm_out, cudaStream_t st,
-                             int64_t* launches) {
-  const int64_t n = (int64_t)P.num_items * P.pr.M;
-  if (n == 0 || !P.spec_pm) return cudaSuccess;
-  pm_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P, pm_out);
+    publish_kernel<int64_t><<<blocks, 256, 0, st>>>(P, end_src, pub, npub, out);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -142,18 +142,6 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   if (P.spec_state && P.state_stride < slots_max)
     return asim_fail(ctx, ASIM_ERANGE, "internal: state stride below slots");
 
-  // ---- per-model counts of one-lane items (the search's base pass)
-  P.spec_pm = P.fix_pm = nullptr;
-  if (opt && opt->pm_out) {
-    const size_t bytes = (size_t)J * I * hp.M * 4;
-    e = ctx->c_spec_pm.ensure(bytes + 8);
-    if (e == cudaSuccess) e = ctx->c_fix_pm.ensure(bytes + 8);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_spec_pm.p, 0, bytes, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_fix_pm.p, 0, bytes, st);
-    if (e != cudaSuccess) return asim_cuda(ctx, e, "per-model buffers");
-    P.spec_pm = ctx->c_spec_pm.as<int32_t>();
-    P.fix_pm = ctx->c_fix_pm.as<int32_t>();
-  }
   // ---- pass 1: every (item, chunk) from the speculative start
   P.num_units = (int32_t)(J * I);
   e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);
@@ -175,12 +163,39 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src");
   }
   e = asim::launch_chunk_reduce(P, out, st, &ctx->launches);
-  if (e == cudaSuccess && P.spec_pm) e = asim::launch_pm_reduce(P, opt->pm_out, st, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk reduce");
-  if (opt && opt->publish_out) {  // true boundary states of lane 0 of every item
-    e = asim::launch_publish_states(P, end_src, u32, opt->publish_row, opt->publish_out, st,
-                                    &ctx->launches);
-    if (e != cudaSuccess) return asim_cuda(ctx, e, "publish states");
-  }
+  ctx->last_valid = true;
+  ctx->last_u32 = u32;
+  ctx->last_params = P;
+  ctx->last_items = std::move(items);
   return ASIM_OK;
+}
+
+asim_status asim_publish_candidates(asim_ctx* ctx, const std::vector<int64_t>& cands,
+                                    const std::vector<int32_t>& rows, int64_t* out,
+                                    cudaStream_t st) {
+  if (cands.empty()) return ASIM_OK;
+  if (!ctx->last_valid)
+    return asim_fail(ctx, ASIM_ESTATE, "internal: no chunked run to publish from");
+  std::vector<asim::PublishItem> pub;
+  const auto& items = ctx->last_items;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    const int64_t c = cands[i];
+    // items are in candidate order: find the one holding c
+    size_t lo = 0, hi = items.size();
+    while (hi - lo > 1) {
+      const size_t mid = (lo + hi) / 2;
+      if (items[mid].first <= c) lo = mid;
+      else hi = mid;
+    }
+    if (items.empty() || c < items[lo].first || c >= items[lo].first + items[lo].count)
+      return asim_fail(ctx, ASIM_ESTATE, "internal: candidate not in the last chunked run");
+    pub.push_back(asim::PublishItem{(int32_t)lo, (int32_t)(c - items[lo].first), rows[i]});
+  }
+  cudaError_t e = upload(ctx->c_pub, pub, st);
+  if (e == cudaSuccess)
+    e = asim::launch_publish_states(ctx->last_params, ctx->c_end_src.as<uint8_t>(), ctx->last_u32,
+                                    ctx->c_pub.as<asim::PublishItem>(), (int32_t)pub.size(), out,
+                                    st, &ctx->launches);
+  return asim_cuda(ctx, e, "publish states");
 }

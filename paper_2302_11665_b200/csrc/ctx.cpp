@@ -283,7 +283,7 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
                     &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src, &ctx->d_cand_kmask,
-                    &ctx->d_cand_gmask, &ctx->c_spec_pm, &ctx->c_fix_pm};
+                    &ctx->d_cand_gmask, &ctx->c_pub};
     for (DBuf* b : bufs) b->release();
   }
   delete ctx;

@@ -73,11 +73,17 @@ struct asim_ctx {
   DBuf c_items, c_begin, c_spec_good, c_spec_sum, c_fix_good, c_fix_sum, c_spec_end, c_fix_end,
       c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_end_src;
   int32_t force_path = 0;  // 0 auto, 1 general kernel, 2 chunked kernel (tests)
+  // the last chunked run (its per-unit buffers stay valid until the next one)
+  bool last_valid = false;
+  bool last_u32 = false;
+  asim::ChunkParams last_params{};
+  std::vector<asim::ItemDesc> last_items;
+  DBuf c_pub;
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
 
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;
-  DBuf d_cand_kmask, d_cand_gmask, c_spec_pm, c_fix_pm;
+  DBuf d_cand_kmask, d_cand_gmask;
   DBuf d_good, d_sum, d_pm, d_argmax;
 
   asim::DevProblem dev_problem() const {
@@ -139,11 +145,14 @@ struct ChunkOptions {
   const int64_t* spec_state = nullptr;   // speculation source (device), see ChunkParams
   const int32_t* spec_row = nullptr;     // [B] device
   int32_t state_stride = 0;
-  int64_t* publish_out = nullptr;        // true boundary states of lane 0 of each item
-  const int32_t* publish_row = nullptr;  // [items] device
-  int64_t* pm_out = nullptr;             // per-model good of lane 0 of each item [items][M]
 };
 bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out);
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                              const asim::DevOut& out, cudaStream_t st,
                              const ChunkOptions* opt = nullptr);
+// After a chunked run: true boundary states of chosen candidates of that run
+// (batch index c -> row of `out`, see publish_kernel).  Returns ASIM_ESTATE if
+// a candidate was not part of the last run.
+asim_status asim_publish_candidates(asim_ctx* ctx, const std::vector<int64_t>& cands,
+                                    const std::vector<int32_t>& rows, int64_t* out,
+                                    cudaStream_t st);

@@ -9,25 +9,40 @@
 //             m-major / g-minor ("for (m, (g, p)) in M x (G, P)", P:706;
 //             "if sel' is in memory constraint"); runs without any
 //             stop ("if new_sels = {} then break").
-//   evaluate  the simulation kernel on a contiguous shard of the step's list.
+//   evaluate  the simulation kernels on a contiguous shard of the step's list.
 //   apply     a7: per run, argmax (ties -> lowest index, "pick_highest",
 //             P:722) and sel <- sel + (m*, g*); best_sel on strict '>'.
 //
-// Exact component memo (always on): a placement's simulation splits into
-// independent connected components of the bipartite (group, model) hosting
-// graph -- a request is only ever dispatched among its model's hosts, and a
-// group's stages only see requests of the models it hosts.  Candidate (m, g)
-// of step t whose component K = comp(g) u comp(m) u {m} in base(t-1) is
-// disjoint from the two components the step-(t-1) winner (m*, g*) merged has
-// good_t(m, g) = good_{t-1}(m, g) + good(base(t)) - good(base(t-1)) exactly,
-// so only the other candidates are simulated.
+// Everything below is exact; it only decides what needs simulating.
 //
-// Exact de-duplication (spec->dedup): adding model m to either of two EMPTY
-// groups g1 < g2 with the same config gives the same simulation whenever g1
-// and g2 sit between the same pair of m's hosting groups in index order
-// (relabelling g1 <-> g2 maps one simulation onto the other and preserves
-// every dispatch tie-break, reading C1).  Only the lowest such g -- the one
-// the argmax would pick on a tie anyway -- is listed.
+// Components.  A placement's simulation splits into independent connected
+// components of the bipartite (group, model) hosting graph: a request is only
+// dispatched among its model's hosts, and a group's stages only see requests
+// of the models it hosts.  So good(placement) = sum over components, and
+// candidate c = base + (m, g) differs from its base only inside
+// K_c = comp(g) u comp(m) u {m}:
+//     good(c) = good(base) - good_base(comp(g)) - good_base(comp(m)) + good_c(K_c).
+// The driver keeps every base component's good on the host (updated from the
+// winner's total alone), and the kernels simulate only K_c's requests
+// ("component restriction", chunk.cu).
+//
+// Memo.  Candidate (m, g) of step t whose K_c in base(t-1) is disjoint from
+// the two components the step-(t-1) winner merged has
+//     good_t(m, g) = good_{t-1}(m, g) + good(base(t)) - good(base(t-1)),
+// so it is not simulated again.
+//
+// De-duplication (spec->dedup): adding model m to either of two EMPTY groups
+// g1 < g2 with the same config gives the same simulation whenever g1 and g2
+// sit between the same pair of m's hosting groups in index order (relabelling
+// g1 <-> g2 preserves every dispatch tie-break, reading C1).  Only the lowest
+// such g -- the one the argmax picks on a tie anyway -- is simulated.
+//
+// Speculation states.  The chunked kernels start every time chunk of a
+// candidate from its base's true state at that chunk boundary.  After a step
+// the new base is the winner: its boundary states are published straight
+// from the winner's lane when this rank simulated it (own component from the
+// lane, every other slot from the old base), else a one-lane pass simulates
+// the winner's component again.  Speculation never affects results.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,40 +58,32 @@ namespace {
 struct Run {
   int32_t G = 0;
   std::vector<int32_t> cfg;
-  std::vector<uint64_t> sel;   // [M] current selection
+  std::vector<uint64_t> sel;   // [M] current selection (the base)
   std::vector<int64_t> used;   // [G] bytes per device
   std::vector<uint64_t> best;  // [M] best selection so far
   int64_t best_good = 0;
   bool active = true;
   int64_t steps = 0;
-  int64_t base_good = 0;  // good of the current selection (the last winner)
+  int64_t base_good = 0;       // good of the base (the last winner)
+  // components of the base: union-find over G groups + M models (node G + m)
+  std::vector<int32_t> parent;
+  std::vector<int64_t> cgood;  // good of the component rooted at a node
   // this step's full candidate list, in (m, g) order
   struct Cand {
     int32_t m, g;
-    int8_t kind;    // 0 simulated (ref = batch index), 1 memo (value), 2 duplicate (ref = rep)
+    int8_t kind;  // 0 simulated (ref = batch index), 1 memo (value), 2 duplicate (ref = rep)
     int64_t ref;
     int64_t good;
+    int32_t r1, r2;  // roots of comp(g) and comp(m) in the base
   };
   std::vector<Cand> cands;
-  // memo carried to the next step: (m, g) -> good, valid when the winner is elsewhere
-  std::map<std::pair<int32_t, int32_t>, int64_t> memo;
-  std::vector<std::pair<int32_t, int32_t>> history;  // winners in order
-};
+  std::map<std::pair<int32_t, int32_t>, int64_t> memo;  // (m, g) -> good, for the next step
+  std::vector<std::pair<int32_t, int32_t>> history;     // winners in order
 
-// union-find over G groups + M models (node G + m) of one selection
-struct Components {
-  std::vector<int32_t> p;
-  Components(int32_t G, int32_t M, const std::vector<uint64_t>& sel) : p(G + M) {
-    for (size_t i = 0; i < p.size(); ++i) p[i] = (int32_t)i;
-    for (int32_t m = 0; m < M; ++m)
-      for (int32_t g = 0; g < G; ++g)
-        if ((sel[m] >> g) & 1ULL) unite(g, G + m);
-  }
   int32_t find(int32_t x) {
-    while (p[x] != x) x = p[x] = p[p[x]];
+    while (parent[x] != x) x = parent[x] = parent[parent[x]];
     return x;
   }
-  void unite(int32_t a, int32_t b) { p[find(a)] = find(b); }
 };
 
 }  // namespace
@@ -90,29 +97,41 @@ struct asim_search {
   bool prepared = false;
   HostBatch hb;
   std::vector<int32_t> base_run;  // base -> run id
-  std::vector<int64_t> seg;       // [bases + 1] candidate offsets per base
+  int64_t eval_lo = 0, eval_hi = 0;  // candidates of the last local evaluate call
   DBuf d_good_all;
   std::vector<int64_t> h_good;
-  // Speculation from the base placement's true trajectory (chunk.cu): per run
-  // the absolute free times at every chunk boundary of the current base.
+  // chunking / speculation states: per run, absolute free times at every chunk
+  // boundary of its base (st_base); st_next receives the next base's
   bool use_states = false;
+  bool restrict_k = false;  // component-restricted simulation (M <= 64)
   int64_t J = 1;
-  int32_t stride = 1;       // slots per boundary row
-  DBuf state_prev, state_cur, d_rows, d_base_good;
-  bool base_ready = false;
-  HostBatch hb_base;        // one candidate per base: the base itself
-  // Component restriction: simulated candidates only replay their own
-  // component; good = good(base) - good_base(K_c) + good_c(K_c).
-  bool restrict_k = false;
-  DBuf d_base_pm;                // [B][M] per-model good of every base (base pass)
-  std::vector<int64_t> h_base_pm;
+  int32_t stride = 1;
+  DBuf st_base, st_next, d_rows, d_rows2, d_scratch;
+  bool rows_uploaded = false;
   // statistics
-  int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0;
+  int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0, base_passes = 0;
   bool finished = false;
 };
 
 static asim_status sfail(asim_search* s, asim_status code, const std::string& m) {
   return asim_fail(s ? s->ctx : nullptr, code, m);
+}
+
+// Restriction masks of candidate (m, g): models and groups of K_c.
+static void component_masks(Run& run, int32_t M, int32_t m, int32_t g, uint64_t* kmask,
+                            uint64_t* gmask) {
+  const int32_t r1 = run.find(g), r2 = run.find(run.G + m);
+  uint64_t km = 1ULL << m, gm = 1ULL << g;
+  for (int32_t x = 0; x < run.G; ++x) {
+    const int32_t r = run.find(x);
+    if (r == r1 || r == r2) gm |= 1ULL << x;
+  }
+  for (int32_t x = 0; x < M; ++x) {
+    const int32_t r = run.find(run.G + x);
+    if (r == r1 || r == r2) km |= 1ULL << x;
+  }
+  *kmask = km;
+  *gmask = gm;
 }
 
 extern "C" {
@@ -160,6 +179,7 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
   if (!s) return asim_fail(ctx, ASIM_ENOMEM, "host allocation failed");
   s->ctx = ctx;
   s->dedup = spec->dedup != 0;
+  int32_t stride = 1;
   for (auto& cfg : groups) {
     Run r;
     r.G = (int32_t)cfg.size();
@@ -167,34 +187,36 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     r.sel.assign(hp.M, 0);
     r.best.assign(hp.M, 0);
     r.used.assign(r.G, 0);
+    r.parent.resize(r.G + hp.M);
+    for (size_t i = 0; i < r.parent.size(); ++i) r.parent[i] = (int32_t)i;
+    r.cgood.assign(r.G + hp.M, 0);
     int64_t devices = 0;
-    for (int32_t c : cfg) devices += hp.cfg_devices[c];
+    int32_t slots = 0;
+    for (int32_t c : cfg) {
+      devices += hp.cfg_devices[c];
+      slots += hp.cfg_stages[c];
+    }
+    stride = std::max(stride, slots);
     if (devices > hp.num_devices) r.active = false;  // the empty placement is already infeasible
     s->G = std::max(s->G, r.G);
     s->runs.push_back(std::move(r));
   }
-  // one chunking for the whole search; rows of idle boundary states per run
-  int32_t stride = 1;
-  for (auto& cfg : groups) {
-    int32_t sl = 0;
-    for (int32_t c : cfg) sl += hp.cfg_stages[c];
-    stride = std::max(stride, sl);
-  }
   s->stride = stride;
   s->J = std::max<int64_t>(1, std::min<int64_t>(1024, ctx->n / std::max<int64_t>(1, ctx->min_chunk)));
-  s->use_states = ctx->force_path != 1;  // the general kernel has no time chunks
   {
     HostBatch probe_hb;
     probe_hb.slots = stride;
     asim::DevOut probe{};
-    s->restrict_k = s->use_states && hp.M <= 64 && asim_chunked_eligible(ctx, probe_hb, probe);
+    const bool eligible = asim_chunked_eligible(ctx, probe_hb, probe);
+    s->use_states = ctx->force_path != 1 && eligible;  // the general kernel has no time chunks
+    s->restrict_k = s->use_states && hp.M <= 64;
   }
   if (s->use_states && !s->runs.empty()) {
     const size_t bytes = s->runs.size() * (size_t)s->J * stride * 8;
-    cudaError_t e = s->state_prev.ensure(bytes);
-    if (e == cudaSuccess) e = s->state_cur.ensure(bytes);
-    if (e == cudaSuccess) e = cudaMemset(s->state_prev.p, 0, bytes);
-    if (e == cudaSuccess) e = cudaMemset(s->state_cur.p, 0, bytes);
+    cudaError_t e = s->st_base.ensure(bytes);
+    if (e == cudaSuccess) e = s->st_next.ensure(bytes);
+    if (e == cudaSuccess) e = cudaMemset(s->st_base.p, 0, bytes);  // the empty base: idle
+    if (e == cudaSuccess) e = cudaMemset(s->st_next.p, 0, bytes);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       asim_search_destroy(s);
@@ -207,12 +229,9 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
 
 void asim_search_destroy(asim_search* s) {
   if (!s) return;
-  s->d_good_all.release();
-  s->d_base_pm.release();
-  s->state_prev.release();
-  s->state_cur.release();
-  s->d_rows.release();
-  s->d_base_good.release();
+  DBuf* bufs[] = {&s->d_good_all, &s->st_base, &s->st_next, &s->d_rows, &s->d_rows2,
+                  &s->d_scratch};
+  for (DBuf* b : bufs) b->release();
   delete s;
 }
 
@@ -229,7 +248,8 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   hb = HostBatch();
   hb.G = G;
   s->base_run.clear();
-  s->seg.assign(1, 0);
+  s->eval_lo = s->eval_hi = 0;
+  s->rows_uploaded = false;
   int64_t full = 0;
   for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r) {
     Run& run = s->runs[r];
@@ -240,15 +260,6 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
       for (int32_t g = 0; g < run.G; ++g)
         if ((run.sel[m] >> g) & 1ULL) empty[g] = 0;
     run.cands.clear();
-    // components of the base: models / groups per root (restriction masks)
-    std::vector<uint64_t> rootK, rootG;
-    Components comp(run.G, M, run.sel);
-    if (s->restrict_k) {
-      rootK.assign(run.G + M, 0);
-      rootG.assign(run.G + M, 0);
-      for (int32_t g = 0; g < run.G; ++g) rootG[comp.find(g)] |= 1ULL << g;
-      for (int32_t m = 0; m < M; ++m) rootK[comp.find(run.G + m)] |= 1ULL << m;
-    }
     for (int32_t m = 0; m < M; ++m) {
       std::map<std::pair<int32_t, int32_t>, int64_t> seen;  // (cfg, rank among hosts) -> rep
       for (int32_t g = 0; g < run.G; ++g) {
@@ -256,7 +267,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
         const int64_t mb = hp.mem_at(m, run.cfg[g]);
         if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
         ++full;
-        Run::Cand c{m, g, 0, 0, 0};
+        Run::Cand c{m, g, 0, 0, 0, run.find(g), run.find(run.G + m)};
         auto it = run.memo.find(std::make_pair(m, g));
         if (it != run.memo.end()) {  // component untouched by the last winner
           c.kind = 1;
@@ -279,10 +290,11 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
           hb.cand_model.push_back(m);
           hb.cand_group.push_back(g);
           hb.cand_ok.push_back(1);
-          if (s->restrict_k) {  // K_c = comp(g) u comp(m) in the base, plus m
-            const int32_t r1 = comp.find(g), r2 = comp.find(run.G + m);
-            hb.cand_kmask.push_back(rootK[r1] | rootK[r2] | (1ULL << m));
-            hb.cand_gmask.push_back(rootG[r1] | rootG[r2] | (1ULL << g));
+          if (s->restrict_k) {
+            uint64_t km = 0, gm = 0;
+            component_masks(run, M, m, g, &km, &gm);
+            hb.cand_kmask.push_back(km);
+            hb.cand_gmask.push_back(gm);
           }
         }
         run.cands.push_back(c);
@@ -298,24 +310,9 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
     int32_t slots = 0;
     for (int32_t c : run.cfg) slots += hp.cfg_stages[c];
     hb.slots = std::max(hb.slots, slots);
-    s->seg.push_back((int64_t)hb.cand_base.size());
-  }
-  // the bases themselves (true boundary states for speculation)
-  s->base_ready = false;
-  s->hb_base = HostBatch();
-  s->hb_base.G = G;
-  s->hb_base.base_cfg = hb.base_cfg;
-  s->hb_base.base_mask = hb.base_mask;
-  s->hb_base.slots = hb.slots;
-  for (int32_t b = 0; b < (int32_t)s->base_run.size(); ++b) {
-    s->hb_base.cand_base.push_back(b);
-    s->hb_base.cand_model.push_back(-1);
-    s->hb_base.cand_group.push_back(0);
-    s->hb_base.cand_ok.push_back(1);
   }
   if (s->base_run.empty()) {  // every run has ended: the search is finished
     s->finished = true;
-    s->prepared = false;
     *num_candidates = -1;
     return ASIM_OK;
   }
@@ -342,57 +339,95 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
   asim_status st = ASIM_OK;
   ChunkOptions opt;
   ChunkOptions* popt = nullptr;
-  asim::DevOut probe{};
-  if (s->use_states && asim_chunked_eligible(s->ctx, s->hb, probe)) {
-    const int32_t B = (int32_t)s->base_run.size();
-    opt.J = s->J;
-    opt.state_stride = s->stride;
-    if (!s->base_ready) {
-      // true boundary states of every base: simulate each base (one lane)
-      // speculating from the previous base's states, publish into state_cur
+  if (s->use_states) {
+    if (!s->rows_uploaded) {
       cudaError_t e = upload(s->d_rows, s->base_run, strm);
-      if (e == cudaSuccess) e = s->d_base_good.ensure(B * 8 + 8);
       if (e != cudaSuccess) {
         if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
-        return asim_cuda(s->ctx, e, "base pass buffers");
+        return asim_cuda(s->ctx, e, "upload rows");
       }
-      if (s->restrict_k) {
-        e = s->d_base_pm.ensure((size_t)B * s->ctx->hp.M * 8 + 8);
-        if (e != cudaSuccess) {
-          if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
-          return asim_cuda(s->ctx, e, "base per-model buffer");
-        }
-      }
-      ChunkOptions ob = opt;
-      ob.pm_out = s->restrict_k ? s->d_base_pm.as<int64_t>() : nullptr;
-      ob.spec_state = s->state_prev.as<int64_t>();
-      ob.spec_row = s->d_rows.as<int32_t>();
-      ob.publish_out = s->state_cur.as<int64_t>();
-      ob.publish_row = s->d_rows.as<int32_t>();
-      asim::DevOut bo{};
-      bo.good = s->d_base_good.as<int64_t>();
-      bo.out_offset = 0;
-      st = asim_upload_batch(s->ctx, s->hb_base, strm);
-      if (!st) st = asim_run_chunked(s->ctx, s->hb_base, 0, B, bo, strm, &ob);
-      if (st) {
-        if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
-        return st;
-      }
-      s->base_ready = true;
+      s->rows_uploaded = true;
     }
-    opt.spec_state = s->state_cur.as<int64_t>();
+    opt.J = s->J;
+    opt.state_stride = s->stride;
+    opt.spec_state = s->st_base.as<int64_t>();
     opt.spec_row = s->d_rows.as<int32_t>();
     popt = &opt;
   }
-  asim::DevOut out;
+  asim::DevOut out{};
   out.good = good_dev;
-  out.sum_latency = nullptr;
-  out.good_per_model = nullptr;
   out.out_offset = begin;
-  out.stage_updates = nullptr;
   st = asim_run_batch(s->ctx, s->hb, begin, end, out, strm, popt);
+  if (!st) {
+    s->eval_lo = begin;  // the chunk buffers now hold these candidates' trajectories
+    s->eval_hi = end;
+  }
   if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
   return st;
+}
+
+// New bases' boundary states into st_next, then swap: winners this rank
+// simulated are published from their lanes; the others are simulated again,
+// one lane each, restricted to their own component.
+static asim_status update_states(asim_search* s, const std::vector<int32_t>& winner_run,
+                                 const std::vector<const Run::Cand*>& winner, cudaStream_t st) {
+  asim_ctx* ctx = s->ctx;
+  const int32_t M = ctx->hp.M;
+  std::vector<int64_t> pub_c;
+  std::vector<int32_t> pub_r;
+  HostBatch hb;
+  hb.G = s->G;
+  std::vector<int32_t> rows;
+  for (size_t i = 0; i < winner_run.size(); ++i) {
+    const Run::Cand& w = *winner[i];
+    if (w.kind == 0 && w.ref >= s->eval_lo && w.ref < s->eval_hi) {
+      pub_c.push_back(w.ref);
+      pub_r.push_back(winner_run[i]);
+      continue;
+    }
+    Run& run = s->runs[winner_run[i]];  // still the old base here
+    const int32_t b = (int32_t)rows.size();
+    rows.push_back(winner_run[i]);
+    for (int32_t g = 0; g < s->G; ++g) hb.base_cfg.push_back(g < run.G ? run.cfg[g] : -1);
+    hb.base_mask.insert(hb.base_mask.end(), run.sel.begin(), run.sel.end());
+    int32_t slots = 0;
+    for (int32_t c : run.cfg) slots += ctx->hp.cfg_stages[c];
+    hb.slots = std::max(hb.slots, slots);
+    hb.cand_base.push_back(b);
+    hb.cand_model.push_back(w.m);
+    hb.cand_group.push_back(w.g);
+    hb.cand_ok.push_back(1);
+    if (s->restrict_k) {
+      uint64_t km = 0, gm = 0;
+      component_masks(run, M, w.m, w.g, &km, &gm);
+      hb.cand_kmask.push_back(km);
+      hb.cand_gmask.push_back(gm);
+    }
+  }
+  asim_status rc = asim_publish_candidates(ctx, pub_c, pub_r, s->st_next.as<int64_t>(), st);
+  if (rc) return rc;
+  if (!rows.empty()) {
+    ++s->base_passes;
+    cudaError_t e = upload(s->d_rows2, rows, st);
+    if (e == cudaSuccess) e = s->d_scratch.ensure(rows.size() * 8 + 8);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "base pass buffers");
+    ChunkOptions ob;
+    ob.J = s->J;
+    ob.state_stride = s->stride;
+    ob.spec_state = s->st_base.as<int64_t>();
+    ob.spec_row = s->d_rows2.as<int32_t>();
+    asim::DevOut bo{};
+    bo.good = s->d_scratch.as<int64_t>();
+    rc = asim_upload_batch(ctx, hb, st);
+    if (!rc) rc = asim_run_chunked(ctx, hb, 0, (int64_t)rows.size(), bo, st, &ob);
+    if (rc) return rc;
+    std::vector<int64_t> all(rows.size());
+    for (size_t i = 0; i < rows.size(); ++i) all[i] = (int64_t)i;
+    rc = asim_publish_candidates(ctx, all, rows, s->st_next.as<int64_t>(), st);
+    if (rc) return rc;
+  }
+  std::swap(s->st_base, s->st_next);
+  return ASIM_OK;
 }
 
 asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void* cuda_stream) {
@@ -409,38 +444,19 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
     if (e != cudaSuccess) return asim_cuda(s->ctx, e, "copy step results");
   }
   const HostProblem& hp = s->ctx->hp;
-  const int32_t M = hp.M;
   const bool restricted = !s->hb.cand_kmask.empty();
-  if (restricted) {  // per-model good of every base (from the base pass)
-    if (!s->base_ready) return sfail(s, ASIM_ESTATE, "internal: base pass missing");
-    const size_t n = s->base_run.size() * (size_t)M;
-    s->h_base_pm.resize(n);
-    cudaError_t e = cudaMemcpyAsync(s->h_base_pm.data(), s->d_base_pm.p, n * 8,
-                                    cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return asim_cuda(s->ctx, e, "copy base per-model good");
-  }
+  std::vector<int32_t> winner_run;
+  std::vector<const Run::Cand*> winner;
   for (size_t b = 0; b < s->base_run.size(); ++b) {
     Run& run = s->runs[s->base_run[b]];
-    if (restricted) {  // internal consistency: the base pass reproduces the base's good
-      int64_t tot = 0;
-      for (int32_t m = 0; m < M; ++m) tot += s->h_base_pm[b * M + m];
-      if (tot != run.base_good)
-        return sfail(s, ASIM_ERANGE, "internal: base pass disagrees with the last winner");
-    }
     // every candidate's good: simulated, memo, or its duplicate's representative
     int64_t bi = -1, bg = -1;
     for (size_t i = 0; i < run.cands.size(); ++i) {
       Run::Cand& c = run.cands[i];
       if (c.kind == 0) {
         c.good = s->h_good[c.ref];
-        if (restricted) {  // good(base) - good_base(K_c) + good_c(K_c)
-          const uint64_t km = s->hb.cand_kmask[c.ref];
-          int64_t gk = 0;
-          for (int32_t m = 0; m < M; ++m)
-            if ((km >> m) & 1ULL) gk += s->h_base_pm[b * M + m];
-          c.good += run.base_good - gk;
-        }
+        if (restricted)  // good(base) - good_base(comp(g)) - good_base(comp(m)) + good_c(K_c)
+          c.good += run.base_good - run.cgood[c.r1] - (c.r2 != c.r1 ? run.cgood[c.r2] : 0);
       } else if (c.kind == 2) {
         c.good = run.cands[c.ref].good;
       }
@@ -450,29 +466,37 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
       }
     }
     if (bi < 0) return sfail(s, ASIM_ERANGE, "step results contain no feasible candidate");
-    const int32_t ms = run.cands[bi].m, gs = run.cands[bi].g;
-    // memo for the next step: candidates whose component avoids the two
-    // components the winner merges keep their good shifted by the base's change
-    Components comp(run.G, M, run.sel);
-    const int32_t w1 = comp.find(gs), w2 = comp.find(run.G + ms);
-    const int64_t shift = bg - run.base_good;
+    winner_run.push_back(s->base_run[b]);
+    winner.push_back(&run.cands[bi]);
+  }
+  if (s->use_states) {  // before the bases change: the update simulates from the old ones
+    asim_status rc = update_states(s, winner_run, winner, st);
+    if (rc) return rc;
+  }
+  for (size_t i = 0; i < winner_run.size(); ++i) {
+    Run& run = s->runs[winner_run[i]];
+    const Run::Cand w = *winner[i];
+    // memo for the next step: candidates whose component avoids the winner's
+    const int64_t shift = w.good - run.base_good;
     run.memo.clear();
-    for (const Run::Cand& c : run.cands) {
-      const int32_t a1 = comp.find(c.g), a2 = comp.find(run.G + c.m);
-      if (a1 != w1 && a1 != w2 && a2 != w1 && a2 != w2)
+    for (const Run::Cand& c : run.cands)
+      if (c.r1 != w.r1 && c.r1 != w.r2 && c.r2 != w.r1 && c.r2 != w.r2)
         run.memo.emplace(std::make_pair(c.m, c.g), c.good + shift);
-    }
-    run.sel[ms] |= 1ULL << gs;
-    run.used[gs] += hp.mem_at(ms, run.cfg[gs]);
-    run.base_good = bg;
-    run.history.emplace_back(ms, gs);
+    // the merged component's good, from the winner's total alone
+    const int64_t merged =
+        w.good - run.base_good + run.cgood[w.r1] + (w.r2 != w.r1 ? run.cgood[w.r2] : 0);
+    run.parent[w.r1] = w.r2;  // unite comp(g*) and comp(m*)
+    run.cgood[w.r2] = merged;
+    run.sel[w.m] |= 1ULL << w.g;
+    run.used[w.g] += hp.mem_at(w.m, run.cfg[w.g]);
+    run.base_good = w.good;
+    run.history.emplace_back(w.m, w.g);
     ++run.steps;
-    if (bg > run.best_good) {  // "if sel*.slo_att > best_sel.slo_att"
-      run.best_good = bg;
+    if (w.good > run.best_good) {  // "if sel*.slo_att > best_sel.slo_att"
+      run.best_good = w.good;
       run.best = run.sel;
     }
   }
-  if (s->base_ready) std::swap(s->state_prev, s->state_cur);  // next step speculates from it
   s->prepared = false;
   return ASIM_OK;
 }
@@ -484,11 +508,13 @@ asim_status asim_search_run(asim_search* s, void* cuda_stream) {
     asim_status st = asim_search_prepare(s, &C);
     if (st) return st;
     if (C < 0) return ASIM_OK;
-    cudaError_t e = s->d_good_all.ensure(C * 8 + 8);
-    if (e != cudaSuccess) return asim_cuda(s->ctx, e, "allocate step results");
-    st = asim_search_evaluate(s, 0, C, s->d_good_all.as<int64_t>(), cuda_stream);
-    if (st) return st;
-    st = asim_search_apply(s, s->d_good_all.as<int64_t>(), cuda_stream);
+    if (C > 0) {
+      cudaError_t e = s->d_good_all.ensure(C * 8 + 8);
+      if (e != cudaSuccess) return asim_cuda(s->ctx, e, "allocate step results");
+      st = asim_search_evaluate(s, 0, C, s->d_good_all.as<int64_t>(), cuda_stream);
+      if (st) return st;
+    }
+    st = asim_search_apply(s, C > 0 ? s->d_good_all.as<int64_t>() : nullptr, cuda_stream);
     if (st) return st;
   }
 }

@@ -80,9 +80,9 @@ class Simulator:
 
     # ------------------------------------------------------------- lifetime
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and A.asim_destroy is not None:  # None at interpreter exit
             A.asim_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         self.close()
@@ -207,9 +207,9 @@ class SearchHandle:
         self.h = h
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and A.asim_search_destroy is not None:
             A.asim_search_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __enter__(self):
         return self

@@ -236,40 +236,51 @@ __device__ __forceinline__ void commit(const ChunkParams& P, const WarpMem<T>& w
 // index on ties), admission at receipt, commit.  Returns latency or -1.
 template <typename T, int S>
 __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& w, T* st, int lane,
-                                        int m, int h0, int h1, bool mine, int my_g, bool active,
-                                        T ar, const T* dv, T tl, T sl, unsigned long long& upd) {
+                                        int m, int hinfo, int h0, bool mine, int my_g,
+                                        bool active, T ar, const T* dv, T tl, T sl,
+                                        unsigned long long& upd) {
+  // hinfo = first host | second host << 8 | host count << 16 (the base's
+  // hosting list of m, ascending); hosts beyond the second come from w.hid
   T best_f = TT<T>::maxv();
   int best_g = 64;
-  // the base's hosts, ascending: strict '<' keeps the lowest index (C1)
+  const int cnt = hinfo >> 16;
+  // ascending hosts, strict '<': the lowest index wins ties (C1)
   if constexpr (S > 0) {
-    // batches of RB hosts: every id and state load of a batch is issued before
-    // the max-plus chains consume them (one shared-memory latency per batch)
-    constexpr int RB = S == 1 ? 2 : 1;  // most models have 1-2 hosts
-    for (int hb = h0; hb < h1; hb += RB) {
-      int g[RB];
-      T v[RB][S];
+    const int g0 = hinfo & 0xFF, g1 = (hinfo >> 8) & 0xFF;
+    T v0[S], v1[S];
 #pragma unroll
-      for (int r = 0; r < RB; ++r) g[r] = (hb + r < h1) ? (int)w.hid[hb + r] : -1;
+    for (int k = 0; k < S; ++k) {  // both hosts' loads in flight together
+      v0[k] = cnt >= 1 ? st[(g0 * S + k) * 32 + lane] : (T)0;
+      v1[k] = cnt >= 2 ? st[(g1 * S + k) * 32 + lane] : (T)0;
+    }
+    if (cnt >= 1) {
+      T x = ar;
 #pragma unroll
-      for (int r = 0; r < RB; ++r)
+      for (int k = 0; k < S; ++k) x = tmax(x, v0[k]) + dv[k];
+      best_f = x + tl;
+      best_g = g0;
+    }
+    if (cnt >= 2) {
+      T x = ar;
 #pragma unroll
-        for (int k = 0; k < S; ++k) v[r][k] = g[r] >= 0 ? st[(g[r] * S + k) * 32 + lane] : (T)0;
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        if (g[r] < 0) break;  // warp-uniform
-        T x = ar;
-#pragma unroll
-        for (int k = 0; k < S; ++k) x = tmax(x, v[r][k]) + dv[k];
-        const T f = x + tl;
-        if (f < best_f) {
-          best_f = f;
-          best_g = g[r];
-        }
+      for (int k = 0; k < S; ++k) x = tmax(x, v1[k]) + dv[k];
+      const T f = x + tl;
+      if (f < best_f) {
+        best_f = f;
+        best_g = g1;
       }
     }
-    upd += (unsigned long long)(h1 - h0) * S;
+    for (int h = h0 + 2; h < h0 + cnt; ++h) {
+      const int g = w.hid[h];
+      const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
+      if (f < best_f) {
+        best_f = f;
+        best_g = g;
+      }
+    }
+    upd += (unsigned long long)cnt * S;
   } else {
-    for (int h = h0; h < h1; ++h) {
+    for (int h = h0; h < h0 + cnt; ++h) {
       const int g = w.hid[h];
       upd += (w.gt[g] >> 24);
       const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
@@ -465,49 +476,69 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
     }
     // lane-parallel per-request fields, broadcast below by independent shuffles
     const T ar_l = (T)(ai - E);
-    const int h0_l = w.hoff[mi], h1_l = w.hoff[mi + 1];
+    const int h0_l = w.hoff[mi];
+    const int cnt_l = w.hoff[mi + 1] - h0_l;
+    const int hinfo_l = (cnt_l >= 1 ? (int)w.hid[h0_l] : 0) |
+                        (cnt_l >= 2 ? (int)w.hid[h0_l + 1] << 8 : 0) | (cnt_l << 16);
     const T sl_l = w.slo[mi];
     T tl_l = 0, d0_l = 0;
     if constexpr (S > 0) tl_l = w.tail[mi];
     if constexpr (S == 1) d0_l = w.d[mi * kSTab];
-    while (todo) {  // requests some lane hosts, in trace order
-      const int jj = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int m = __shfl_sync(FULL, mi, jj);
-      T ar = __shfl_sync(FULL, ar_l, jj);
-      const int h0 = __shfl_sync(FULL, h0_l, jj), h1 = __shfl_sync(FULL, h1_l, jj);
-      const T sl = __shfl_sync(FULL, sl_l, jj);
-      T tl = 0;
-      if constexpr (S > 0) tl = __shfl_sync(FULL, tl_l, jj);
+    // software pipeline: the next request's shuffles issue before this one runs
+    int jj = __ffs(todo) - 1;
+    todo &= todo - 1;
+    int m = __shfl_sync(FULL, mi, jj);
+    T ar = __shfl_sync(FULL, ar_l, jj);
+    int hinfo = __shfl_sync(FULL, hinfo_l, jj), h0 = __shfl_sync(FULL, h0_l, jj);
+    T sl = __shfl_sync(FULL, sl_l, jj), tl = 0, d0 = 0;
+    if constexpr (S > 0) tl = __shfl_sync(FULL, tl_l, jj);
+    if constexpr (S == 1) d0 = __shfl_sync(FULL, d0_l, jj);
+    for (;;) {  // requests some lane hosts, in trace order
+      const int cjj = jj, cm = m, chinfo = hinfo, ch0 = h0;
+      T car = ar;
+      const T csl = sl, ctl = tl;
+      const bool more = todo != 0;
+      if (more) {
+        jj = __ffs(todo) - 1;
+        todo &= todo - 1;
+        m = __shfl_sync(FULL, mi, jj);
+        ar = __shfl_sync(FULL, ar_l, jj);
+        hinfo = __shfl_sync(FULL, hinfo_l, jj);
+        h0 = __shfl_sync(FULL, h0_l, jj);
+        sl = __shfl_sync(FULL, sl_l, jj);
+        if constexpr (S > 0) tl = __shfl_sync(FULL, tl_l, jj);
+      }
       if constexpr (S == 1) {
-        dv[0] = __shfl_sync(FULL, d0_l, jj);
+        dv[0] = d0;
+        if (more) d0 = __shfl_sync(FULL, d0_l, jj);
       } else if constexpr (S > 1) {
 #pragma unroll
-        for (int k = 0; k < S; ++k) dv[k] = w.d[m * kSTab + k];
+        for (int k = 0; k < S; ++k) dv[k] = w.d[cm * kSTab + k];
       }
       if constexpr (TT<T>::kRel) {
         if (per_req) {
-          const int64_t a = __shfl_sync(FULL, ai, jj);
+          const int64_t a = __shfl_sync(FULL, ai, cjj);
           maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
-          ar = (T)(a - E);
+          car = (T)(a - E);
         }
       }
-      const bool live = active && ((kmask >> (m & 63)) & 1ull);
-      const bool mine = live && m == my_m;
-      const int64_t l0 =
-          step<T, S>(P, w, w.st0, lane, m, h0, h1, mine, my_g, live, ar, dv, tl, sl, upd);
+      const bool live = active && ((kmask >> (cm & 63)) & 1ull);
+      const bool mine = live && cm == my_m;
+      const int64_t l0 = step<T, S>(P, w, w.st0, lane, cm, chinfo, ch0, mine, my_g, live, car,
+                                    dv, ctl, csl, upd);
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
       }
       if constexpr (MODE == DUAL) {
-        const int64_t l1 =
-            step<T, S>(P, w, w.st1, lane, m, h0, h1, mine, my_g, live, ar, dv, tl, sl, upd);
+        const int64_t l1 = step<T, S>(P, w, w.st1, lane, cm, chinfo, ch0, mine, my_g, live,
+                                      car, dv, ctl, csl, upd);
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;
         }
       }
+      if (!more) break;
     }
   }
 

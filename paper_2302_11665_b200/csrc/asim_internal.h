@@ -102,7 +102,7 @@ struct ChunkParams {
   int64_t* fix_sum;
   void* fix_end;
   int64_t* fix_epoch;
-  uint8_t* fix_flag;           // [J][items] 1 = not coalesced within the chunk
+  uint32_t* fix_flag;          // [J][items] lanes whose trajectories never met in the chunk
   unsigned long long* stage_updates;  // nullable statistics counter
   // Speculation source (nullable = idle): absolute int64 free times of the
   // base placement's TRUE trajectory at every chunk boundary,
@@ -117,12 +117,13 @@ struct ChunkParams {
 
 // Publish the true state at every chunk boundary of chosen lanes (item, lane)
 // into out[(row * J + j) * state_stride + k] (absolute int64; j = 0 idle).
-// end_src[j * items + i] = 0 if the true end of chunk j is spec_end, 1 if
-// fix_end.  Slots outside the lane's component mask come from spec_state.
+// Bit `lane` of end_src[j * items + i] = 0 if that lane's true end of chunk j
+// is in spec_end, 1 if in fix_end.  Slots outside the lane's component mask
+// come from spec_state.
 struct PublishItem {
   int32_t item, lane, row;
 };
-cudaError_t launch_publish_states(const ChunkParams& P, const uint8_t* end_src, bool u32,
+cudaError_t launch_publish_states(const ChunkParams& P, const uint32_t* end_src, bool u32,
                                   const PublishItem* pub, int32_t npub, int64_t* out,
                                   cudaStream_t st, int64_t* launches);
 
@@ -130,10 +131,10 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
                               int64_t* launches);
 cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
                                 int64_t* launches);
-// Pass 3: per item, re-simulate the chunks whose start state was wrong and
-// record for every (j, item) whether chunk j's true end is spec_end (0) or
-// fix_end (1) in end_src[j * items + item].
-cudaError_t launch_chunk_walk(const ChunkParams& P, uint8_t* end_src, bool u32, cudaStream_t st,
-                              int sms, int64_t* launches);
+// Pass 3: re-simulate every chunk whose start state was wrong (per lane) and
+// record in bit `lane` of end_src[j * items + item] whether that lane's true
+// end of chunk j is in spec_end (0) or fix_end (1).
+cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32, bool any_dynamic,
+                              cudaStream_t st, int sms, int64_t* launches);
 
 }  // namespace asim

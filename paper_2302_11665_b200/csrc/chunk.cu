@@ -77,6 +77,10 @@ template <typename T>
 __device__ __forceinline__ T tmax(T a, T b) {
   return a > b ? a : b;
 }
+template <typename T>
+__device__ __forceinline__ T tmin(T a, T b) {
+  return a < b ? a : b;
+}
 
 // Per-warp shared-memory region.
 template <typename T>
@@ -91,6 +95,7 @@ struct WarpMem {
   uint8_t* hid;    // [M*64] group ids, ascending
   uint8_t* rel;    // [M]   some lane of the unit hosts model m
   uint8_t* sgrp;   // [128] group of each stage slot
+  uint64_t* hmask; // [M]   hosting groups of model m (bit set; warp-cooperative walker)
 };
 
 __host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, bool dual) {
@@ -98,6 +103,8 @@ __host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, b
   b += (size_t)M * tsz * (kSTab + 2) + 64 * 4 + 2 * (size_t)(M + 1);
   b = (b + 15) & ~size_t(15);
   b += (size_t)M * 64 + ((M + 15) & ~15) + 128;
+  b = (b + 15) & ~size_t(15);
+  b += (size_t)M * 8;
   return (b + 15) & ~size_t(15);
 }
 
@@ -129,6 +136,9 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   w.rel = base + off;
   off += (M + 15) & ~size_t(15);
   w.sgrp = base + off;
+  off += 128;
+  off = (off + 15) & ~size_t(15);
+  w.hmask = reinterpret_cast<uint64_t*>(base + off);
   return w;
 }
 
@@ -161,6 +171,7 @@ __device__ __forceinline__ void load_base(const ChunkParams& P, const ItemDesc& 
   }
   if (lane == 0) w.hoff[M] = (uint16_t)base_off;
   for (int m = lane; m < M; m += 32) {
+    w.hmask[m] = bm[m];
     w.slo[m] = TT<T>::clip(P.pr.slo[m]);
     if (it.cfg >= 0) {
       const int64_t* d = P.pr.stage + ((int64_t)m * PP + it.cfg) * SS;
@@ -364,11 +375,28 @@ __device__ __forceinline__ void load_state(T* dst, const T* src, int64_t Ep, int
   }
 }
 
+// Store `slots` values of column `lane` relative to the unit's canonical epoch
+// Ec (the chunk's last arrival; every writer of a unit uses it, whatever its
+// own epoch E <= Ec was: clamping below Ec is exact by the equivalence).
+template <typename T>
+__device__ __forceinline__ void store_state(T* out, const T* st, int64_t E, int64_t Ec, int slots,
+                                            int lane, int col) {
+  for (int k = 0; k < slots; ++k) {
+    const T v = st[k * 32 + lane];
+    if constexpr (TT<T>::kRel) {
+      const int64_t r = (int64_t)v - (Ec - E);
+      out[k * 32 + col] = r > 0 ? (T)r : (T)0;
+    } else {
+      out[k * 32 + col] = v;
+    }
+  }
+}
+
 // Simulate one unit (item, chunk j) in MODE.  Returns (WALK) whether the true
 // end state is equivalent to the stored speculative end state of chunk j.
 template <typename T, int S, int MODE>
-__device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it, int item, int j,
-                         int lane, int src) {
+__device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w, const ItemDesc& it,
+                                             int item, int j, int lane, uint32_t srcmask) {
   const int64_t i_begin = P.chunk_begin[j], i_end = P.chunk_begin[j + 1];
   const bool in_item = lane < it.count;
   const int64_t c = (int64_t)it.first + lane;
@@ -416,8 +444,9 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
       for (int k = 0; k < slots; ++k) spec_st[k * 32 + lane] = (T)0;
     }
   }
-  if constexpr (MODE != SPEC) {  // the true trajectory: true end of chunk j-1
+  if constexpr (MODE != SPEC) {  // the true trajectory: true end of chunk j-1 (per lane)
     const int64_t prev = unit - P.num_items;
+    const bool src = (srcmask >> lane) & 1u;
     const T* s0 = reinterpret_cast<const T*>(src ? P.fix_end : P.spec_end) + prev * P.slots_max * 32;
     load_state<T>(w.st0, s0, (src ? P.fix_epoch : P.spec_epoch)[prev], E, slots, lane);
   }
@@ -547,25 +576,37 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
     if (lane == 0) atomicAdd(P.stage_updates, upd);
   }
   const int64_t cstride = (int64_t)P.num_items * 32;
-  bool equivalent = true;
+  const int64_t Ec = P.tr.arrival[i_end - 1];  // the unit's canonical epoch
+  uint32_t eqmask = FULL;
   if constexpr (MODE == SPEC) {
     P.spec_good[j * cstride + slot_id] = (int32_t)good0;
     P.spec_sum[j * cstride + slot_id] = sum0;
     if (j + 1 < P.J) {  // end state for the next chunk's fix-up
-      T* out = reinterpret_cast<T*>(P.spec_end) + unit * P.slots_max * 32;
-      for (int k = 0; k < slots; ++k) out[k * 32 + lane] = w.st0[k * 32 + lane];
-      if (lane == 0) P.spec_epoch[unit] = E;
+      store_state<T>(reinterpret_cast<T*>(P.spec_end) + unit * P.slots_max * 32, w.st0, E, Ec,
+                     slots, lane, lane);
+      if (lane == 0) P.spec_epoch[unit] = Ec;
     }
   } else if constexpr (MODE == DUAL) {
     P.fix_good[j * cstride + slot_id] = (int32_t)(good0 - good1);
     P.fix_sum[j * cstride + slot_id] = sum0 - sum1;
-    if (lane == 0) P.fix_flag[unit] = coalesced ? 0 : 1;
-    if (!coalesced && j + 1 < P.J) {  // publish the true end state
-      T* out = reinterpret_cast<T*>(P.fix_end) + unit * P.slots_max * 32;
-      for (int k = 0; k < slots; ++k) out[k * 32 + lane] = w.st0[k * 32 + lane];
-      if (lane == 0) P.fix_epoch[unit] = E;
+    uint32_t flag = 0;
+    if (!coalesced && j + 1 < P.J) {
+      // lanes whose trajectories differ at the next arrival; publish the true ends
+      const int64_t a_next = P.tr.arrival[i_end];
+      bool eq = true;
+      for (int k = 0; k < slots; ++k) {
+        if (!((gmask >> w.sgrp[k]) & 1ull)) continue;
+        const int64_t t0 = (TT<T>::kRel ? E : 0) + (int64_t)w.st0[k * 32 + lane];
+        const int64_t t1 = (TT<T>::kRel ? E : 0) + (int64_t)w.st1[k * 32 + lane];
+        eq &= (t0 > a_next ? t0 : a_next) == (t1 > a_next ? t1 : a_next);
+      }
+      flag = __ballot_sync(FULL, !eq && active);
+      store_state<T>(reinterpret_cast<T*>(P.fix_end) + unit * P.slots_max * 32, w.st0, E, Ec,
+                     slots, lane, lane);
+      if (lane == 0) P.fix_epoch[unit] = Ec;
     }
-  } else {  // WALK: exact correction of the whole chunk
+    if (lane == 0) P.fix_flag[unit] = flag;
+  } else {  // WALK: exact correction of the whole chunk, every lane from its true start
     P.fix_good[j * cstride + slot_id] = (int32_t)(good0 - P.spec_good[j * cstride + slot_id]);
     P.fix_sum[j * cstride + slot_id] = sum0 - P.spec_sum[j * cstride + slot_id];
     if (j + 1 < P.J) {
@@ -580,21 +621,21 @@ __device__ __forceinline__ bool run_unit(const ChunkParams& P, WarpMem<T>& w, co
         const int64_t t1 = (TT<T>::kRel ? Es : 0) + (int64_t)se[k * 32 + lane];
         eq &= (t0 > a_next ? t0 : a_next) == (t1 > a_next ? t1 : a_next);
       }
-      equivalent = __all_sync(FULL, eq || !active);
-      if (!equivalent) {
-        T* out = reinterpret_cast<T*>(P.fix_end) + unit * P.slots_max * 32;
-        for (int k = 0; k < slots; ++k) out[k * 32 + lane] = w.st0[k * 32 + lane];
-        if (lane == 0) P.fix_epoch[unit] = E;
+      eqmask = __ballot_sync(FULL, eq || !active);
+      if (eqmask != FULL) {
+        store_state<T>(reinterpret_cast<T*>(P.fix_end) + unit * P.slots_max * 32, w.st0, E, Ec,
+                       slots, lane, lane);
+        if (lane == 0) P.fix_epoch[unit] = Ec;
       }
     }
   }
-  return equivalent;
+  return eqmask;
 }
 
 template <typename T, int MODE>
-__device__ __forceinline__ bool dispatch_unit(const ChunkParams& P, WarpMem<T>& w,
-                                              const ItemDesc& it, int item, int j, int lane,
-                                              int src) {
+__device__ __forceinline__ uint32_t dispatch_unit(const ChunkParams& P, WarpMem<T>& w,
+                                                  const ItemDesc& it, int item, int j, int lane,
+                                                  uint32_t src) {
   switch (it.S) {
     case 1: return run_unit<T, 1, MODE>(P, w, it, item, j, lane, src);
     case 2: return run_unit<T, 2, MODE>(P, w, it, item, j, lane, src);
@@ -634,9 +675,12 @@ __global__ void __launch_bounds__(kWarps * 32) chunk_kernel(ChunkParams P) {
   }
 }
 
-// Pass 3: one warp per item walks the chunks whose start state was wrong.
+// Pass 3, items with mixed configs (S == 0): one warp per item walks the
+// chunks in order; where some lane's start state was wrong, every lane is
+// re-simulated from its true start.  end_src[u] gets the lanes whose true end
+// is in fix_end.  Items of uniform configs are walked by coop_walk_kernel.
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) walk_kernel(ChunkParams P, uint8_t* end_src) {
+__global__ void __launch_bounds__(kWarps * 32) walk_kernel(ChunkParams P, uint32_t* end_src) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
@@ -646,15 +690,15 @@ __global__ void __launch_bounds__(kWarps * 32) walk_kernel(ChunkParams P, uint8_
     const int item = next_unit(P, lane);
     if (item >= P.num_items) break;
     const ItemDesc it = P.items[item];
-    if (lane == 0) end_src[item] = 0;  // chunk 0 starts idle: exact
-    bool start_ok = true;  // pass 2 started chunk j from its true start state
+    if (it.S != 0) continue;  // warp-uniform
+    uint32_t start_ok = FULL;  // lanes whose pass-2 start (chunk j-1's spec end) was true
     unsigned long long walked = 0;
     for (int j = 1; j < P.J; ++j) {
       const int64_t u = (int64_t)j * P.num_items + item;
-      if (start_ok) {
-        const bool met = P.fix_flag[u] == 0;  // pass 2's correction is exact
-        if (lane == 0) end_src[u] = met ? 0 : 1;
-        start_ok = met;  // else the true end of chunk j is pass 2's fix_end
+      if (start_ok == FULL) {  // pass 2's corrections of chunk j are exact for every lane
+        const uint32_t f = P.fix_flag[u];
+        if (lane == 0) end_src[u] = f;
+        start_ok = ~f;
         continue;
       }
       if (it.base != cur_base) {
@@ -662,12 +706,254 @@ __global__ void __launch_bounds__(kWarps * 32) walk_kernel(ChunkParams P, uint8_
         cur_base = it.base;
       }
       ++walked;
-      const bool eq = dispatch_unit<T, WALK>(P, w, it, item, j, lane, 1);
-      if (lane == 0) end_src[u] = eq ? 0 : 1;
+      const uint32_t eq = dispatch_unit<T, WALK>(P, w, it, item, j, lane, end_src[u - P.num_items]);
+      if (lane == 0) end_src[u] = ~eq;
       start_ok = eq;
       __syncwarp();
     }
     if (P.walked && lane == 0 && walked) atomicAdd(P.walked, walked);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass 3, uniform configs: the warp-cooperative walker.  One warp per
+// CANDIDATE that needs walking; its state is spread over the lanes in
+// registers (slot t = lane + 32 q lives in v[q]), so a request costs a few
+// register ops, one warp-wide min and one ballot instead of a 32-lane
+// dependent chain through shared memory.  Within a group the S stages sit in
+// S consecutive lanes (32 % S == 0) and the tandem recurrence
+//     y_k = max(y_{k-1}, free_k) + d_k,  y_{-1} = a
+// is evaluated as a max-plus scan: element k = (A_k, B_k) = (d_k, free_k + d_k),
+// (A1, B1) then (A2, B2) = (A1 + A2, max(B1 + A2, B2)), y_k = max(a + A, B).
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+  if constexpr (sizeof(T) == 4) {
+    return (T)__reduce_min_sync(FULL, (unsigned)v);
+  } else {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T x = __shfl_xor_sync(FULL, v, o);
+      v = x < v ? x : v;
+    }
+    return v;
+  }
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpMem<T>& w,
+                                               const ItemDesc& it, int item, int cl, int lane,
+                                               uint32_t* end_src, unsigned long long& walked,
+                                               unsigned long long& upd) {
+  constexpr int Q = 4;  // up to 128 slots
+  const int64_t c = (int64_t)it.first + cl;
+  const int my_m = P.bt.cand_model[c], my_g = P.bt.cand_group[c];
+  const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;
+  const uint64_t gmask = P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull;
+  const uint64_t my_bit = my_m >= 0 ? (1ull << my_g) : 0ull;
+  const int slots = it.slots;
+  const int64_t cstride = (int64_t)P.num_items * 32;
+  bool start_ok = true;
+  for (int j = 1; j < P.J; ++j) {
+    const int64_t u = (int64_t)j * P.num_items + item;
+    if (start_ok) {
+      if ((P.fix_flag[u] >> cl) & 1u) {  // pass 2 exact; true end of j is its fix_end
+        if (lane == 0) atomicOr(end_src + u, 1u << cl);
+        start_ok = false;
+      }
+      continue;
+    }
+    ++walked;
+    const int64_t i_begin = P.chunk_begin[j], i_end = P.chunk_begin[j + 1];
+    int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
+    // true start: chunk j-1's true end, always in fix_end when walking
+    T v[Q];
+    {
+      const int64_t prev = u - P.num_items;
+      const T* s0 = reinterpret_cast<const T*>(P.fix_end) + prev * P.slots_max * 32;
+      const int64_t Ep = P.fix_epoch[prev];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int t = lane + 32 * q;
+        T x = 0;
+        if (t < slots) {
+          const T raw = s0[t * 32 + cl];
+          if constexpr (TT<T>::kRel) {
+            const int64_t r = (int64_t)raw - (E - Ep);
+            x = r > 0 ? (T)r : (T)0;
+          } else {
+            x = raw;
+          }
+        }
+        v[q] = x;
+      }
+    }
+    int64_t good = 0, sum = 0;
+    for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
+      const bool valid = i0 + lane < i_end;
+      const int64_t al = valid ? P.tr.arrival[i0 + lane] : 0;
+      const int ml = valid ? (int)P.tr.model[i0 + lane] : 0;
+      unsigned todo = __ballot_sync(FULL, valid && ((kmask >> (ml & 63)) & 1ull));
+      if (!todo) continue;
+      bool per_req = false;
+      if constexpr (TT<T>::kRel) {
+        const int64_t a_last = __shfl_sync(FULL, al, 31 - __clz(todo));
+        if (a_last - E > P.theta) {  // move the epoch to the tile's first request
+          const int64_t a_first = __shfl_sync(FULL, al, __ffs(todo) - 1);
+          const int64_t gap = a_first - E;
+          const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) v[q] = v[q] > delta ? v[q] - delta : (T)0;
+          E = a_first;
+          per_req = a_last - E > P.theta;
+        }
+      }
+      const T arl = (T)(al - E);
+      while (todo) {
+        const int jj = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int m = __shfl_sync(FULL, ml, jj);
+        T ar = __shfl_sync(FULL, arl, jj);
+        if constexpr (TT<T>::kRel) {
+          if (per_req) {
+            const int64_t a = __shfl_sync(FULL, al, jj);
+            if (a - E > P.theta) {
+              const int64_t gap = a - E;
+              const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) v[q] = v[q] > delta ? v[q] - delta : (T)0;
+              E = a;
+            }
+            ar = (T)(a - E);
+          }
+        }
+        const uint64_t hm = w.hmask[m] | (m == my_m ? my_bit : 0ull);
+        const T tl = w.tail[m], sl = w.slo[m];
+        upd += (unsigned long long)__popcll(hm) * S;
+        // predicted finish at the last stage of every hosting group
+        T y[Q], f[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int t = lane + 32 * q, g = t / S, k = t % S;
+          const T d = w.d[m * kSTab + k];
+          if constexpr (S == 1) {
+            y[q] = tmax(ar, v[q]) + d;
+          } else {
+            T A = d, B = v[q] + d;
+#pragma unroll
+            for (int o = 1; o < S; o <<= 1) {
+              const T A2 = __shfl_up_sync(FULL, A, o, S), B2 = __shfl_up_sync(FULL, B, o, S);
+              if (k >= o) {
+                B = tmax(B2 + A, B);
+                A = A2 + A;
+              }
+            }
+            y[q] = tmax(ar + A, B);
+          }
+          const bool last = (k == S - 1) && t < slots && ((hm >> (g & 63)) & 1ull);
+          f[q] = last ? y[q] + tl : TT<T>::maxv();
+        }
+        T fmin = TT<T>::maxv();
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (32 * q < slots) fmin = tmin(fmin, warp_min<T>(f[q]));
+        if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) continue;  // no host / misses the SLO
+        // lowest group index among the minima (slots ascend with q, then lane)
+        int wq = 0, wl = 0;
+#pragma unroll
+        for (int q = Q - 1; q >= 0; --q) {
+          const unsigned b = __ballot_sync(FULL, f[q] == fmin);
+          if (b) {
+            wq = q;
+            wl = __ffs(b) - 1;
+          }
+        }
+        const int gw = (wl + 32 * wq) / S;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (q == wq && (lane + 32 * q) / S == gw) v[q] = y[q];
+        ++good;
+        sum += (int64_t)(fmin - ar);
+      }
+    }
+    // the chunk's exact correction, and equivalence with the speculative end
+    if (lane == 0) {
+      P.fix_good[j * cstride + (int64_t)item * 32 + cl] =
+          (int32_t)(good - P.spec_good[j * cstride + (int64_t)item * 32 + cl]);
+      P.fix_sum[j * cstride + (int64_t)item * 32 + cl] =
+          sum - P.spec_sum[j * cstride + (int64_t)item * 32 + cl];
+    }
+    if (j + 1 < P.J) {
+      const int64_t a_next = P.tr.arrival[i_end];
+      const T* se = reinterpret_cast<const T*>(P.spec_end) + u * P.slots_max * 32;
+      const int64_t Es = P.spec_epoch[u];
+      bool eq = true;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int t = lane + 32 * q;
+        if (t >= slots || !((gmask >> ((t / S) & 63)) & 1ull)) continue;
+        const int64_t t0 = (TT<T>::kRel ? E : 0) + (int64_t)v[q];
+        const int64_t t1 = (TT<T>::kRel ? Es : 0) + (int64_t)se[t * 32 + cl];
+        eq &= (t0 > a_next ? t0 : a_next) == (t1 > a_next ? t1 : a_next);
+      }
+      start_ok = __all_sync(FULL, eq);
+      if (!start_ok) {  // publish column cl at the unit's canonical epoch
+        const int64_t Ec = P.tr.arrival[i_end - 1];
+        T* out = reinterpret_cast<T*>(P.fix_end) + u * P.slots_max * 32;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int t = lane + 32 * q;
+          if (t >= slots) continue;
+          if constexpr (TT<T>::kRel) {
+            const int64_t r = (int64_t)v[q] - (Ec - E);
+            out[t * 32 + cl] = r > 0 ? (T)r : (T)0;
+          } else {
+            out[t * 32 + cl] = v[q];
+          }
+        }
+        if (lane == 0) {
+          P.fix_epoch[u] = Ec;
+          atomicOr(end_src + u, 1u << cl);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, uint32_t* end_src) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  WarpMem<T> w = carve<T>(smem + warp * wb, P, false);
+  int cur_base = -1;
+  unsigned long long walked = 0, upd = 0;
+  for (;;) {
+    const int u = next_unit(P, lane);  // candidate slot = item * 32 + lane of the item
+    if (u >= P.num_items * 32) break;
+    const int item = u >> 5, cl = u & 31;
+    const ItemDesc it = P.items[item];
+    if (it.S == 0 || cl >= it.count || !P.bt.cand_ok[(int64_t)it.first + cl]) continue;
+    // any chunk of this candidate flagged by pass 2?  (else nothing to walk)
+    bool any = false;
+    for (int j = 1 + lane; j < P.J; j += 32)
+      any |= (P.fix_flag[(int64_t)j * P.num_items + item] >> cl) & 1u;
+    if (!__any_sync(FULL, any)) continue;
+    if (it.base != cur_base) {
+      load_base<T>(P, it, w, lane);
+      cur_base = it.base;
+    }
+    switch (it.S) {
+      case 1: coop_candidate<T, 1>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+      case 2: coop_candidate<T, 2>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+      case 4: coop_candidate<T, 4>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+      case 8: coop_candidate<T, 8>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+      default: coop_candidate<T, 16>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    }
+  }
+  if (lane == 0) {
+    if (P.walked && walked) atomicAdd(P.walked, walked);
+    if (P.stage_updates && upd) atomicAdd(P.stage_updates, upd);
   }
 }
 
@@ -700,7 +986,7 @@ __global__ void chunk_reduce_kernel(ChunkParams P, DevOut out) {
 // never simulated by that lane: they evolve exactly like the speculation
 // source (the base placement), whose state at boundary j is copied instead.
 template <typename T>
-__global__ void publish_kernel(ChunkParams P, const uint8_t* __restrict__ end_src,
+__global__ void publish_kernel(ChunkParams P, const uint32_t* __restrict__ end_src,
                                const PublishItem* __restrict__ pub, int32_t npub,
                                int64_t* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -727,7 +1013,7 @@ __global__ void publish_kernel(ChunkParams P, const uint8_t* __restrict__ end_sr
     }
     if (own || P.spec_state == nullptr) {
       const int64_t u = (int64_t)(j - 1) * P.num_items + pi.item;  // end of chunk j-1
-      const bool fix = end_src[u] != 0;
+      const bool fix = (end_src[u] >> pi.lane) & 1u;
       const T* st = reinterpret_cast<const T*>(fix ? P.fix_end : P.spec_end) + u * P.slots_max * 32;
       const T x = st[k * 32 + pi.lane];
       v = (TT<T>::kRel ? (fix ? P.fix_epoch : P.spec_epoch)[u] : 0) + (int64_t)x;
@@ -766,10 +1052,20 @@ cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
 }
 
 template <typename T>
-cudaError_t launch_walk_t(const ChunkParams& P, uint8_t* end_src, cudaStream_t st, int sms) {
+cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, cudaStream_t st, int sms,
+                          bool any_dynamic) {
   const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
   int64_t blocks = 1;
-  cudaError_t e = grid_for(walk_kernel<T>, smem, P.num_items, sms, &blocks);
+  cudaError_t e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  e = grid_for(coop_walk_kernel<T>, smem, (int64_t)P.num_items * 32, sms, &blocks);
+  if (e != cudaSuccess) return e;
+  coop_walk_kernel<T><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !any_dynamic) return e;
+  e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  e = grid_for(walk_kernel<T>, smem, P.num_items, sms, &blocks);
   if (e != cudaSuccess) return e;
   walk_kernel<T><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
   return cudaGetLastError();
@@ -790,16 +1086,17 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
   return e;
 }
 
-cudaError_t launch_chunk_walk(const ChunkParams& P, uint8_t* end_src, bool u32, cudaStream_t st,
-                              int sms, int64_t* launches) {
-  cudaError_t e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
+cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32, bool any_dynamic,
+                              cudaStream_t st, int sms, int64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(end_src, 0, (size_t)P.J * P.num_items * 4, st);
   if (e != cudaSuccess) return e;
-  e = u32 ? launch_walk_t<uint32_t>(P, end_src, st, sms) : launch_walk_t<int64_t>(P, end_src, st, sms);
-  if (launches) ++*launches;
+  e = u32 ? launch_walk_t<uint32_t>(P, end_src, st, sms, any_dynamic)
+          : launch_walk_t<int64_t>(P, end_src, st, sms, any_dynamic);
+  if (launches) *launches += any_dynamic ? 2 : 1;
   return e;
 }
 
-cudaError_t launch_publish_states(const ChunkParams& P, const uint8_t* end_src, bool u32,
+cudaError_t launch_publish_states(const ChunkParams& P, const uint32_t* end_src, bool u32,
                                   const PublishItem* pub, int32_t npub, int64_t* out,
                                   cudaStream_t st, int64_t* launches) {
   const int64_t total = (int64_t)npub * P.J * P.state_stride;

@@ -101,7 +101,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   if (e == cudaSuccess) e = ctx->c_fix_end.ensure(J * I * (int64_t)slots_max * 32 * tsz);
   if (e == cudaSuccess) e = ctx->c_spec_epoch.ensure(J * I * 8);
   if (e == cudaSuccess) e = ctx->c_fix_epoch.ensure(J * I * 8);
-  if (e == cudaSuccess) e = ctx->c_flag.ensure(J * I);
+  if (e == cudaSuccess) e = ctx->c_flag.ensure(J * I * 4 + 8);
   if (e == cudaSuccess) e = ctx->c_counter.ensure(16);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk buffers");
 
@@ -133,7 +133,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.fix_sum = ctx->c_fix_sum.as<int64_t>();
   P.fix_end = ctx->c_fix_end.p;
   P.fix_epoch = ctx->c_fix_epoch.as<int64_t>();
-  P.fix_flag = ctx->c_flag.as<uint8_t>();
+  P.fix_flag = ctx->c_flag.as<uint32_t>();
   P.stage_updates = out.stage_updates;
   P.walked = ctx->profiling ? ctx->d_walked.as<unsigned long long>() : nullptr;
   P.spec_state = opt ? opt->spec_state : nullptr;
@@ -147,19 +147,21 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
 
-  e = ctx->c_end_src.ensure(J * I + 8);
+  e = ctx->c_end_src.ensure(J * I * 4 + 8);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src buffer");
-  uint8_t* end_src = ctx->c_end_src.as<uint8_t>();
+  uint32_t* end_src = ctx->c_end_src.as<uint32_t>();
+  bool any_dynamic = false;
+  for (const auto& it : items) any_dynamic |= it.S == 0;
   if (J > 1) {
     // ---- pass 2: fix-up of every chunk j >= 1 from chunk j-1's speculative end
     P.num_units = (int32_t)((J - 1) * I);
     e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 2");
     // ---- pass 3: walk the chunks whose start state was wrong (exact chains)
-    e = asim::launch_chunk_walk(P, end_src, u32, st, ctx->sms, &ctx->launches);
+    e = asim::launch_chunk_walk(P, end_src, u32, any_dynamic, st, ctx->sms, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk walk");
   } else {
-    e = cudaMemsetAsync(end_src, 0, J * I, st);
+    e = cudaMemsetAsync(end_src, 0, J * I * 4, st);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src");
   }
   e = asim::launch_chunk_reduce(P, out, st, &ctx->launches);
@@ -194,7 +196,7 @@ asim_status asim_publish_candidates(asim_ctx* ctx, const std::vector<int64_t>& c
   }
   cudaError_t e = upload(ctx->c_pub, pub, st);
   if (e == cudaSuccess)
-    e = asim::launch_publish_states(ctx->last_params, ctx->c_end_src.as<uint8_t>(), ctx->last_u32,
+    e = asim::launch_publish_states(ctx->last_params, ctx->c_end_src.as<uint32_t>(), ctx->last_u32,
                                     ctx->c_pub.as<asim::PublishItem>(), (int32_t)pub.size(), out,
                                     st, &ctx->launches);
   return asim_cuda(ctx, e, "publish states");

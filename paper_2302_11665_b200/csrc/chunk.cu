@@ -739,12 +739,12 @@ __device__ __forceinline__ T warp_min(T v) {
   }
 }
 
-template <typename T, int S>
+template <typename T, int S, int Q>
 __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpMem<T>& w,
                                                const ItemDesc& it, int item, int cl, int lane,
                                                uint32_t* end_src, unsigned long long& walked,
                                                unsigned long long& upd) {
-  constexpr int Q = 4;  // up to 128 slots
+  // Q = ceil(slots / 32) blocks of 32 slots; slot t = lane + 32 q
   const int64_t c = (int64_t)it.first + cl;
   const int my_m = P.bt.cand_model[c], my_g = P.bt.cand_group[c];
   const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;
@@ -752,6 +752,13 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
   const uint64_t my_bit = my_m >= 0 ? (1ull << my_g) : 0ull;
   const int slots = it.slots;
   const int64_t cstride = (int64_t)P.num_items * 32;
+  // per-lane slot facts: the group bit of a group's LAST stage (0 elsewhere)
+  uint64_t lastbit[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int t = lane + 32 * q;
+    lastbit[q] = (t < slots && t % S == S - 1) ? (1ull << ((t / S) & 63)) : 0ull;
+  }
   bool start_ok = true;
   for (int j = 1; j < P.J; ++j) {
     const int64_t u = (int64_t)j * P.num_items + item;
@@ -831,13 +838,16 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
         upd += (unsigned long long)__popcll(hm) * S;
         // predicted finish at the last stage of every hosting group
         T y[Q], f[Q];
+        T dk = 0;
+        if constexpr (S == 1) dk = w.d[m * kSTab];
+        T fl = TT<T>::maxv();
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const int t = lane + 32 * q, g = t / S, k = t % S;
-          const T d = w.d[m * kSTab + k];
           if constexpr (S == 1) {
-            y[q] = tmax(ar, v[q]) + d;
+            y[q] = tmax(ar, v[q]) + dk;
           } else {
+            const int k = (lane + 32 * q) % S;
+            const T d = w.d[m * kSTab + k];
             T A = d, B = v[q] + d;
 #pragma unroll
             for (int o = 1; o < S; o <<= 1) {
@@ -849,13 +859,10 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
             }
             y[q] = tmax(ar + A, B);
           }
-          const bool last = (k == S - 1) && t < slots && ((hm >> (g & 63)) & 1ull);
-          f[q] = last ? y[q] + tl : TT<T>::maxv();
+          f[q] = (hm & lastbit[q]) ? y[q] + tl : TT<T>::maxv();
+          fl = tmin(fl, f[q]);
         }
-        T fmin = TT<T>::maxv();
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-          if (32 * q < slots) fmin = tmin(fmin, warp_min<T>(f[q]));
+        const T fmin = warp_min<T>(fl);
         if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) continue;  // no host / misses the SLO
         // lowest group index among the minima (slots ascend with q, then lane)
         int wq = 0, wl = 0;
@@ -920,6 +927,33 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
   }
 }
 
+template <typename T, int S>
+__device__ __forceinline__ void coop_dispatch_q(const ChunkParams& P, const WarpMem<T>& w,
+                                                const ItemDesc& it, int item, int cl, int lane,
+                                                uint32_t* end_src, unsigned long long& walked,
+                                                unsigned long long& upd) {
+  switch ((it.slots + 31) / 32) {
+    case 1: coop_candidate<T, S, 1>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    case 2: coop_candidate<T, S, 2>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    case 3: coop_candidate<T, S, 3>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    default: coop_candidate<T, S, 4>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void coop_dispatch(const ChunkParams& P, const WarpMem<T>& w,
+                                              const ItemDesc& it, int item, int cl, int lane,
+                                              uint32_t* end_src, unsigned long long& walked,
+                                              unsigned long long& upd) {
+  switch (it.S) {
+    case 1: coop_dispatch_q<T, 1>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    case 2: coop_dispatch_q<T, 2>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    case 4: coop_dispatch_q<T, 4>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    case 8: coop_dispatch_q<T, 8>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+    default: coop_dispatch_q<T, 16>(P, w, it, item, cl, lane, end_src, walked, upd); break;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, uint32_t* end_src) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -943,13 +977,7 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
       load_base<T>(P, it, w, lane);
       cur_base = it.base;
     }
-    switch (it.S) {
-      case 1: coop_candidate<T, 1>(P, w, it, item, cl, lane, end_src, walked, upd); break;
-      case 2: coop_candidate<T, 2>(P, w, it, item, cl, lane, end_src, walked, upd); break;
-      case 4: coop_candidate<T, 4>(P, w, it, item, cl, lane, end_src, walked, upd); break;
-      case 8: coop_candidate<T, 8>(P, w, it, item, cl, lane, end_src, walked, upd); break;
-      default: coop_candidate<T, 16>(P, w, it, item, cl, lane, end_src, walked, upd); break;
-    }
+    coop_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
   }
   if (lane == 0) {
     if (P.walked && walked) atomicAdd(P.walked, walked);

@@ -815,34 +815,14 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
         }
       }
       const T arl = (T)(al - E);
-      // software pipeline: the next request's shuffles and table loads are
-      // issued before the current request's dependent chain runs
-      int jj = __ffs(todo) - 1;
-      todo &= todo - 1;
-      int m = __shfl_sync(FULL, ml, jj);
-      T ar_n = __shfl_sync(FULL, arl, jj);
-      uint64_t hm_n = w.hmask[m];
-      T tl_n = w.tail[m], sl_n = w.slo[m], dk_n = 0;
-      if constexpr (S == 1) dk_n = w.d[m * kSTab];
-      for (;;) {
-        const int cjj = jj, cm = m;
-        T ar = ar_n;
-        const uint64_t hm = hm_n | (cm == my_m ? my_bit : 0ull);
-        const T tl = tl_n, sl = sl_n, dk = dk_n;
-        const bool more = todo != 0;
-        if (more) {
-          jj = __ffs(todo) - 1;
-          todo &= todo - 1;
-          m = __shfl_sync(FULL, ml, jj);
-          ar_n = __shfl_sync(FULL, arl, jj);
-          hm_n = w.hmask[m];
-          tl_n = w.tail[m];
-          sl_n = w.slo[m];
-          if constexpr (S == 1) dk_n = w.d[m * kSTab];
-        }
+      while (todo) {
+        const int jj = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int m = __shfl_sync(FULL, ml, jj);
+        T ar = __shfl_sync(FULL, arl, jj);
         if constexpr (TT<T>::kRel) {
           if (per_req) {
-            const int64_t a = __shfl_sync(FULL, al, cjj);
+            const int64_t a = __shfl_sync(FULL, al, jj);
             if (a - E > P.theta) {
               const int64_t gap = a - E;
               const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
@@ -853,9 +833,13 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
             ar = (T)(a - E);
           }
         }
+        const uint64_t hm = w.hmask[m] | (m == my_m ? my_bit : 0ull);
+        const T tl = w.tail[m], sl = w.slo[m];
         upd += (unsigned long long)__popcll(hm) * S;
         // predicted finish at the last stage of every hosting group
         T y[Q], f[Q];
+        T dk = 0;
+        if constexpr (S == 1) dk = w.d[m * kSTab];
         T fl = TT<T>::maxv();
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -863,7 +847,7 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
             y[q] = tmax(ar, v[q]) + dk;
           } else {
             const int k = (lane + 32 * q) % S;
-            const T d = w.d[cm * kSTab + k];
+            const T d = w.d[m * kSTab + k];
             T A = d, B = v[q] + d;
 #pragma unroll
             for (int o = 1; o < S; o <<= 1) {
@@ -879,10 +863,7 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
           fl = tmin(fl, f[q]);
         }
         const T fmin = warp_min<T>(fl);
-        if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) {  // no host / misses the SLO
-          if (!more) break;
-          continue;
-        }
+        if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) continue;  // no host / misses the SLO
         // lowest group index among the minima (slots ascend with q, then lane)
         int wq = 0, wl = 0;
 #pragma unroll
@@ -899,7 +880,6 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
           if (q == wq && (lane + 32 * q) / S == gw) v[q] = y[q];
         ++good;
         sum += (int64_t)(fmin - ar);
-        if (!more) break;
       }
     }
     // the chunk's exact correction, and equivalence with the speculative end

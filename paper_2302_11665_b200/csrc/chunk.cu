@@ -814,12 +814,26 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
           per_req = a_last - E > P.theta;
         }
       }
+      // lane-parallel per-request fields of the tile, broadcast by independent
+      // shuffles (no shared-memory load on the per-request dependent chain)
       const T arl = (T)(al - E);
+      const uint64_t hml = w.hmask[ml] | (ml == my_m ? my_bit : 0ull);
+      const T tll = w.tail[ml], sll = w.slo[ml];
+      T dkl = 0;
+      if constexpr (S == 1) dkl = w.d[ml * kSTab];
+      {
+        const bool rel = (todo >> lane) & 1u;
+        upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popcll(hml) : 0u) * S;
+      }
       while (todo) {
         const int jj = __ffs(todo) - 1;
         todo &= todo - 1;
         const int m = __shfl_sync(FULL, ml, jj);
         T ar = __shfl_sync(FULL, arl, jj);
+        const uint64_t hm = __shfl_sync(FULL, hml, jj);
+        const T tl = __shfl_sync(FULL, tll, jj), sl = __shfl_sync(FULL, sll, jj);
+        T dk = 0;
+        if constexpr (S == 1) dk = __shfl_sync(FULL, dkl, jj);
         if constexpr (TT<T>::kRel) {
           if (per_req) {
             const int64_t a = __shfl_sync(FULL, al, jj);
@@ -833,13 +847,8 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
             ar = (T)(a - E);
           }
         }
-        const uint64_t hm = w.hmask[m] | (m == my_m ? my_bit : 0ull);
-        const T tl = w.tail[m], sl = w.slo[m];
-        upd += (unsigned long long)__popcll(hm) * S;
         // predicted finish at the last stage of every hosting group
         T y[Q], f[Q];
-        T dk = 0;
-        if constexpr (S == 1) dk = w.d[m * kSTab];
         T fl = TT<T>::maxv();
 #pragma unroll
         for (int q = 0; q < Q; ++q) {

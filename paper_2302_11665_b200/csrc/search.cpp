@@ -77,7 +77,11 @@ struct Run {
     int32_t r1, r2;  // roots of comp(g) and comp(m) in the base
   };
   std::vector<Cand> cands;
-  std::map<std::pair<int32_t, int32_t>, int64_t> memo;  // (m, g) -> good, for the next step
+  // memo for the next step, flat over (m, g): good and validity
+  std::vector<int64_t> memo_good;
+  std::vector<uint8_t> memo_ok;
+  // per-root model / group masks of the base (component restriction)
+  std::vector<uint64_t> rootK, rootG;
   std::vector<std::pair<int32_t, int32_t>> history;     // winners in order
 
   int32_t find(int32_t x) {
@@ -117,21 +121,19 @@ static asim_status sfail(asim_search* s, asim_status code, const std::string& m)
   return asim_fail(s ? s->ctx : nullptr, code, m);
 }
 
+// Per-root model and group masks of the run's base (O(G + M) per step).
+static void root_masks(Run& run, int32_t M) {
+  run.rootK.assign(run.G + M, 0);
+  run.rootG.assign(run.G + M, 0);
+  for (int32_t x = 0; x < run.G; ++x) run.rootG[run.find(x)] |= 1ULL << x;
+  for (int32_t x = 0; x < M; ++x) run.rootK[run.find(run.G + x)] |= 1ULL << x;
+}
+
 // Restriction masks of candidate (m, g): models and groups of K_c.
-static void component_masks(Run& run, int32_t M, int32_t m, int32_t g, uint64_t* kmask,
-                            uint64_t* gmask) {
-  const int32_t r1 = run.find(g), r2 = run.find(run.G + m);
-  uint64_t km = 1ULL << m, gm = 1ULL << g;
-  for (int32_t x = 0; x < run.G; ++x) {
-    const int32_t r = run.find(x);
-    if (r == r1 || r == r2) gm |= 1ULL << x;
-  }
-  for (int32_t x = 0; x < M; ++x) {
-    const int32_t r = run.find(run.G + x);
-    if (r == r1 || r == r2) km |= 1ULL << x;
-  }
-  *kmask = km;
-  *gmask = gm;
+static void component_masks(const Run& run, int32_t m, int32_t g, int32_t r1, int32_t r2,
+                            uint64_t* kmask, uint64_t* gmask) {
+  *kmask = run.rootK[r1] | run.rootK[r2] | (1ULL << m);
+  *gmask = run.rootG[r1] | run.rootG[r2] | (1ULL << g);
 }
 
 extern "C" {
@@ -190,6 +192,8 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     r.parent.resize(r.G + hp.M);
     for (size_t i = 0; i < r.parent.size(); ++i) r.parent[i] = (int32_t)i;
     r.cgood.assign(r.G + hp.M, 0);
+    r.memo_good.assign((size_t)hp.M * r.G, 0);
+    r.memo_ok.assign((size_t)hp.M * r.G, 0);
     int64_t devices = 0;
     int32_t slots = 0;
     for (int32_t c : cfg) {
@@ -260,6 +264,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
       for (int32_t g = 0; g < run.G; ++g)
         if ((run.sel[m] >> g) & 1ULL) empty[g] = 0;
     run.cands.clear();
+    if (s->restrict_k) root_masks(run, M);
     for (int32_t m = 0; m < M; ++m) {
       std::map<std::pair<int32_t, int32_t>, int64_t> seen;  // (cfg, rank among hosts) -> rep
       for (int32_t g = 0; g < run.G; ++g) {
@@ -268,10 +273,10 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
         if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
         ++full;
         Run::Cand c{m, g, 0, 0, 0, run.find(g), run.find(run.G + m)};
-        auto it = run.memo.find(std::make_pair(m, g));
-        if (it != run.memo.end()) {  // component untouched by the last winner
+        const size_t mi = (size_t)m * run.G + g;
+        if (run.memo_ok[mi]) {  // component untouched by the last winner
           c.kind = 1;
-          c.good = it->second;
+          c.good = run.memo_good[mi];
           ++s->memo_hits;
         } else if (s->dedup && empty[g]) {
           const uint64_t below = g ? (run.sel[m] & ((1ULL << g) - 1)) : 0ULL;
@@ -292,7 +297,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
           hb.cand_ok.push_back(1);
           if (s->restrict_k) {
             uint64_t km = 0, gm = 0;
-            component_masks(run, M, m, g, &km, &gm);
+            component_masks(run, m, g, c.r1, c.r2, &km, &gm);
             hb.cand_kmask.push_back(km);
             hb.cand_gmask.push_back(gm);
           }
@@ -397,9 +402,9 @@ static asim_status update_states(asim_search* s, const std::vector<int32_t>& win
     hb.cand_model.push_back(w.m);
     hb.cand_group.push_back(w.g);
     hb.cand_ok.push_back(1);
-    if (s->restrict_k) {
+    if (s->restrict_k) {  // rootK / rootG still describe the old base
       uint64_t km = 0, gm = 0;
-      component_masks(run, M, w.m, w.g, &km, &gm);
+      component_masks(run, w.m, w.g, w.r1, w.r2, &km, &gm);
       hb.cand_kmask.push_back(km);
       hb.cand_gmask.push_back(gm);
     }
@@ -478,10 +483,13 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
     const Run::Cand w = *winner[i];
     // memo for the next step: candidates whose component avoids the winner's
     const int64_t shift = w.good - run.base_good;
-    run.memo.clear();
+    std::fill(run.memo_ok.begin(), run.memo_ok.end(), 0);
     for (const Run::Cand& c : run.cands)
-      if (c.r1 != w.r1 && c.r1 != w.r2 && c.r2 != w.r1 && c.r2 != w.r2)
-        run.memo.emplace(std::make_pair(c.m, c.g), c.good + shift);
+      if (c.r1 != w.r1 && c.r1 != w.r2 && c.r2 != w.r1 && c.r2 != w.r2) {
+        const size_t mi = (size_t)c.m * run.G + c.g;
+        run.memo_ok[mi] = 1;
+        run.memo_good[mi] = c.good + shift;
+      }
     // the merged component's good, from the winner's total alone
     const int64_t merged =
         w.good - run.base_good + run.cgood[w.r1] + (w.r2 != w.r1 ? run.cgood[w.r2] : 0);

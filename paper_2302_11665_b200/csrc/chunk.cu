@@ -1064,8 +1064,10 @@ __global__ void publish_kernel(ChunkParams P, const uint32_t* __restrict__ end_s
 template <typename K>
 cudaError_t grid_for(K kernel, size_t smem, int64_t units, int sms, int64_t* blocks) {
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  // always the maximum: concurrent contexts (threads) may launch the same
+  // kernel with different sizes, and a smaller attribute would fail theirs
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+                                       227 * 1024);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem);

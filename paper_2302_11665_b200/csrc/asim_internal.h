@@ -113,7 +113,22 @@ struct ChunkParams {
   const int32_t* spec_row;     // [B] row of base b in spec_state
   int32_t state_stride;        // slots per boundary row of spec_state / published states
   unsigned long long* walked;  // nullable statistics: chunks re-simulated by the walk pass
+  // Per-candidate speculation rows (nullable): spec_cand[(c * J + j) * state_stride + k],
+  // c = batch index; when set they replace spec_state for the candidate's own
+  // trajectory (spec_state still supplies out-of-component slots when publishing).
+  const int64_t* spec_cand;
 };
+
+// Per-candidate speculation rows for the search (see search.cpp):
+// out[c][j][k] = (cprev[kp][j][k] != bprev[r][j][k]) ? cprev[kp][j][k] : bcur[r][j][k]
+// with (r, kp) = rows[c] (kp < 0: bcur).  Canonical (boundary-clamped) states.
+struct MixRow {
+  int32_t run, prev;
+};
+cudaError_t launch_mix_states(int64_t C0, int64_t C1, int32_t J, int32_t stride,
+                              const int64_t* bcur, const int64_t* bprev, const int64_t* cprev,
+                              const MixRow* rows, int64_t* out, cudaStream_t st,
+                              int64_t* launches);
 
 // Publish the true state at every chunk boundary of chosen lanes (item, lane)
 // into out[(row * J + j) * state_stride + k] (absolute int64; j = 0 idle).

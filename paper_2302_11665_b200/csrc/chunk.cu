@@ -430,7 +430,10 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
   if constexpr (MODE != WALK) {  // the speculative trajectory
     T* spec_st = (MODE == DUAL) ? w.st1 : w.st0;
     if (P.spec_state != nullptr && j > 0) {
-      const int64_t* ss = P.spec_state + ((int64_t)P.spec_row[it.base] * P.J + j) * P.state_stride;
+      const int64_t* ss =
+          (P.spec_cand && in_item)
+              ? P.spec_cand + ((int64_t)c * P.J + j) * P.state_stride
+              : P.spec_state + ((int64_t)P.spec_row[it.base] * P.J + j) * P.state_stride;
       for (int k = 0; k < slots; ++k) {
         const int64_t v = ss[k];
         if constexpr (TT<T>::kRel) {
@@ -1058,7 +1061,30 @@ __global__ void publish_kernel(ChunkParams P, const uint32_t* __restrict__ end_s
       v = P.spec_state[((int64_t)P.spec_row[it.base] * P.J + j) * P.state_stride + k];
     }
   }
+  if (j > 0) {  // canonical form: a free time below the boundary's arrival is that arrival
+    const int64_t a0 = P.tr.arrival[P.chunk_begin[j]];
+    v = v > a0 ? v : a0;
+  }
   out[((int64_t)pi.row * P.J + j) * P.state_stride + k] = v;
+}
+
+__global__ void mix_states_kernel(int64_t C0, int64_t C1, int32_t J, int32_t stride,
+                                  const int64_t* __restrict__ bcur,
+                                  const int64_t* __restrict__ bprev,
+                                  const int64_t* __restrict__ cprev,
+                                  const MixRow* __restrict__ rows, int64_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)J * stride;
+  if (t >= (C1 - C0) * per) return;
+  const int64_t c = C0 + t / per, jk = t % per;
+  const MixRow r = rows[c];
+  const int64_t b = bcur[(int64_t)r.run * per + jk];
+  int64_t v = b;
+  if (r.prev >= 0) {
+    const int64_t cp = cprev[(int64_t)r.prev * per + jk];
+    if (cp != bprev[(int64_t)r.run * per + jk]) v = cp;  // the candidate's own difference
+  }
+  out[c * per + jk] = v;
 }
 
 template <typename K>
@@ -1145,6 +1171,18 @@ cudaError_t launch_publish_states(const ChunkParams& P, const uint32_t* end_src,
     publish_kernel<uint32_t><<<blocks, 256, 0, st>>>(P, end_src, pub, npub, out);
   else
     publish_kernel<int64_t><<<blocks, 256, 0, st>>>(P, end_src, pub, npub, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mix_states(int64_t C0, int64_t C1, int32_t J, int32_t stride,
+                              const int64_t* bcur, const int64_t* bprev, const int64_t* cprev,
+                              const MixRow* rows, int64_t* out, cudaStream_t st,
+                              int64_t* launches) {
+  const int64_t n = (C1 - C0) * J * stride;
+  if (n <= 0) return cudaSuccess;
+  mix_states_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(C0, C1, J, stride, bcur, bprev,
+                                                                 cprev, rows, out);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -138,6 +138,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.walked = ctx->profiling ? ctx->d_walked.as<unsigned long long>() : nullptr;
   P.spec_state = opt ? opt->spec_state : nullptr;
   P.spec_row = opt ? opt->spec_row : nullptr;
+  P.spec_cand = opt ? opt->spec_cand : nullptr;
   P.state_stride = (opt && opt->state_stride > 0) ? opt->state_stride : slots_max;
   if (P.spec_state && P.state_stride < slots_max)
     return asim_fail(ctx, ASIM_ERANGE, "internal: state stride below slots");

@@ -144,6 +144,7 @@ struct ChunkOptions {
   int64_t J = 0;                         // fixed chunk count (0 = automatic)
   const int64_t* spec_state = nullptr;   // speculation source (device), see ChunkParams
   const int32_t* spec_row = nullptr;     // [B] device
+  const int64_t* spec_cand = nullptr;    // per-candidate rows (device), see ChunkParams
   int32_t state_stride = 0;
 };
 bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out);

@@ -42,7 +42,11 @@
 // the new base is the winner: its boundary states are published straight
 // from the winner's lane when this rank simulated it (own component from the
 // lane, every other slot from the old base), else a one-lane pass simulates
-// the winner's component again.  Speculation never affects results.
+// the winner's component again.  A candidate simulated in the previous step
+// too starts from a mix: the new base's state, except in the slots where its
+// own previous trajectory differed from the previous base -- the effect of
+// its own replica, which the base cannot know.  Speculation never affects
+// results; it only decides how soon the fix-up meets the true trajectory.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -83,6 +87,9 @@ struct Run {
   // per-root model / group masks of the base (component restriction)
   std::vector<uint64_t> rootK, rootG;
   std::vector<std::pair<int32_t, int32_t>> history;     // winners in order
+  // batch index of (m, g) among the candidates simulated locally in the
+  // previous / current step (-1: not simulated here)
+  std::vector<int32_t> prev_idx, cur_idx;
 
   int32_t find(int32_t x) {
     while (parent[x] != x) x = parent[x] = parent[parent[x]];
@@ -112,10 +119,17 @@ struct asim_search {
   int32_t stride = 1;
   DBuf st_base, st_next, d_rows, d_rows2, d_scratch;
   bool rows_uploaded = false;
+  // candidate memory for mixed speculation (see header)
+  DBuf cs_prev, cs_cur, spec_mix, d_mixrows;
+  std::vector<asim::MixRow> mixrows;  // per batch candidate: (run, previous index)
+  bool have_prev = false;
   // statistics
   int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0, base_passes = 0;
   bool finished = false;
 };
+
+// candidate memory is skipped when a step's rows would exceed this
+static constexpr size_t kMixBytesCap = size_t(6) << 30;
 
 static asim_status sfail(asim_search* s, asim_status code, const std::string& m) {
   return asim_fail(s ? s->ctx : nullptr, code, m);
@@ -194,6 +208,8 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     r.cgood.assign(r.G + hp.M, 0);
     r.memo_good.assign((size_t)hp.M * r.G, 0);
     r.memo_ok.assign((size_t)hp.M * r.G, 0);
+    r.prev_idx.assign((size_t)hp.M * r.G, -1);
+    r.cur_idx.assign((size_t)hp.M * r.G, -1);
     int64_t devices = 0;
     int32_t slots = 0;
     for (int32_t c : cfg) {
@@ -234,7 +250,7 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
 void asim_search_destroy(asim_search* s) {
   if (!s) return;
   DBuf* bufs[] = {&s->d_good_all, &s->st_base, &s->st_next, &s->d_rows, &s->d_rows2,
-                  &s->d_scratch};
+                  &s->d_scratch, &s->cs_prev, &s->cs_cur, &s->spec_mix, &s->d_mixrows};
   for (DBuf* b : bufs) b->release();
   delete s;
 }
@@ -254,6 +270,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   s->base_run.clear();
   s->eval_lo = s->eval_hi = 0;
   s->rows_uploaded = false;
+  s->mixrows.clear();
   int64_t full = 0;
   for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r) {
     Run& run = s->runs[r];
@@ -301,6 +318,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
             hb.cand_kmask.push_back(km);
             hb.cand_gmask.push_back(gm);
           }
+          s->mixrows.push_back(asim::MixRow{r, run.prev_idx[(size_t)m * run.G + g]});
         }
         run.cands.push_back(c);
       }
@@ -358,6 +376,22 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
     opt.spec_state = s->st_base.as<int64_t>();
     opt.spec_row = s->d_rows.as<int32_t>();
     popt = &opt;
+    // mixed speculation rows for [begin, end) (candidate memory of the last step)
+    const size_t per = (size_t)s->J * s->stride * 8;
+    if (s->have_prev && (size_t)C * per <= kMixBytesCap) {
+      cudaError_t e = s->spec_mix.ensure((size_t)C * per + 8);
+      if (e == cudaSuccess) e = upload(s->d_mixrows, s->mixrows, strm);
+      if (e == cudaSuccess)
+        e = asim::launch_mix_states(begin, end, (int32_t)s->J, s->stride, s->st_base.as<int64_t>(),
+                                    s->st_next.as<int64_t>(), s->cs_prev.as<int64_t>(),
+                                    s->d_mixrows.as<asim::MixRow>(), s->spec_mix.as<int64_t>(),
+                                    strm, &s->ctx->launches);
+      if (e != cudaSuccess) {
+        if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
+        return asim_cuda(s->ctx, e, "mix speculation");
+      }
+      opt.spec_cand = s->spec_mix.as<int64_t>();
+    }
   }
   asim::DevOut out{};
   out.good = good_dev;
@@ -474,7 +508,34 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
     winner_run.push_back(s->base_run[b]);
     winner.push_back(&run.cands[bi]);
   }
-  if (s->use_states) {  // before the bases change: the update simulates from the old ones
+  if (s->use_states) {
+    // candidate memory: every locally simulated candidate's boundary states
+    const size_t per = (size_t)s->J * s->stride * 8;
+    const bool keep = s->eval_hi > s->eval_lo && (size_t)C * per <= kMixBytesCap;
+    if (keep) {
+      cudaError_t e = s->cs_cur.ensure((size_t)C * per + 8);
+      if (e != cudaSuccess) return asim_cuda(s->ctx, e, "candidate memory");
+      std::vector<int64_t> cs;
+      std::vector<int32_t> rows;
+      for (int64_t c = s->eval_lo; c < s->eval_hi; ++c) {
+        cs.push_back(c);
+        rows.push_back((int32_t)c);
+      }
+      asim_status rc = asim_publish_candidates(s->ctx, cs, rows, s->cs_cur.as<int64_t>(), st);
+      if (rc) return rc;
+    }
+    for (size_t b = 0; b < s->base_run.size(); ++b) {
+      Run& run = s->runs[s->base_run[b]];
+      std::fill(run.cur_idx.begin(), run.cur_idx.end(), -1);
+      if (keep)
+        for (const Run::Cand& c : run.cands)
+          if (c.kind == 0 && c.ref >= s->eval_lo && c.ref < s->eval_hi)
+            run.cur_idx[(size_t)c.m * run.G + c.g] = (int32_t)c.ref;
+      std::swap(run.prev_idx, run.cur_idx);
+    }
+    if (keep) std::swap(s->cs_prev, s->cs_cur);
+    s->have_prev = keep;
+    // before the bases change: the update simulates from the old ones
     asim_status rc = update_states(s, winner_run, winner, st);
     if (rc) return rc;
   }

@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dedup", action="store_true",
                     help="exact de-duplication of identical candidates (fewer simulations)")
+    ap.add_argument("--search", default="greedy", choices=["greedy", "fast"],
+                    help="Alg. 1 inside Alg. 2 (the headline) or the fast heuristic of P:737")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -237,8 +239,11 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def one_search(s):
-        with s.search_handle(dedup=args.dedup) as sh:
-            adist.run_search(sh, pg=pg, stream=stream)
+        with s.search_handle(dedup=args.dedup, fast=args.search == "fast") as sh:
+            if args.search == "fast":
+                sh.run(stream=stream)  # every rank computes the whole heuristic
+            else:
+                adist.run_search(sh, pg=pg, stream=stream)
             return sh.result()
 
     def barrier():
@@ -331,7 +336,7 @@ def main():
                         devices=prob.num_devices, runs=len(res.runs), search_steps=res.steps,
                         candidates_per_search=res.candidates,
                         simulated_per_search=res.evaluated, memo_hits=res.memo_hits,
-                        dedup=bool(args.dedup),
+                        dedup=bool(args.dedup), search=args.search,
                         best_run=res.best_run, best_attainment=res.best_good / max(N, 1),
                         l2="flushed between timed steps (256 MB write)",
                         parallelism=f"candidate-sharded x{world}"),

@@ -127,6 +127,8 @@ asim_status asim_set_chunk_size(asim_ctx* ctx, int64_t min_requests);
  *   mem_bytes[M][P]   bytes per device of one replica; < 0 = (m,p) not placeable
  *   num_devices       cluster size D >= 1;  device_budget_bytes >= 0
  * Bound (reading C20): sum_k stage_ns + tail_ns <= 2^60 for every (m, p).
+ * A trace set earlier stays valid when M is unchanged, else it must be set
+ * again (ASIM_ESTATE until then).
  * Errors: ASIM_EINVAL (null/size), ASIM_ERANGE (values out of range). */
 typedef struct {
   int32_t num_models, num_configs, max_stages;
@@ -190,13 +192,19 @@ typedef struct {
  *   sum_latency_ns[C]     optional (NULL); sum of (finish - arrival) over good
  *   good_per_model[C][M]  optional; good split by model
  *   argmax[1]             optional; index of the max good (ties -> lowest
- *                         index), -1 if no candidate is feasible */
+ *                         index), -1 if no candidate is feasible
+ *   busy_ns[C][max_groups] optional; per group, the sum over its accepted
+ *                         requests of their stage occupancies (sum_k stage_ns)
+ *                         -- the group's busy time times its stage count
+ *   ptr_kind              where every output array lives
+ * Requesting good_per_model or busy_ns selects the general kernel. */
 typedef struct {
   int64_t* good;
   int64_t* sum_latency_ns;
   int64_t* good_per_model;
   int64_t* argmax;
   int32_t ptr_kind;
+  int64_t* busy_ns;
 } asim_results;
 
 asim_status asim_evaluate(asim_ctx* ctx, const asim_candidates* cands, asim_results* out,
@@ -238,13 +246,25 @@ double asim_attainment(int64_t good, int64_t n);
  *   asim_search_apply    -> per-run argmax over good_all_dev[C] (NULL if C == 0)
  *                           and the memo values; apply
  * asim_search_run does the whole loop on this context's GPU.
- * The search borrows ctx (problem and trace must stay set while it lives). */
+ * The search borrows ctx (problem and trace must stay set while it lives).
+ *
+ * Fast heuristic (spec->fast = 1; "run the simulator only once and
+ * place a model with the most unserved requests in an available group with
+ * the lowest utilization"; readings C22-C24 in DESIGN.md): each iteration
+ * simulates the current selection once; unserved(m) = requests of m not
+ * finished within their SLO; among models with unserved > 0 and at least one
+ * feasible addition, the largest unserved wins (ties -> lowest m); among its
+ * feasible groups the lowest utilization busy_ns / stages wins (ties ->
+ * lowest g); the run stops when no such model exists; the best selection
+ * (strict '>') is kept.  Fast mode is driven by asim_search_run only. */
 typedef struct {
   int32_t num_runs;              /* 0 = Alg. 2 single-bucket enumeration */
   const int32_t* run_num_groups; /* [num_runs] */
   const int32_t* run_group_cfg;  /* [sum run_num_groups] */
   int32_t dedup;                 /* 1 = evaluate one representative of provably
                                     identical candidates (exact) */
+  int32_t fast;                  /* 1 = the fast heuristic of P:737 instead of
+                                    Alg. 1 inside every run (see below) */
 } asim_search_spec;
 
 typedef struct {

@@ -22,6 +22,17 @@ groups for every divisor size of the device count, ascending ("all groups
 have the same size and the same parallel configurations"); for each,
 every config of that size in problem order; the best run (strict '>') wins.
 
+Fast heuristic: "Instead of using the simulator to evaluate all
+(model, group) pairs at each iteration, we can run the simulator only once
+and place a model with the most unserved requests in an available group with
+the lowest utilization."  Readings (C22-C24): unserved(m) = requests
+of m not good in the simulation of the current selection; a model qualifies
+when unserved > 0 and it has an available group (not hosting it, memory
+feasible); utilization(g) = sum over the requests g served of their stage
+occupancies / (s_g * horizon) -- the mean stage utilization, horizon common
+to all groups; ties -> lowest m, lowest g; the loop ends when no model
+qualifies; best selection on strict '>' as in Alg. 1.
+
 Brute force: every placement of a tiny cluster -- every multiset of group
 sizes summing to D (non-increasing), every config per group, every
 memory-feasible model subset per group.
@@ -30,6 +41,7 @@ memory-feasible model subset per group.
 from __future__ import annotations
 
 import itertools
+from fractions import Fraction
 
 import numpy as np
 
@@ -75,6 +87,76 @@ def greedy(prob, trace, group_cfg, threads: int = 0, record: bool = False):
         if goods[i] > best_good:
             best_sel, best_good = sel.copy(), int(goods[i])
     return dict(placement=Placement(cfg, best_sel), good=best_good, steps=steps)
+
+
+def utilization_busy(prob, model, group_cfg, served_by):
+    """Per group g: sum over the requests it served of sum_k stage_ns[m][cfg_g][k]
+    (the numerator of its mean stage utilization, reading C23)."""
+    cfg = np.asarray(group_cfg, dtype=np.int64)
+    served_by = np.asarray(served_by)
+    model = np.asarray(model)
+    busy = [0] * len(cfg)
+    for g in range(len(cfg)):
+        p = int(cfg[g])
+        s = int(prob.cfg_stages[p])
+        occ = np.asarray(prob.stage_ns)[:, p, :s].sum(axis=1)  # per model, one request
+        counts = np.bincount(model[served_by == g], minlength=prob.num_models)
+        busy[g] = sum(int(c) * int(o) for c, o in zip(counts, occ))
+    return busy
+
+
+def greedy_fast(prob, trace, group_cfg, record: bool = False):
+    """The fast heuristic of P:737 on fixed groups `group_cfg`.
+    Returns dict(placement, good, steps=[(good, (m, g) or None)])."""
+    op = prob if isinstance(prob, OracleProblem) else OracleProblem(prob)
+    ot = trace if isinstance(trace, OracleTrace) else OracleTrace(trace)
+    pr = op.prob
+    M = pr.num_models
+    cfg = np.asarray(group_cfg, dtype=np.int32)
+    G = len(cfg)
+    n_m = np.bincount(ot.model, minlength=M)
+    sel = np.zeros(M, dtype=np.uint64)
+    best_sel, best_good = sel.copy(), 0
+    steps = []
+    while feasible(op, Placement(cfg, sel)):
+        # "run the simulator only once"
+        r = simulate(op, ot, Placement(cfg, sel), detail=True)
+        if r["good"] > best_good:
+            best_sel, best_good = sel.copy(), r["good"]
+        unserved = [int(n_m[m]) - int(r["good_per_model"][m]) for m in range(M)]
+        busy = utilization_busy(pr, ot.model, cfg, r["served_by"])
+        pick = None
+        for m in sorted(range(M), key=lambda m: (-unserved[m], m)):  # most unserved first
+            if unserved[m] <= 0:
+                break
+            # "an available group with the lowest utilization": busy_g / s_g, lowest g on ties
+            avail = [g for g in range(G)
+                     if not (int(sel[m]) >> g) & 1 and feasible(op, Placement(cfg, _add(sel, m, g)))]
+            if avail:
+                g = min(avail, key=lambda g: (Fraction(busy[g], int(pr.cfg_stages[cfg[g]])), g))
+                pick = (m, g)
+                break
+        if record:
+            steps.append((r["good"], pick))
+        if pick is None:
+            break
+        sel = _add(sel, *pick)
+    return dict(placement=Placement(cfg, best_sel), good=best_good, steps=steps)
+
+
+def alg2_fast(prob, trace, record: bool = False):
+    """Alg. 2 (single bucket) around the fast heuristic; strict '>' across runs."""
+    op, ot = OracleProblem(prob), OracleTrace(trace)
+    best = dict(placement=Placement(np.zeros(0, np.int32), np.zeros(prob.num_models, np.uint64)),
+                good=0, run=-1)
+    runs = []
+    for r, (size, p, cfg) in enumerate(alg2_runs(prob)):
+        res = greedy_fast(op, ot, cfg, record)
+        runs.append(res)
+        if res["good"] > best["good"]:
+            best = dict(res, run=r)
+    best["runs"] = runs
+    return best
 
 
 def alg2_runs(prob):

@@ -43,7 +43,7 @@ class asim_deltas(ctypes.Structure):
 
 class asim_results(ctypes.Structure):
     _fields_ = [("good", vp), ("sum_latency_ns", vp), ("good_per_model", vp), ("argmax", vp),
-                ("ptr_kind", i32)]
+                ("ptr_kind", i32), ("busy_ns", vp)]
 
 
 class asim_stats(ctypes.Structure):
@@ -53,7 +53,7 @@ class asim_stats(ctypes.Structure):
 
 class asim_search_spec(ctypes.Structure):
     _fields_ = [("num_runs", i32), ("run_num_groups", vp), ("run_group_cfg", vp),
-                ("dedup", i32)]
+                ("dedup", i32), ("fast", i32)]
 
 
 class asim_search_result(ctypes.Structure):

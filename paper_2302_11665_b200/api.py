@@ -146,61 +146,71 @@ class Simulator:
 
     # ------------------------------------------------------------- evaluate
     def evaluate(self, group_cfg, host_mask, per_model=False, sum_latency=True, argmax=True,
-                 stream=None) -> dict:
+                 busy=False, stream=None) -> dict:
         """Full candidates: group_cfg [C, G] int32, host_mask [C, M] uint64 (host)."""
         cfg = _host(group_cfg, np.int32)
         mask = _host(host_mask, np.uint64)
         C, G = cfg.shape
         cands = A.asim_candidates(C, G, _ptr(cfg), _ptr(mask), A.ASIM_HOST)
-        return self._run(A.asim_evaluate, cands, C, per_model, sum_latency, argmax, stream)
+        return self._run(A.asim_evaluate, cands, C, G, per_model, sum_latency, argmax, busy,
+                         stream)
 
     def evaluate_deltas(self, base_cfg, base_mask, cand_base, cand_model, cand_group,
-                        per_model=False, sum_latency=True, argmax=True, stream=None) -> dict:
+                        per_model=False, sum_latency=True, argmax=True, busy=False,
+                        stream=None) -> dict:
         bc = _host(base_cfg, np.int32)
         bm = _host(base_mask, np.uint64)
         cb, cm, cg = (_host(x, np.int32) for x in (cand_base, cand_model, cand_group))
         B, G = bc.shape
         C = int(cb.shape[0])
         d = A.asim_deltas(B, G, _ptr(bc), _ptr(bm), C, _ptr(cb), _ptr(cm), _ptr(cg), A.ASIM_HOST)
-        return self._run(A.asim_evaluate_deltas, d, C, per_model, sum_latency, argmax, stream)
+        return self._run(A.asim_evaluate_deltas, d, C, G, per_model, sum_latency, argmax, busy,
+                         stream)
 
-    def _run(self, fn, cands, C, per_model, sum_latency, argmax, stream):
+    def _run(self, fn, cands, C, G, per_model, sum_latency, argmax, busy, stream):
         good = np.zeros(C, np.int64)
         sl = np.zeros(C, np.int64) if sum_latency else None
         pm = np.zeros((C, self.M), np.int64) if per_model else None
         am = np.zeros(1, np.int64) if argmax else None
-        res = A.asim_results(_ptr(good), _ptr(sl), _ptr(pm), _ptr(am), A.ASIM_HOST)
+        bz = np.zeros((C, G), np.int64) if busy else None
+        res = A.asim_results(_ptr(good), _ptr(sl), _ptr(pm), _ptr(am), A.ASIM_HOST, _ptr(bz))
         self._check(fn(self.h, ctypes.byref(cands), ctypes.byref(res), _stream_ptr(stream)))
         return dict(good=good, sum_latency_ns=sl, good_per_model=pm,
-                    argmax=int(am[0]) if argmax else None)
+                    argmax=int(am[0]) if argmax else None, busy_ns=bz)
 
     # ------------------------------------------------------------- search
-    def search_handle(self, runs=None, dedup=True) -> "SearchHandle":
-        return SearchHandle(self, runs, dedup)
+    def search_handle(self, runs=None, dedup=True, fast=False) -> "SearchHandle":
+        return SearchHandle(self, runs, dedup, fast)
 
-    def search(self, runs=None, dedup=True, pg=None, stream=None) -> SearchResult:
+    def search(self, runs=None, dedup=True, pg=None, stream=None, fast=False) -> SearchResult:
         """Full Alg. 2 (single bucket) / Alg. 1 search.  With a
         torch.distributed process group the step candidates shard across its
-        ranks (dist.run_search)."""
+        ranks (dist.run_search).  fast=True runs the fast heuristic of P:737
+        instead of Alg. 1 (one simulation per run and step; every rank
+        computes it whole -- there is nothing to shard)."""
         from . import dist
 
-        with self.search_handle(runs, dedup) as sh:
-            dist.run_search(sh, pg=pg, stream=stream)
+        with self.search_handle(runs, dedup, fast) as sh:
+            if fast:
+                sh.run(stream=stream)
+            else:
+                dist.run_search(sh, pg=pg, stream=stream)
             return sh.result()
 
 
 class SearchHandle:
     """Stepwise search protocol of include/asim.h (prepare / evaluate / apply)."""
 
-    def __init__(self, sim: Simulator, runs=None, dedup=True):
+    def __init__(self, sim: Simulator, runs=None, dedup=True, fast=False):
         self.sim = sim
         if runs is None:
-            spec = A.asim_search_spec(0, None, None, int(bool(dedup)))
+            spec = A.asim_search_spec(0, None, None, int(bool(dedup)), int(bool(fast)))
             self._keep = ()
         else:
             ng = np.array([len(r) for r in runs], np.int32)
             cfg = np.concatenate([np.asarray(r, np.int32) for r in runs]).astype(np.int32)
-            spec = A.asim_search_spec(len(runs), _ptr(ng), _ptr(cfg), int(bool(dedup)))
+            spec = A.asim_search_spec(len(runs), _ptr(ng), _ptr(cfg), int(bool(dedup)),
+                                      int(bool(fast)))
             self._keep = (ng, cfg)
         h = ctypes.c_void_p()
         sim._check(A.asim_search_create(sim.h, ctypes.byref(spec), ctypes.byref(h)))

@@ -55,6 +55,7 @@ struct DevOut {
   int64_t* good_per_model;  // nullable [C][M]
   int64_t out_offset;
   unsigned long long* stage_updates;  // nullable device counter (statistics)
+  int64_t* busy;            // nullable [C][G]: sum of stage occupancies of accepted requests
 };
 
 // Launchers (sim.cu).  All asynchronous on `stream`; return cudaError_t.

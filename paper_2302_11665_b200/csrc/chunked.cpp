@@ -18,7 +18,7 @@ int stage_class(int s) { return (s == 1 || s == 2 || s == 4 || s == 8 || s == 16
 }  // namespace
 
 bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out) {
-  if (out.good_per_model) return false;  // per-model counts: general kernel (sim.cu)
+  if (out.good_per_model || out.busy) return false;  // per-model / per-group outputs: sim.cu
   if (hb.slots > ASIM_MAX_SLOTS) return false;
   const size_t M = (size_t)ctx->hp.M;
   const size_t per_warp = (size_t)hb.slots * 32 * 8 * 2 + M * (8 + 8 * (kSTab + 2)) + 256;

@@ -96,8 +96,8 @@ asim_status check_base(asim_ctx* ctx, const int32_t* cfg, const uint64_t* mask, 
   return ASIM_OK;
 }
 
-asim_status finish_outputs(asim_ctx* ctx, asim_results* out, int64_t C, bool want_sum, bool want_pm,
-                           bool want_arg, cudaStream_t st) {
+asim_status finish_outputs(asim_ctx* ctx, asim_results* out, int64_t C, int32_t G, bool want_sum,
+                           bool want_pm, bool want_busy, bool want_arg, cudaStream_t st) {
   const int64_t M = ctx->hp.M;
   cudaError_t e = cudaSuccess;
   if (out->ptr_kind == ASIM_HOST) {
@@ -106,6 +106,8 @@ asim_status finish_outputs(asim_ctx* ctx, asim_results* out, int64_t C, bool wan
       e = cudaMemcpyAsync(out->sum_latency_ns, ctx->d_sum.p, C * 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess && want_pm && C > 0)
       e = cudaMemcpyAsync(out->good_per_model, ctx->d_pm.p, C * M * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && want_busy && C * G > 0)
+      e = cudaMemcpyAsync(out->busy_ns, ctx->d_busy.p, C * G * 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess && want_arg)
       e = cudaMemcpyAsync(out->argmax, ctx->d_argmax.p, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -278,7 +280,7 @@ void asim_destroy(asim_ctx* ctx) {
     DBuf* bufs[] = {&ctx->d_stage, &ctx->d_tail, &ctx->d_slo, &ctx->d_cfg_stages,
                     &ctx->d_arrival, &ctx->d_model, &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group,
-                    &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm,
+                    &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm, &ctx->d_busy,
                     &ctx->d_argmax, &ctx->d_counter, &ctx->d_walked, &ctx->c_items, &ctx->c_begin,
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
@@ -434,9 +436,10 @@ asim_status asim_set_problem(asim_ctx* ctx, const asim_problem* p) {
   if (e == cudaSuccess) e = upload(ctx->d_cfg_stages, hp.cfg_stages, 0);
   if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload problem");
+  // a trace set for another model count must be set again
+  if (ctx->has_trace && hp.M != ctx->hp.M) ctx->has_trace = false;
   ctx->hp = std::move(hp);
   ctx->has_problem = true;
-  // a trace whose model ids no longer fit must be re-set
   return ASIM_OK;
 }
 
@@ -475,6 +478,8 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload trace");
   ctx->n = n;
   ctx->max_arrival = n ? a[n - 1] : 0;
+  ctx->model_n.assign(ctx->hp.M, 0);
+  for (int64_t i = 0; i < n; ++i) ++ctx->model_n[m[i]];
   ctx->has_trace = true;
   return ASIM_OK;
 }
@@ -489,7 +494,9 @@ static asim_status evaluate_batch(asim_ctx* ctx, HostBatch& hb, asim_results* ou
   const bool want_sum = out->sum_latency_ns != nullptr;
   const bool want_pm = out->good_per_model != nullptr;
   const bool want_arg = out->argmax != nullptr;
-  asim::DevOut dout;
+  const bool want_busy = out->busy_ns != nullptr;
+  const int32_t G = hb.G;
+  asim::DevOut dout{};
   dout.out_offset = 0;
   dout.stage_updates = nullptr;
   cudaError_t e = cudaSuccess;
@@ -497,18 +504,25 @@ static asim_status evaluate_batch(asim_ctx* ctx, HostBatch& hb, asim_results* ou
     dout.good = out->good;
     dout.sum_latency = out->sum_latency_ns;
     dout.good_per_model = out->good_per_model;
+    dout.busy = out->busy_ns;
   } else {
     e = ctx->d_good.ensure(C * 8 + 8);
     if (e == cudaSuccess && want_sum) e = ctx->d_sum.ensure(C * 8 + 8);
     if (e == cudaSuccess && want_pm) e = ctx->d_pm.ensure(C * M * 8 + 8);
+    if (e == cudaSuccess && want_busy) e = ctx->d_busy.ensure(C * G * 8 + 8);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "allocate results");
     dout.good = ctx->d_good.as<int64_t>();
     dout.sum_latency = want_sum ? ctx->d_sum.as<int64_t>() : nullptr;
     dout.good_per_model = want_pm ? ctx->d_pm.as<int64_t>() : nullptr;
+    dout.busy = want_busy ? ctx->d_busy.as<int64_t>() : nullptr;
   }
   if (want_pm && C > 0) {
     e = cudaMemsetAsync(dout.good_per_model, 0, C * M * 8, st);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "memset per-model");
+  }
+  if (want_busy && C * G > 0) {
+    e = cudaMemsetAsync(dout.busy, 0, C * G * 8, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "memset busy");
   }
   asim_status s = asim_run_batch(ctx, hb, 0, C, dout, st);
   if (s) return s;
@@ -518,7 +532,7 @@ static asim_status evaluate_batch(asim_ctx* ctx, HostBatch& hb, asim_results* ou
     if (e == cudaSuccess) e = asim::launch_argmax(dout.good, C, arg_dev, st, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "argmax kernel");
   }
-  return finish_outputs(ctx, out, C, want_sum, want_pm, want_arg, st);
+  return finish_outputs(ctx, out, C, G, want_sum, want_pm, want_busy, want_arg, st);
 }
 
 asim_status asim_evaluate(asim_ctx* ctx, const asim_candidates* cands, asim_results* out,

@@ -57,6 +57,7 @@ struct asim_ctx {
   bool has_trace = false;
   int64_t n = 0;
   int64_t max_arrival = 0;
+  std::vector<int64_t> model_n;  // [M] requests per model in the trace
   DBuf d_arrival, d_model;
 
   // statistics (asim_set_profiling)
@@ -84,7 +85,7 @@ struct asim_ctx {
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;
   DBuf d_cand_kmask, d_cand_gmask;
-  DBuf d_good, d_sum, d_pm, d_argmax;
+  DBuf d_good, d_sum, d_pm, d_argmax, d_busy;
 
   asim::DevProblem dev_problem() const {
     asim::DevProblem p;

@@ -123,6 +123,9 @@ struct asim_search {
   DBuf cs_prev, cs_cur, spec_mix, d_mixrows;
   std::vector<asim::MixRow> mixrows;  // per batch candidate: (run, previous index)
   bool have_prev = false;
+  // fast heuristic: per-model good and per-group busy of each base
+  bool fast = false;
+  DBuf d_pm, d_busy;
   // statistics
   int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0, base_passes = 0;
   bool finished = false;
@@ -195,6 +198,7 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
   if (!s) return asim_fail(ctx, ASIM_ENOMEM, "host allocation failed");
   s->ctx = ctx;
   s->dedup = spec->dedup != 0;
+  s->fast = spec->fast != 0;
   int32_t stride = 1;
   for (auto& cfg : groups) {
     Run r;
@@ -228,7 +232,8 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     probe_hb.slots = stride;
     asim::DevOut probe{};
     const bool eligible = asim_chunked_eligible(ctx, probe_hb, probe);
-    s->use_states = ctx->force_path != 1 && eligible;  // the general kernel has no time chunks
+    // the general kernel has no time chunks; the fast heuristic only uses it
+    s->use_states = ctx->force_path != 1 && eligible && !s->fast;
     s->restrict_k = s->use_states && hp.M <= 64;
   }
   if (s->use_states && !s->runs.empty()) {
@@ -250,7 +255,8 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
 void asim_search_destroy(asim_search* s) {
   if (!s) return;
   DBuf* bufs[] = {&s->d_good_all, &s->st_base, &s->st_next, &s->d_rows, &s->d_rows2,
-                  &s->d_scratch, &s->cs_prev, &s->cs_cur, &s->spec_mix, &s->d_mixrows};
+                  &s->d_scratch, &s->cs_prev, &s->cs_cur, &s->spec_mix, &s->d_mixrows,
+                  &s->d_pm, &s->d_busy};
   for (DBuf* b : bufs) b->release();
   delete s;
 }
@@ -262,6 +268,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   asim_status st = asim_ready(s->ctx);
   if (st) return st;
   if (s->prepared) return sfail(s, ASIM_ESTATE, "prepare called twice without apply");
+  if (s->fast) return sfail(s, ASIM_ESTATE, "the fast heuristic is driven by asim_search_run");
   const HostProblem& hp = s->ctx->hp;
   const int32_t M = hp.M, G = s->G;
   HostBatch& hb = s->hb;
@@ -411,7 +418,6 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
 static asim_status update_states(asim_search* s, const std::vector<int32_t>& winner_run,
                                  const std::vector<const Run::Cand*>& winner, cudaStream_t st) {
   asim_ctx* ctx = s->ctx;
-  const int32_t M = ctx->hp.M;
   std::vector<int64_t> pub_c;
   std::vector<int32_t> pub_r;
   HostBatch hb;
@@ -570,8 +576,113 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
   return ASIM_OK;
 }
 
+}  // extern "C"
+
+// The fast heuristic (readings C22-C24): one simulation of every active
+// run's current selection per step, then a host decision per run.
+static asim_status run_fast(asim_search* s, cudaStream_t st) {
+  asim_ctx* ctx = s->ctx;
+  const HostProblem& hp = ctx->hp;
+  const int32_t M = hp.M, G = s->G;
+  std::vector<int64_t> good, pm, busy;
+  for (;;) {
+    asim_status rs = asim_ready(ctx);
+    if (rs) return rs;
+    HostBatch hb;
+    hb.G = G;
+    std::vector<int32_t> act;
+    for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r) {
+      Run& run = s->runs[r];
+      if (!run.active) continue;
+      const int32_t b = (int32_t)act.size();
+      act.push_back(r);
+      for (int32_t g = 0; g < G; ++g) hb.base_cfg.push_back(g < run.G ? run.cfg[g] : -1);
+      hb.base_mask.insert(hb.base_mask.end(), run.sel.begin(), run.sel.end());
+      hb.cand_base.push_back(b);
+      hb.cand_model.push_back(-1);  // the selection itself
+      hb.cand_group.push_back(0);
+      hb.cand_ok.push_back(1);
+      int32_t slots = 0;
+      for (int32_t c : run.cfg) slots += hp.cfg_stages[c];
+      hb.slots = std::max(hb.slots, slots);
+    }
+    if (act.empty()) {
+      s->finished = true;
+      return ASIM_OK;
+    }
+    const int64_t C = (int64_t)act.size();
+    cudaError_t e = s->d_good_all.ensure(C * 8 + 8);
+    if (e == cudaSuccess) e = s->d_pm.ensure(C * M * 8 + 8);
+    if (e == cudaSuccess) e = s->d_busy.ensure(C * G * 8 + 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->d_pm.p, 0, C * M * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->d_busy.p, 0, C * G * 8, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "fast heuristic buffers");
+    asim::DevOut out{};
+    out.good = s->d_good_all.as<int64_t>();
+    out.good_per_model = s->d_pm.as<int64_t>();
+    out.busy = s->d_busy.as<int64_t>();
+    asim_status rc = asim_run_batch(ctx, hb, 0, C, out, st);
+    if (rc) return rc;
+    good.resize(C);
+    pm.resize(C * M);
+    busy.resize(C * G);
+    e = cudaMemcpyAsync(good.data(), out.good, C * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pm.data(), out.good_per_model, C * M * 8,
+                                              cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(busy.data(), out.busy, C * G * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "copy fast heuristic results");
+    ++s->steps;
+    s->candidates += C;
+    s->evaluated += C;
+    for (int64_t b = 0; b < C; ++b) {
+      Run& run = s->runs[act[b]];
+      run.base_good = good[b];
+      if (good[b] > run.best_good) {  // best selection so far, strict '>' (C24)
+        run.best_good = good[b];
+        run.best = run.sel;
+      }
+      // C22: the model with the most unserved requests among those with an
+      // available group; C23: its available group with the lowest mean stage
+      // utilization busy_g / s_g (the common horizon cancels)
+      int32_t bm = -1, bgp = -1;
+      int64_t bu = 0;
+      for (int32_t m = 0; m < M; ++m) {
+        const int64_t un = ctx->model_n[m] - pm[b * M + m];
+        if (un <= 0 || (bm >= 0 && un <= bu)) continue;
+        int32_t gbest = -1;
+        for (int32_t g = 0; g < run.G; ++g) {
+          if ((run.sel[m] >> g) & 1ULL) continue;  // a model at most once per group (C11)
+          const int64_t mb = hp.mem_at(m, run.cfg[g]);
+          if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
+          if (gbest < 0 ||
+              (__int128)busy[b * G + g] * hp.cfg_stages[run.cfg[gbest]] <
+                  (__int128)busy[b * G + gbest] * hp.cfg_stages[run.cfg[g]])
+            gbest = g;
+        }
+        if (gbest < 0) continue;
+        bm = m;
+        bgp = gbest;
+        bu = un;
+      }
+      if (bm < 0) {  // every request served, or no available pair: this run ends
+        run.active = false;
+        continue;
+      }
+      run.sel[bm] |= 1ULL << bgp;
+      run.used[bgp] += hp.mem_at(bm, run.cfg[bgp]);
+      run.history.emplace_back(bm, bgp);
+      ++run.steps;
+    }
+  }
+}
+
+extern "C" {
+
 asim_status asim_search_run(asim_search* s, void* cuda_stream) {
   if (!s) return ASIM_EINVAL;
+  if (s->fast) return run_fast(s, static_cast<cudaStream_t>(cuda_stream));
   for (;;) {
     int64_t C = 0;
     asim_status st = asim_search_prepare(s, &C);

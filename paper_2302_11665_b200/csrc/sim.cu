@@ -77,6 +77,7 @@ simulate_kernel(DevProblem pr, DevTrace tr, DevBatch bt, const WarpItem* __restr
   int64_t* pm = (out.good_per_model && in_item)
                     ? out.good_per_model + (c - out.out_offset) * pr.M
                     : nullptr;
+  int64_t* busy = (out.busy && in_item) ? out.busy + (c - out.out_offset) * bt.G : nullptr;
 
   for (int64_t i0 = 0; i0 < tr.n; i0 += 32) {
     // coalesced load of 32 requests; broadcast one at a time by shuffles
@@ -111,14 +112,17 @@ simulate_kernel(DevProblem pr, DevTrace tr, DevBatch bt, const WarpItem* __restr
         const uint32_t e = gt[best_g * 32 + lane];
         const int p = gt_cfg(e), off = gt_off(e), s = gt_stages(e);
         const int64_t* d = stage + ((int64_t)m * P + p) * S;
-        int64_t x = a;
+        int64_t x = a, occ = 0;
         for (int k = 0; k < s; ++k) {
-          x = imax64(x, st[(off + k) * 32 + lane]) + __ldg(d + k);
+          const int64_t dk = __ldg(d + k);
+          x = imax64(x, st[(off + k) * 32 + lane]) + dk;
           st[(off + k) * 32 + lane] = x;
+          occ += dk;
         }
         good += 1;
         sum += best_f - a;
         if (pm) pm[m] += 1;
+        if (busy) busy[best_g] += occ;
       }
     }
   }

@@ -256,7 +256,33 @@ double asim_attainment(int64_t good, int64_t n);
  * feasible addition, the largest unserved wins (ties -> lowest m); among its
  * feasible groups the lowest utilization busy_ns / stages wins (ties ->
  * lowest g); the run stops when no such model exists; the best selection
- * (strict '>') is kept.  Fast mode is driven by asim_search_run only. */
+ * (strict '>') is kept.  Fast mode is driven by asim_search_run only.
+ *
+ * Model and device buckets (spec->buckets = 1; Alg. 2 as printed, P:740-785;
+ * readings C25-C28 in DESIGN.md; requires num_runs = 0):
+ *   get_potential_model_buckets: models sorted by (model_latency_ns, id) are
+ *     cut into contiguous buckets, never between equal latencies, each with
+ *     max latency <= ratio * min latency, and only where needed (no two
+ *     neighbouring buckets could form one valid bucket); ordered by bucket
+ *     count, then cut positions; max_buckets > 0 drops larger partitions.
+ *   get_potential_device_buckets: every (H_1..H_k), H_i >= 1, sum = D, in
+ *     lexicographic order; with k >= 2 kept iff max r <= bound * min r, with
+ *     r_b = (demand_b / sum demand) / (capacity_b / sum capacity), demand_b =
+ *     trace requests of bucket b's models, capacity_b = H_b / mean latency of
+ *     its models (no demand at all: kept).
+ *   each (bucket, H_i) is solved by the runs of the single-bucket
+ *     enumeration over H_i devices, restricted to the bucket's models (the
+ *     whole trace is simulated; other models are simply not hosted); the best
+ *     run (strict '>', first wins) is plm_i*; plm* = concatenation, its good
+ *     the sum of the buckets' goods; the best plm* (strict '>') is the result.
+ * All runs of all buckets advance in lockstep like single-bucket runs (the
+ * fast heuristic applies inside each of them when fast = 1).  The result is
+ * read with asim_search_buckets_get; asim_search_result_get reports the
+ * concatenated placement (best_run = -1) when it has <= ASIM_MAX_GROUPS
+ * groups, else num_groups only.
+ * Errors (asim_search_create): ASIM_EINVAL null latency / bad ratio or bound;
+ * ASIM_ERANGE latency outside [1, 2^60], a run with > ASIM_MAX_GROUPS groups,
+ * or more than 2^20 runs in total. */
 typedef struct {
   int32_t num_runs;              /* 0 = Alg. 2 single-bucket enumeration */
   const int32_t* run_num_groups; /* [num_runs] */
@@ -265,6 +291,11 @@ typedef struct {
                                     identical candidates (exact) */
   int32_t fast;                  /* 1 = the fast heuristic of P:737 instead of
                                     Alg. 1 inside every run (see below) */
+  int32_t buckets;               /* 1 = Alg. 2 with model / device buckets */
+  int32_t max_buckets;           /* 0 = no cap on the bucket count */
+  int64_t ratio_num, ratio_den;  /* bucket latency threshold (SPEC: 4 / 1) */
+  int64_t bound_num, bound_den;  /* discrepancy bound (SPEC: 3 / 1) */
+  const int64_t* model_latency_ns; /* [M] host; single-device latency (Table 1) */
 } asim_search_spec;
 
 typedef struct {
@@ -293,6 +324,24 @@ asim_status asim_search_run_info(const asim_search* s, int32_t run, int32_t* num
                                  int32_t* group_cfg, uint64_t* host_mask, int64_t* best_good,
                                  int64_t* steps);
 int32_t asim_search_num_runs(const asim_search* s);
+
+/* Bucketed result (spec->buckets = 1), after the search finished.  Arrays are
+ * caller-provided host arrays of M entries (a partition has <= M buckets).
+ *   bucket_of_model[m]  bucket of model m in the best partition (-1: none)
+ *   bucket_devices[i]   H_i of bucket i
+ *   bucket_run[i]       run solving bucket i (asim_search_run_info), -1 when no
+ *                       run of the bucket serves any request (plm_i* empty)
+ * ASIM_ESTATE if the search is not bucketed or not finished. */
+typedef struct {
+  int64_t best_good;       /* 0 and num_buckets = 0 if nothing improved on {} */
+  int32_t num_buckets;
+  int64_t partitions;      /* model bucket partitions enumerated */
+  int64_t considered;      /* (partition, device buckets) kept after pruning */
+  int32_t* bucket_of_model;
+  int32_t* bucket_devices;
+  int32_t* bucket_run;
+} asim_bucket_result;
+asim_status asim_search_buckets_get(const asim_search* s, asim_bucket_result* out);
 
 #ifdef __cplusplus
 }

@@ -56,8 +56,10 @@ def _add(mask: np.ndarray, m: int, g: int) -> np.ndarray:
     return out
 
 
-def greedy(prob, trace, group_cfg, threads: int = 0, record: bool = False):
-    """Alg. 1 with k = 1 on fixed groups `group_cfg`.
+def greedy(prob, trace, group_cfg, threads: int = 0, record: bool = False, models=None):
+    """Alg. 1 with k = 1 on fixed groups `group_cfg`; `models` restricts the
+    selectable models (a bucket of Alg. 2: requests of other models
+    are simply not served).
     Returns dict(placement, good, steps=[(candidates, goods, chosen)])."""
     op = prob if isinstance(prob, OracleProblem) else OracleProblem(prob)
     ot = trace if isinstance(trace, OracleTrace) else OracleTrace(trace)
@@ -67,9 +69,10 @@ def greedy(prob, trace, group_cfg, threads: int = 0, record: bool = False):
     sel = np.zeros(M, dtype=np.uint64)
     best_sel, best_good = sel.copy(), 0
     steps = []
+    allowed = range(M) if models is None else sorted(models)
     while True:
         cands = []
-        for m in range(M):
+        for m in allowed:
             for g in range(G):
                 if (int(sel[m]) >> g) & 1:
                     continue  # already hosted on g
@@ -105,7 +108,7 @@ def utilization_busy(prob, model, group_cfg, served_by):
     return busy
 
 
-def greedy_fast(prob, trace, group_cfg, record: bool = False):
+def greedy_fast(prob, trace, group_cfg, record: bool = False, models=None):
     """The fast heuristic of P:737 on fixed groups `group_cfg`.
     Returns dict(placement, good, steps=[(good, (m, g) or None)])."""
     op = prob if isinstance(prob, OracleProblem) else OracleProblem(prob)
@@ -126,7 +129,8 @@ def greedy_fast(prob, trace, group_cfg, record: bool = False):
         unserved = [int(n_m[m]) - int(r["good_per_model"][m]) for m in range(M)]
         busy = utilization_busy(pr, ot.model, cfg, r["served_by"])
         pick = None
-        for m in sorted(range(M), key=lambda m: (-unserved[m], m)):  # most unserved first
+        allowed = range(M) if models is None else models
+        for m in sorted(allowed, key=lambda m: (-unserved[m], m)):  # most unserved first
             if unserved[m] <= 0:
                 break
             # "an available group with the lowest utilization": busy_g / s_g, lowest g on ties
@@ -159,9 +163,10 @@ def alg2_fast(prob, trace, record: bool = False):
     return best
 
 
-def alg2_runs(prob):
-    """Single-bucket Alg. 2 enumeration: [(size, config id, group_cfg list)]."""
-    D = prob.num_devices
+def alg2_runs(prob, D=None):
+    """Single-bucket Alg. 2 enumeration over D devices (default: the cluster):
+    [(size, config id, group_cfg list)]."""
+    D = prob.num_devices if D is None else D
     devs = prob.cfg_devices
     runs = []
     for size in range(1, D + 1):
@@ -246,3 +251,124 @@ def bruteforce(prob, trace, threads: int = 0):
 
 
 __all__ = ["greedy", "alg2", "alg2_runs", "bruteforce", "bruteforce_placements", "simulate"]
+
+
+# ----------------------------------------------------------------- Alg. 2, buckets
+# get_potential_model_buckets / get_potential_device_buckets and the
+# discrepancy pruning (readings C25-C28 in DESIGN.md).
+
+def model_buckets(latency, ratio=Fraction(4), max_buckets=0):
+    """Every model bucket partition (reading C25): models sorted by (latency,
+    id) and cut into contiguous buckets, never between equal latencies; in each
+    bucket max latency <= ratio * min latency ("separate models whose latency
+    difference is larger than a threshold"); cuts only where needed -- no two
+    neighbouring buckets could form one valid bucket.  Ordered by bucket count,
+    then cut positions; max_buckets > 0 drops partitions with more buckets.
+    Returns [[sorted model ids of bucket 1], ...] per partition."""
+    M = len(latency)
+    order = sorted(range(M), key=lambda m: (latency[m], m))
+    lat = [latency[m] for m in order]
+    cut_points = [i for i in range(1, M) if lat[i - 1] < lat[i]]
+
+    def ok(a, b):  # order[a:b] forms one bucket
+        return lat[b - 1] <= ratio * lat[a]
+
+    out = []
+    for k in range(1, M + 1):
+        if max_buckets and k > max_buckets:
+            break
+        for cuts in itertools.combinations(cut_points, k - 1):
+            bounds = [0, *cuts, M]
+            segs = list(zip(bounds[:-1], bounds[1:]))
+            if not all(ok(a, b) for a, b in segs):
+                continue
+            if any(ok(segs[i][0], segs[i + 1][1]) for i in range(len(segs) - 1)):
+                continue  # two neighbours would merge: a cut that is not needed
+            out.append([sorted(order[a:b]) for a, b in segs])
+    return out
+
+
+def device_buckets(D, k):
+    """get_potential_device_buckets: every (H_1, ..., H_k), H_i >= 1, sum D,
+    in lexicographic order (reading C26)."""
+    if k == 1:
+        return [(D,)]
+    out = []
+    for h in range(1, D - k + 2):
+        out += [(h, *rest) for rest in device_buckets(D - h, k - 1)]
+    return out
+
+
+def discrepancy_ok(buckets, H, latency, demand, bound=Fraction(3)):
+    """P:783-785 "eliminate the bucket configurations with high discrepancies in
+    the estimated number of requests it can serve per second" (reading C26,
+    SPEC S:405): capacity_b = H_b / mean latency of bucket b; r_b = demand
+    share / capacity share; kept iff max r <= bound * min r."""
+    if len(buckets) == 1:
+        return True
+    dem = [sum(int(demand[m]) for m in b) for b in buckets]
+    if sum(dem) == 0:
+        return True
+    cap = [Fraction(h) / Fraction(sum(int(latency[m]) for m in b), len(b))
+           for b, h in zip(buckets, H)]
+    r = [Fraction(d, sum(dem)) / (c / sum(cap)) for d, c in zip(dem, cap)]
+    return max(r) <= bound * min(r)
+
+
+def alg2_buckets(prob, trace, latency=None, ratio=Fraction(4), bound=Fraction(3),
+                 max_buckets=0, fast=False, threads: int = 0):
+    """Alg. 2 with model and device buckets.  Each bucket is
+    solved on its own by Alg. 1 (or the fast heuristic) restricted to its
+    models over the whole workload; the bucket's best run wins on
+    strict '>' ("plm.slo_att > plm_i*.slo_att"); the concatenation's good is
+    the sum over buckets (disjoint models and devices); best_plm on strict '>'.
+    Returns dict(good, buckets=[(models, H, run group_cfg, host_mask)], ...)."""
+    op, ot = OracleProblem(prob), OracleTrace(trace)
+    latency = list(prob.meta["latency_ns"] if latency is None else latency)
+    M = prob.num_models
+    demand = np.bincount(ot.model, minlength=M)
+    cache = {}
+
+    def solve(models, h):  # plm_i*: the best of every (G, P) of the bucket
+        key = (tuple(models), h)
+        if key not in cache:
+            best = None
+            for size, p, cfg in alg2_runs(prob, h):
+                if fast:
+                    res = greedy_fast(op, ot, cfg, models=models)
+                else:
+                    res = greedy(op, ot, cfg, threads, models=models)
+                if res["good"] > (best["good"] if best else 0):
+                    best = res
+            cache[key] = best
+        return cache[key]
+
+    best = dict(good=0, buckets=None, partition=None, devices=None)
+    considered = []
+    for part in model_buckets(latency, ratio, max_buckets):
+        for H in device_buckets(prob.num_devices, len(part)):
+            if not discrepancy_ok(part, H, latency, demand, bound):
+                continue
+            considered.append((part, H))
+            sols = [solve(b, h) for b, h in zip(part, H)]
+            good = sum(s["good"] for s in sols if s is not None)
+            if good > best["good"]:
+                best = dict(good=good, partition=part, devices=H,
+                            buckets=[(b, h, s["placement"] if s else None)
+                                     for b, h, s in zip(part, H, sols)])
+    best["considered"] = considered
+    return best
+
+
+def concat(prob, bucket_solutions):
+    """plm* = concat(plm_1*, ..., plm_k*) as one Placement (groups of bucket 1
+    first)."""
+    cfgs, masks = [], np.zeros(prob.num_models, np.uint64)
+    for _, _, pl in bucket_solutions:
+        if pl is None:
+            continue
+        off = len(cfgs)
+        cfgs += [int(c) for c in pl.group_cfg]
+        for m in range(prob.num_models):
+            masks[m] |= np.uint64(int(pl.host_mask[m]) << off)
+    return Placement(np.array(cfgs, np.int32), masks)

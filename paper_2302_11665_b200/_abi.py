@@ -53,7 +53,15 @@ class asim_stats(ctypes.Structure):
 
 class asim_search_spec(ctypes.Structure):
     _fields_ = [("num_runs", i32), ("run_num_groups", vp), ("run_group_cfg", vp),
-                ("dedup", i32), ("fast", i32)]
+                ("dedup", i32), ("fast", i32), ("buckets", i32), ("max_buckets", i32),
+                ("ratio_num", i64), ("ratio_den", i64), ("bound_num", i64), ("bound_den", i64),
+                ("model_latency_ns", vp)]
+
+
+class asim_bucket_result(ctypes.Structure):
+    _fields_ = [("best_good", i64), ("num_buckets", i32), ("partitions", i64),
+                ("considered", i64), ("bucket_of_model", vp), ("bucket_devices", vp),
+                ("bucket_run", vp)]
 
 
 class asim_search_result(ctypes.Structure):
@@ -104,6 +112,7 @@ asim_search_result_get = _bind("asim_search_result_get", i32, [vp, _P(asim_searc
 asim_search_run_info = _bind("asim_search_run_info", i32,
                              [vp, i32, _P(i32), vp, vp, _P(i64), _P(i64)])
 asim_search_num_runs = _bind("asim_search_num_runs", i32, [vp])
+asim_search_buckets_get = _bind("asim_search_buckets_get", i32, [vp, _P(asim_bucket_result)])
 
 EXPORTED = [n for n in dir() if n.startswith("asim_") and callable(globals()[n])
             and not isinstance(globals()[n], type)]

@@ -64,6 +64,27 @@ class SearchResult:
     runs: list
 
 
+@dataclass
+class BucketResult:
+    """Alg. 2 with model / device buckets: the best partition (sorted model ids
+    per bucket), its device counts, the run solving each bucket (-1: empty),
+    and the concatenated placement (groups of bucket 1 first)."""
+    best_good: int
+    partition: list
+    devices: list
+    bucket_runs: list
+    group_cfg: np.ndarray
+    host_mask: np.ndarray
+    partitions: int
+    considered: int
+    search: SearchResult
+
+    @property
+    def placement(self):
+        from types import SimpleNamespace
+        return SimpleNamespace(group_cfg=self.group_cfg, host_mask=self.host_mask)
+
+
 class Simulator:
     """One asim context on one CUDA device (one per process and GPU)."""
 
@@ -179,8 +200,37 @@ class Simulator:
                     argmax=int(am[0]) if argmax else None, busy_ns=bz)
 
     # ------------------------------------------------------------- search
-    def search_handle(self, runs=None, dedup=True, fast=False) -> "SearchHandle":
-        return SearchHandle(self, runs, dedup, fast)
+    def search_handle(self, runs=None, dedup=True, fast=False, buckets=None) -> "SearchHandle":
+        return SearchHandle(self, runs, dedup, fast, buckets)
+
+    def search_buckets(self, latency, ratio=4, bound=3, max_buckets=0, fast=False, dedup=True,
+                       pg=None, stream=None) -> BucketResult:
+        """Alg. 2 with model and device buckets (include/asim.h).
+        latency[m]: single-device latency in ns; ratio / bound: ints or
+        fractions.Fraction (threshold 4x and discrepancy bound 3x by default)."""
+        from fractions import Fraction
+
+        from . import dist
+
+        b = dict(latency=_host(latency, np.int64), ratio=Fraction(ratio), bound=Fraction(bound),
+                 max_buckets=int(max_buckets))
+        with self.search_handle(None, dedup, fast, b) as sh:
+            if fast:
+                sh.run(stream=stream)
+            else:
+                dist.run_search(sh, pg=pg, stream=stream)
+            res = sh.result()
+            M = self.M
+            of = np.full(M, -1, np.int32)
+            dv = np.zeros(M, np.int32)
+            br = np.full(M, -1, np.int32)
+            r = A.asim_bucket_result(0, 0, 0, 0, _ptr(of), _ptr(dv), _ptr(br))
+            self._check(A.asim_search_buckets_get(sh.h, ctypes.byref(r)))
+            k = r.num_buckets
+            part = [sorted(int(m) for m in np.nonzero(of == i)[0]) for i in range(k)]
+            return BucketResult(r.best_good, part, [int(x) for x in dv[:k]],
+                                [int(x) for x in br[:k]], res.group_cfg, res.host_mask,
+                                r.partitions, r.considered, res)
 
     def search(self, runs=None, dedup=True, pg=None, stream=None, fast=False) -> SearchResult:
         """Full Alg. 2 (single bucket) / Alg. 1 search.  With a
@@ -201,9 +251,16 @@ class Simulator:
 class SearchHandle:
     """Stepwise search protocol of include/asim.h (prepare / evaluate / apply)."""
 
-    def __init__(self, sim: Simulator, runs=None, dedup=True, fast=False):
+    def __init__(self, sim: Simulator, runs=None, dedup=True, fast=False, buckets=None):
         self.sim = sim
-        if runs is None:
+        if buckets is not None:
+            lat = buckets["latency"]
+            spec = A.asim_search_spec(0, None, None, int(bool(dedup)), int(bool(fast)), 1,
+                                      buckets["max_buckets"], buckets["ratio"].numerator,
+                                      buckets["ratio"].denominator, buckets["bound"].numerator,
+                                      buckets["bound"].denominator, _ptr(lat))
+            self._keep = (lat,)
+        elif runs is None:
             spec = A.asim_search_spec(0, None, None, int(bool(dedup)), int(bool(fast)))
             self._keep = ()
         else:

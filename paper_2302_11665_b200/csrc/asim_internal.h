@@ -147,6 +147,12 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
                               int64_t* launches);
 cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
                                 int64_t* launches);
+// Fast heuristic statistics: one warp per item (one candidate each, uniform
+// config, S class != 0) over the whole trace; writes good, sum, per-model good
+// and per-group busy into `out`.  fast_stats_smem: dynamic shared memory.
+size_t fast_stats_smem(int slots_max, int M, bool u32);
+cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32, cudaStream_t st,
+                              int64_t* launches);
 // Pass 3: re-simulate every chunk whose start state was wrong (per lane) and
 // record in bit `lane` of end_src[j * items + item] whether that lane's true
 // end of chunk j is in spec_end (0) or fix_end (1).

@@ -742,6 +742,128 @@ __device__ __forceinline__ T warp_min(T v) {
   }
 }
 
+// One warp simulates ONE candidate over requests [i_begin, i_end): state v
+// (slot = lane + 32 q) in registers, epoch E (uint32 mode).  STATS adds the
+// fast heuristic's outputs: per-model good counts in shared memory (cnt[M])
+// and per-group busy time in registers (busy[q2] = group lane + 32 q2).
+template <typename T, int S, int Q, bool STATS>
+__device__ __forceinline__ void coop_range(const ChunkParams& P, const WarpMem<T>& w,
+                                           int64_t i_begin, int64_t i_end, T (&v)[Q], int64_t& E,
+                                           uint64_t kmask, int my_m, uint64_t my_bit,
+                                           const uint64_t (&lastbit)[Q], int lane, int64_t& good,
+                                           int64_t& sum, unsigned long long& upd,
+                                           int32_t* cnt, int64_t (&busy)[2]) {
+  for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
+    const bool valid = i0 + lane < i_end;
+    const int64_t al = valid ? P.tr.arrival[i0 + lane] : 0;
+    const int ml = valid ? (int)P.tr.model[i0 + lane] : 0;
+    unsigned todo = __ballot_sync(FULL, valid && ((kmask >> (ml & 63)) & 1ull));
+    if (!todo) continue;
+    bool per_req = false;
+    if constexpr (TT<T>::kRel) {
+      const int64_t a_last = __shfl_sync(FULL, al, 31 - __clz(todo));
+      if (a_last - E > P.theta) {  // move the epoch to the tile's first request
+        const int64_t a_first = __shfl_sync(FULL, al, __ffs(todo) - 1);
+        const int64_t gap = a_first - E;
+        const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) v[q] = v[q] > delta ? v[q] - delta : (T)0;
+        E = a_first;
+        per_req = a_last - E > P.theta;
+      }
+    }
+    // lane-parallel per-request fields of the tile, broadcast by independent
+    // shuffles (no shared-memory load on the per-request dependent chain)
+    const T arl = (T)(al - E);
+    const uint64_t hml = w.hmask[ml] | (ml == my_m ? my_bit : 0ull);
+    const T tll = w.tail[ml], sll = w.slo[ml];
+    T dkl = 0;
+    if constexpr (S == 1) dkl = w.d[ml * kSTab];
+    int64_t occl = 0;  // sum_k d_k of the lane's request (STATS)
+    if constexpr (STATS) {
+#pragma unroll
+      for (int k = 0; k < S; ++k) occl += (int64_t)w.d[ml * kSTab + k];
+    }
+    {
+      const bool rel = (todo >> lane) & 1u;
+      upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popcll(hml) : 0u) * S;
+    }
+    while (todo) {
+      const int jj = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int m = __shfl_sync(FULL, ml, jj);
+      T ar = __shfl_sync(FULL, arl, jj);
+      const uint64_t hm = __shfl_sync(FULL, hml, jj);
+      const T tl = __shfl_sync(FULL, tll, jj), sl = __shfl_sync(FULL, sll, jj);
+      T dk = 0;
+      if constexpr (S == 1) dk = __shfl_sync(FULL, dkl, jj);
+      if constexpr (TT<T>::kRel) {
+        if (per_req) {
+          const int64_t a = __shfl_sync(FULL, al, jj);
+          if (a - E > P.theta) {
+            const int64_t gap = a - E;
+            const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) v[q] = v[q] > delta ? v[q] - delta : (T)0;
+            E = a;
+          }
+          ar = (T)(a - E);
+        }
+      }
+      // predicted finish at the last stage of every hosting group
+      T y[Q], f[Q];
+      T fl = TT<T>::maxv();
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if constexpr (S == 1) {
+          y[q] = tmax(ar, v[q]) + dk;
+        } else {
+          const int k = (lane + 32 * q) % S;
+          const T d = w.d[m * kSTab + k];
+          T A = d, B = v[q] + d;
+#pragma unroll
+          for (int o = 1; o < S; o <<= 1) {
+            const T A2 = __shfl_up_sync(FULL, A, o, S), B2 = __shfl_up_sync(FULL, B, o, S);
+            if (k >= o) {
+              B = tmax(B2 + A, B);
+              A = A2 + A;
+            }
+          }
+          y[q] = tmax(ar + A, B);
+        }
+        f[q] = (hm & lastbit[q]) ? y[q] + tl : TT<T>::maxv();
+        fl = tmin(fl, f[q]);
+      }
+      const T fmin = warp_min<T>(fl);
+      if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) continue;  // no host / misses the SLO
+      // lowest group index among the minima (slots ascend with q, then lane)
+      int wq = 0, wl = 0;
+#pragma unroll
+      for (int q = Q - 1; q >= 0; --q) {
+        const unsigned b = __ballot_sync(FULL, f[q] == fmin);
+        if (b) {
+          wq = q;
+          wl = __ffs(b) - 1;
+        }
+      }
+      const int gw = (wl + 32 * wq) / S;
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (q == wq && (lane + 32 * q) / S == gw) v[q] = y[q];
+      ++good;
+      sum += (int64_t)(fmin - ar);
+      if constexpr (STATS) {
+        const int64_t occ = __shfl_sync(FULL, occl, jj);
+        if (lane == 0) cnt[m] += 1;
+        if (lane == (gw & 31)) {  // constant indices keep busy[] in registers
+          if (gw >> 5) busy[1] += occ;
+          else busy[0] += occ;
+        }
+      }
+    }
+  }
+}
+
 template <typename T, int S, int Q>
 __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpMem<T>& w,
                                                const ItemDesc& it, int item, int cl, int lane,
@@ -798,102 +920,9 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
       }
     }
     int64_t good = 0, sum = 0;
-    for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
-      const bool valid = i0 + lane < i_end;
-      const int64_t al = valid ? P.tr.arrival[i0 + lane] : 0;
-      const int ml = valid ? (int)P.tr.model[i0 + lane] : 0;
-      unsigned todo = __ballot_sync(FULL, valid && ((kmask >> (ml & 63)) & 1ull));
-      if (!todo) continue;
-      bool per_req = false;
-      if constexpr (TT<T>::kRel) {
-        const int64_t a_last = __shfl_sync(FULL, al, 31 - __clz(todo));
-        if (a_last - E > P.theta) {  // move the epoch to the tile's first request
-          const int64_t a_first = __shfl_sync(FULL, al, __ffs(todo) - 1);
-          const int64_t gap = a_first - E;
-          const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
-#pragma unroll
-          for (int q = 0; q < Q; ++q) v[q] = v[q] > delta ? v[q] - delta : (T)0;
-          E = a_first;
-          per_req = a_last - E > P.theta;
-        }
-      }
-      // lane-parallel per-request fields of the tile, broadcast by independent
-      // shuffles (no shared-memory load on the per-request dependent chain)
-      const T arl = (T)(al - E);
-      const uint64_t hml = w.hmask[ml] | (ml == my_m ? my_bit : 0ull);
-      const T tll = w.tail[ml], sll = w.slo[ml];
-      T dkl = 0;
-      if constexpr (S == 1) dkl = w.d[ml * kSTab];
-      {
-        const bool rel = (todo >> lane) & 1u;
-        upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popcll(hml) : 0u) * S;
-      }
-      while (todo) {
-        const int jj = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int m = __shfl_sync(FULL, ml, jj);
-        T ar = __shfl_sync(FULL, arl, jj);
-        const uint64_t hm = __shfl_sync(FULL, hml, jj);
-        const T tl = __shfl_sync(FULL, tll, jj), sl = __shfl_sync(FULL, sll, jj);
-        T dk = 0;
-        if constexpr (S == 1) dk = __shfl_sync(FULL, dkl, jj);
-        if constexpr (TT<T>::kRel) {
-          if (per_req) {
-            const int64_t a = __shfl_sync(FULL, al, jj);
-            if (a - E > P.theta) {
-              const int64_t gap = a - E;
-              const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
-#pragma unroll
-              for (int q = 0; q < Q; ++q) v[q] = v[q] > delta ? v[q] - delta : (T)0;
-              E = a;
-            }
-            ar = (T)(a - E);
-          }
-        }
-        // predicted finish at the last stage of every hosting group
-        T y[Q], f[Q];
-        T fl = TT<T>::maxv();
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          if constexpr (S == 1) {
-            y[q] = tmax(ar, v[q]) + dk;
-          } else {
-            const int k = (lane + 32 * q) % S;
-            const T d = w.d[m * kSTab + k];
-            T A = d, B = v[q] + d;
-#pragma unroll
-            for (int o = 1; o < S; o <<= 1) {
-              const T A2 = __shfl_up_sync(FULL, A, o, S), B2 = __shfl_up_sync(FULL, B, o, S);
-              if (k >= o) {
-                B = tmax(B2 + A, B);
-                A = A2 + A;
-              }
-            }
-            y[q] = tmax(ar + A, B);
-          }
-          f[q] = (hm & lastbit[q]) ? y[q] + tl : TT<T>::maxv();
-          fl = tmin(fl, f[q]);
-        }
-        const T fmin = warp_min<T>(fl);
-        if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) continue;  // no host / misses the SLO
-        // lowest group index among the minima (slots ascend with q, then lane)
-        int wq = 0, wl = 0;
-#pragma unroll
-        for (int q = Q - 1; q >= 0; --q) {
-          const unsigned b = __ballot_sync(FULL, f[q] == fmin);
-          if (b) {
-            wq = q;
-            wl = __ffs(b) - 1;
-          }
-        }
-        const int gw = (wl + 32 * wq) / S;
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-          if (q == wq && (lane + 32 * q) / S == gw) v[q] = y[q];
-        ++good;
-        sum += (int64_t)(fmin - ar);
-      }
-    }
+    int64_t busy_unused[2] = {0, 0};
+    coop_range<T, S, Q, false>(P, w, i_begin, i_end, v, E, kmask, my_m, my_bit, lastbit, lane,
+                               good, sum, upd, nullptr, busy_unused);
     // the chunk's exact correction, and equivalence with the speculative end
     if (lane == 0) {
       P.fix_good[j * cstride + (int64_t)item * 32 + cl] =
@@ -995,6 +1024,82 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     if (P.walked && walked) atomicAdd(P.walked, walked);
     if (P.stage_updates && upd) atomicAdd(P.stage_updates, upd);
   }
+}
+
+// Fast heuristic statistics (search.cpp run_fast): one warp per
+// candidate of a uniform-config item simulates the whole trace from idle with
+// the warp-cooperative recurrence and writes good, sum, per-model good and
+// per-group busy.  Items hold one candidate each (cl = 0).
+template <typename T, int S, int Q>
+__device__ __forceinline__ void fast_candidate(const ChunkParams& P, const WarpMem<T>& w,
+                                               const ItemDesc& it, int lane, int32_t* cnt,
+                                               const DevOut& out, unsigned long long& upd) {
+  const int64_t c = it.first;
+  const int slots = it.slots;
+  uint64_t lastbit[Q];
+  T v[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int t = lane + 32 * q;
+    lastbit[q] = (t < slots && t % S == S - 1) ? (1ull << ((t / S) & 63)) : 0ull;
+    v[q] = 0;  // idle
+  }
+  const int my_m = P.bt.cand_model[c], my_g = P.bt.cand_group[c];
+  const uint64_t my_bit = my_m >= 0 ? (1ull << my_g) : 0ull;
+  int64_t E = (TT<T>::kRel && P.tr.n > 0) ? P.tr.arrival[0] : 0;
+  int64_t good = 0, sum = 0;
+  int64_t busy[2] = {0, 0};
+  coop_range<T, S, Q, true>(P, w, 0, P.tr.n, v, E, ~0ull, my_m, my_bit, lastbit, lane, good, sum,
+                            upd, cnt, busy);
+  __syncwarp();
+  const int64_t o = c - out.out_offset;
+  if (lane == 0) {
+    out.good[o] = good;
+    if (out.sum_latency) out.sum_latency[o] = sum;
+  }
+  if (out.good_per_model)
+    for (int m = lane; m < P.pr.M; m += 32) out.good_per_model[o * P.pr.M + m] = cnt[m];
+  if (out.busy) {
+    if (lane < P.bt.G) out.busy[o * P.bt.G + lane] = busy[0];
+    if (lane + 32 < P.bt.G) out.busy[o * P.bt.G + lane + 32] = busy[1];
+  }
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void fast_dispatch_q(const ChunkParams& P, const WarpMem<T>& w,
+                                                const ItemDesc& it, int lane, int32_t* cnt,
+                                                const DevOut& out, unsigned long long& upd) {
+  switch ((it.slots + 31) / 32) {
+    case 1: fast_candidate<T, S, 1>(P, w, it, lane, cnt, out, upd); break;
+    case 2: fast_candidate<T, S, 2>(P, w, it, lane, cnt, out, upd); break;
+    case 3: fast_candidate<T, S, 3>(P, w, it, lane, cnt, out, upd); break;
+    default: fast_candidate<T, S, 4>(P, w, it, lane, cnt, out, upd); break;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) fast_stats_kernel(ChunkParams P, DevOut out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  const size_t cb = ((size_t)P.pr.M * 4 + 15) & ~size_t(15);
+  unsigned char* mine = smem + warp * (wb + cb);
+  WarpMem<T> w = carve<T>(mine, P, false);
+  int32_t* cnt = reinterpret_cast<int32_t*>(mine + wb);
+  const int item = blockIdx.x * kWarps + warp;
+  if (item >= P.num_items) return;
+  const ItemDesc it = P.items[item];
+  for (int m = lane; m < P.pr.M; m += 32) cnt[m] = 0;
+  load_base<T>(P, it, w, lane);
+  unsigned long long upd = 0;
+  switch (it.S) {
+    case 1: fast_dispatch_q<T, 1>(P, w, it, lane, cnt, out, upd); break;
+    case 2: fast_dispatch_q<T, 2>(P, w, it, lane, cnt, out, upd); break;
+    case 4: fast_dispatch_q<T, 4>(P, w, it, lane, cnt, out, upd); break;
+    case 8: fast_dispatch_q<T, 8>(P, w, it, lane, cnt, out, upd); break;
+    default: fast_dispatch_q<T, 16>(P, w, it, lane, cnt, out, upd); break;
+  }
+  if (lane == 0 && P.stage_updates && upd) atomicAdd(P.stage_updates, upd);
 }
 
 // good[c] = sum_j spec_good[j][c] + sum_{j>=1} fix_good[j][c] (same for sums)
@@ -1183,6 +1288,32 @@ cudaError_t launch_mix_states(int64_t C0, int64_t C1, int32_t J, int32_t stride,
   if (n <= 0) return cudaSuccess;
   mix_states_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(C0, C1, J, stride, bcur, bprev,
                                                                  cprev, rows, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+size_t fast_stats_smem(int slots_max, int M, bool u32) {
+  const size_t wb = warp_bytes(slots_max, M, u32 ? 4 : 8, false);
+  return kWarps * (wb + (((size_t)M * 4 + 15) & ~size_t(15)));
+}
+
+cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32, cudaStream_t st,
+                              int64_t* launches) {
+  if (P.num_items <= 0) return cudaSuccess;
+  const size_t smem = fast_stats_smem(P.slots_max, P.pr.M, u32);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  const unsigned blocks = (unsigned)((P.num_items + kWarps - 1) / kWarps);
+  cudaError_t e;
+  if (u32) {
+    e = cudaFuncSetAttribute(fast_stats_kernel<uint32_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) fast_stats_kernel<uint32_t><<<blocks, kWarps * 32, smem, st>>>(P, out);
+  } else {
+    e = cudaFuncSetAttribute(fast_stats_kernel<int64_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) fast_stats_kernel<int64_t><<<blocks, kWarps * 32, smem, st>>>(P, out);
+  }
+  if (e != cudaSuccess) return e;
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -35,6 +35,83 @@ static int64_t theta_for(const asim_ctx* ctx) {
   return (int64_t)th;
 }
 
+asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out,
+                                cudaStream_t st, bool* done) {
+  *done = false;
+  const HostProblem& hp = ctx->hp;
+  const int64_t C = (int64_t)hb.cand_base.size();
+  if (C == 0) {
+    *done = true;
+    return ASIM_OK;
+  }
+  std::vector<asim::ItemDesc> items;
+  int32_t slots_max = 1;
+  for (int64_t c = 0; c < C; ++c) {
+    const int32_t b = hb.cand_base[c];
+    int32_t u = -2, slots = 0;
+    bool hole = false;
+    for (int32_t g = 0; g < hb.G; ++g) {
+      const int32_t k = hb.base_cfg[(int64_t)b * hb.G + g];
+      if (k < 0) {
+        hole = true;
+        continue;
+      }
+      slots += hp.cfg_stages[k];
+      u = (!hole && (u == -2 || u == k)) ? k : -1;
+    }
+    if (u < 0 || !hb.cand_ok[c] || hb.cand_model[c] >= 0) return ASIM_OK;
+    asim::ItemDesc it{};
+    it.base = b;
+    it.first = (int32_t)c;
+    it.count = 1;
+    it.cfg = u;
+    it.stages = hp.cfg_stages[u];
+    it.S = stage_class(it.stages);
+    it.slots = slots;
+    if (it.S == 0 || slots > ASIM_MAX_SLOTS) return ASIM_OK;
+    slots_max = std::max(slots_max, slots);
+    items.push_back(it);
+  }
+  const int64_t theta = ctx->force_path == 3 ? -1 : theta_for(ctx);
+  const bool u32 = theta > 0;
+  if (asim::fast_stats_smem(slots_max, hp.M, u32) > 227 * 1024) return ASIM_OK;
+  cudaError_t e = upload(ctx->c_items, items, st);
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "upload fast items");
+  asim::ChunkParams P{};
+  P.pr = ctx->dev_problem();
+  P.tr = ctx->dev_trace();
+  P.bt.G = hb.G;
+  P.bt.base_cfg = ctx->d_base_cfg.as<int32_t>();
+  P.bt.base_mask = ctx->d_base_mask.as<uint64_t>();
+  P.bt.cand_base = ctx->d_cand_base.as<int32_t>();
+  P.bt.cand_model = ctx->d_cand_model.as<int32_t>();
+  P.bt.cand_group = ctx->d_cand_group.as<int32_t>();
+  P.bt.cand_ok = ctx->d_cand_ok.as<uint8_t>();
+  P.bt.C = C;
+  P.items = ctx->c_items.as<asim::ItemDesc>();
+  P.num_items = (int32_t)items.size();
+  P.J = 1;
+  P.theta = theta;
+  P.slots_max = slots_max;
+  P.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (ctx->profiling) {
+    if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
+      return asim_cuda(ctx, cudaGetLastError(), "event create");
+    cudaEventRecord(ev0, st);
+  }
+  e = asim::launch_fast_stats(P, out, u32, st, &ctx->launches);
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "fast statistics kernel");
+  if (ctx->profiling) {
+    cudaEventRecord(ev1, st);
+    ctx->events.emplace_back(ev0, ev1);
+    ++ctx->sim_launches;
+    ctx->request_evals += C * ctx->n;
+  }
+  *done = true;
+  return ASIM_OK;
+}
+
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                              const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
   const int64_t N = ctx->n;
@@ -47,11 +124,16 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   base_slots.assign(B, 0);
   for (int32_t b = 0; b < B; ++b) {
     int32_t u = -2, slots = 0;
+    bool hole = false;
     for (int32_t g = 0; g < hb.G; ++g) {
       const int32_t c = hb.base_cfg[(int64_t)b * hb.G + g];
-      if (c < 0) continue;
+      if (c < 0) {
+        hole = true;
+        continue;
+      }
       slots += hp.cfg_stages[c];
-      u = (u == -2 || u == c) ? c : -1;
+      // uniform kernels address group g's stages at g * S: no gaps allowed
+      u = (!hole && (u == -2 || u == c)) ? c : -1;
     }
     base_cfg_uniform[b] = u >= 0 ? u : -1;
     base_slots[b] = slots;

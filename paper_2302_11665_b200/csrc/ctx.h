@@ -149,6 +149,12 @@ struct ChunkOptions {
   int32_t state_stride = 0;
 };
 bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out);
+// Fast heuristic statistics (good, sum, per-model good, per-group busy) of
+// every candidate of hb with the warp-cooperative whole-trace kernel; *done =
+// false (nothing launched) when some base is not a gap-free uniform config of
+// a supported stage count, or its tables do not fit shared memory.
+asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out,
+                                cudaStream_t st, bool* done);
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                              const asim::DevOut& out, cudaStream_t st,
                              const ChunkOptions* opt = nullptr);

@@ -50,6 +50,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <new>
 #include <string>
@@ -62,6 +63,7 @@ namespace {
 struct Run {
   int32_t G = 0;
   std::vector<int32_t> cfg;
+  std::vector<uint8_t> allowed;  // [M] selectable models (a bucket); empty = all
   std::vector<uint64_t> sel;   // [M] current selection (the base)
   std::vector<int64_t> used;   // [G] bytes per device
   std::vector<uint64_t> best;  // [M] best selection so far
@@ -95,7 +97,61 @@ struct Run {
     while (parent[x] != x) x = parent[x] = parent[parent[x]];
     return x;
   }
+  bool may_place(int32_t m) const { return allowed.empty() || allowed[m]; }
 };
+
+// Alg. 2 with buckets: one job per distinct (model bucket, H)
+// solved by `runs`; one combo per kept (partition, device buckets).
+struct BucketJob {
+  std::vector<int32_t> models;
+  int32_t H = 0;
+  std::vector<int32_t> runs;
+};
+struct BucketCombo {
+  int32_t partition = 0;
+  std::vector<int32_t> H;
+  std::vector<int32_t> jobs;
+};
+
+// 256-bit unsigned products for the exact discrepancy test (bounded inputs:
+// every product below stays under 2^230).
+struct U256 {
+  uint64_t w[4] = {0, 0, 0, 0};
+};
+U256 u256(unsigned __int128 x) {
+  U256 r;
+  r.w[0] = (uint64_t)x;
+  r.w[1] = (uint64_t)(x >> 64);
+  return r;
+}
+U256 mul64(const U256& a, uint64_t b) {
+  U256 r;
+  unsigned __int128 carry = 0;
+  for (int i = 0; i < 4; ++i) {
+    const unsigned __int128 t = (unsigned __int128)a.w[i] * b + carry;
+    r.w[i] = (uint64_t)t;
+    carry = t >> 64;
+  }
+  return r;
+}
+U256 mul128(const U256& a, unsigned __int128 b) {
+  const U256 lo = mul64(a, (uint64_t)b);
+  const U256 hi = mul64(a, (uint64_t)(b >> 64));
+  U256 r;
+  unsigned __int128 carry = 0;
+  for (int i = 0; i < 4; ++i) {
+    const unsigned __int128 t =
+        (unsigned __int128)lo.w[i] + (i ? hi.w[i - 1] : 0) + carry;
+    r.w[i] = (uint64_t)t;
+    carry = t >> 64;
+  }
+  return r;
+}
+bool u256_le(const U256& a, const U256& b) {
+  for (int i = 3; i >= 0; --i)
+    if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  return true;
+}
 
 }  // namespace
 
@@ -126,6 +182,11 @@ struct asim_search {
   // fast heuristic: per-model good and per-group busy of each base
   bool fast = false;
   DBuf d_pm, d_busy;
+  // Alg. 2 with buckets
+  bool bucketed = false;
+  std::vector<std::vector<std::vector<int32_t>>> partitions;
+  std::vector<BucketJob> jobs;
+  std::vector<BucketCombo> combos;
   // statistics
   int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0, base_passes = 0;
   bool finished = false;
@@ -153,6 +214,179 @@ static void component_masks(const Run& run, int32_t m, int32_t g, int32_t r1, in
   *gmask = run.rootG[r1] | run.rootG[r2] | (1ULL << g);
 }
 
+// Single-bucket enumeration over H devices (reading C13): for every divisor
+// size of H (ascending) and config of that size (ascending id), H/size groups.
+static asim_status bucket_runs(asim_ctx* ctx, int32_t H, std::vector<std::vector<int32_t>>* out) {
+  const HostProblem& hp = ctx->hp;
+  for (int32_t size = 1; size <= H; ++size) {
+    if (H % size) continue;
+    for (int32_t p = 0; p < hp.P; ++p) {
+      if (hp.cfg_devices[p] != size) continue;
+      const int32_t G = H / size;
+      if (G > ASIM_MAX_GROUPS)
+        return asim_fail(ctx, ASIM_ERANGE,
+                         "Alg. 2 run with more than ASIM_MAX_GROUPS groups; pass explicit runs");
+      out->emplace_back(G, p);
+    }
+  }
+  return ASIM_OK;
+}
+
+// get_potential_model_buckets (reading C25): backtracking over cut positions
+// in lexicographic order for each bucket count k.
+static void model_partitions(const std::vector<int64_t>& lat, const std::vector<int32_t>& order,
+                             int64_t rn, int64_t rd, int32_t max_buckets,
+                             std::vector<std::vector<std::vector<int32_t>>>* out, size_t cap) {
+  const int32_t M = (int32_t)order.size();
+  auto ok = [&](int32_t a, int32_t b) {  // order[a, b) forms one bucket
+    return (unsigned __int128)lat[order[b - 1]] * (uint64_t)rd <=
+           (unsigned __int128)(uint64_t)rn * lat[order[a]];
+  };
+  std::vector<int32_t> cuts;
+  for (int32_t k = 1; k <= M && (max_buckets <= 0 || k <= max_buckets); ++k) {
+    // rec(prev_start, seg_start, left): choose the next cut > seg_start
+    std::function<void(int32_t, int32_t, int32_t)> rec = [&](int32_t prev, int32_t a,
+                                                              int32_t left) {
+      if (out->size() > cap) return;
+      if (left == 0) {
+        if (!ok(a, M) || (prev >= 0 && ok(prev, M))) return;
+        std::vector<std::vector<int32_t>> part;
+        int32_t lo = 0;
+        for (size_t i = 0; i <= cuts.size(); ++i) {
+          const int32_t hi = i < cuts.size() ? cuts[i] : M;
+          std::vector<int32_t> b(order.begin() + lo, order.begin() + hi);
+          std::sort(b.begin(), b.end());
+          part.push_back(std::move(b));
+          lo = hi;
+        }
+        out->push_back(std::move(part));
+        return;
+      }
+      for (int32_t c = a + 1; c < M; ++c) {
+        if (lat[order[c - 1]] == lat[order[c]]) continue;  // never between equal latencies
+        if (!ok(a, c)) break;                               // longer segments stay invalid
+        if (prev >= 0 && ok(prev, c)) continue;             // would merge with its neighbour
+        cuts.push_back(c);
+        rec(a, c, left - 1);
+        cuts.pop_back();
+      }
+    };
+    rec(-1, 0, k - 1);
+  }
+}
+
+// get_potential_device_buckets (reading C26), lexicographic.
+static void compositions(int32_t D, int32_t k, std::vector<int32_t>& cur,
+                         std::vector<std::vector<int32_t>>* out, size_t cap) {
+  if (out->size() > cap) return;
+  if (k == 1) {
+    cur.push_back(D);
+    out->push_back(cur);
+    cur.pop_back();
+    return;
+  }
+  for (int32_t h = 1; h <= D - k + 1; ++h) {
+    cur.push_back(h);
+    compositions(D - h, k - 1, cur, out, cap);
+    cur.pop_back();
+  }
+}
+
+// Discrepancy pruning (reading C26): r_b ~ demand_b * sumlat_b / (H_b * n_b).
+static bool discrepancy_ok(const std::vector<std::vector<int32_t>>& part,
+                           const std::vector<int32_t>& H, const std::vector<int64_t>& lat,
+                           const std::vector<int64_t>& demand, int64_t bn, int64_t bd) {
+  const size_t k = part.size();
+  if (k == 1) return true;
+  std::vector<uint64_t> dem(k, 0);
+  std::vector<unsigned __int128> sl(k, 0);
+  uint64_t total = 0;
+  for (size_t b = 0; b < k; ++b)
+    for (int32_t m : part[b]) {
+      dem[b] += (uint64_t)demand[m];
+      sl[b] += (unsigned __int128)lat[m];
+    }
+  for (uint64_t d : dem) total += d;
+  if (total == 0) return true;
+  for (size_t i = 0; i < k; ++i)
+    for (size_t j = 0; j < k; ++j) {
+      if (i == j) continue;
+      // r_i <= bound * r_j
+      U256 l = mul128(u256(dem[i]), sl[i]);
+      l = mul64(mul64(mul64(l, (uint64_t)H[j]), (uint64_t)part[j].size()), (uint64_t)bd);
+      U256 r = mul128(u256(dem[j]), sl[j]);
+      r = mul64(mul64(mul64(r, (uint64_t)H[i]), (uint64_t)part[i].size()), (uint64_t)bn);
+      if (!u256_le(l, r)) return false;
+    }
+  return true;
+}
+
+static constexpr size_t kMaxRuns = size_t(1) << 20;
+
+// Builds the bucketed run list: groups/allowed per run, jobs and combos.
+static asim_status bucket_plan(asim_ctx* ctx, const asim_search_spec* spec, asim_search* s,
+                               std::vector<std::vector<int32_t>>* groups,
+                               std::vector<std::vector<uint8_t>>* allowed) {
+  const HostProblem& hp = ctx->hp;
+  const int32_t M = hp.M;
+  if (spec->num_runs != 0) return asim_fail(ctx, ASIM_EINVAL, "buckets require num_runs = 0");
+  if (!spec->model_latency_ns) return asim_fail(ctx, ASIM_EINVAL, "null model_latency_ns");
+  if (spec->ratio_num <= 0 || spec->ratio_den <= 0 || spec->bound_num <= 0 || spec->bound_den <= 0)
+    return asim_fail(ctx, ASIM_EINVAL, "ratio and bound must be positive fractions");
+  std::vector<int64_t> lat(spec->model_latency_ns, spec->model_latency_ns + M);
+  for (int64_t l : lat)
+    if (l < 1 || l > (int64_t(1) << 60))
+      return asim_fail(ctx, ASIM_ERANGE, "model_latency_ns outside [1, 2^60]");
+  std::vector<int32_t> order(M);
+  for (int32_t m = 0; m < M; ++m) order[m] = m;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return lat[a] < lat[b]; });
+  model_partitions(lat, order, spec->ratio_num, spec->ratio_den, spec->max_buckets,
+                   &s->partitions, kMaxRuns);
+  if (s->partitions.size() > kMaxRuns)
+    return asim_fail(ctx, ASIM_ERANGE, "too many model bucket partitions");
+  std::map<std::pair<std::vector<int32_t>, int32_t>, int32_t> job_of;
+  for (int32_t pi = 0; pi < (int32_t)s->partitions.size(); ++pi) {
+    const auto& part = s->partitions[pi];
+    std::vector<std::vector<int32_t>> splits;
+    std::vector<int32_t> cur;
+    compositions(hp.num_devices, (int32_t)part.size(), cur, &splits, kMaxRuns);
+    if (splits.size() > kMaxRuns) return asim_fail(ctx, ASIM_ERANGE, "too many device buckets");
+    for (const auto& H : splits) {
+      if (!discrepancy_ok(part, H, lat, ctx->model_n, spec->bound_num, spec->bound_den)) continue;
+      BucketCombo cb;
+      cb.partition = pi;
+      cb.H = H;
+      for (size_t b = 0; b < part.size(); ++b) {
+        auto key = std::make_pair(part[b], H[b]);
+        auto it = job_of.find(key);
+        if (it == job_of.end()) {
+          BucketJob job;
+          job.models = part[b];
+          job.H = H[b];
+          std::vector<std::vector<int32_t>> rg;
+          asim_status st = bucket_runs(ctx, H[b], &rg);
+          if (st) return st;
+          std::vector<uint8_t> al(M, 0);
+          for (int32_t m : part[b]) al[m] = 1;
+          for (auto& g : rg) {
+            job.runs.push_back((int32_t)groups->size());
+            groups->push_back(std::move(g));
+            allowed->push_back(al);
+          }
+          if (groups->size() > kMaxRuns) return asim_fail(ctx, ASIM_ERANGE, "more than 2^20 runs");
+          it = job_of.emplace(key, (int32_t)s->jobs.size()).first;
+          s->jobs.push_back(std::move(job));
+        }
+        cb.jobs.push_back(it->second);
+      }
+      s->combos.push_back(std::move(cb));
+    }
+  }
+  s->bucketed = true;
+  return ASIM_OK;
+}
+
 extern "C" {
 
 asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim_search** out) {
@@ -163,47 +397,77 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
   if (!spec) return asim_fail(ctx, ASIM_EINVAL, "null spec");
   const HostProblem& hp = ctx->hp;
   std::vector<std::vector<int32_t>> groups;
-  if (spec->num_runs == 0) {
+  std::vector<std::vector<uint8_t>> allowed;
+  asim_search* s = new (std::nothrow) asim_search();
+  if (!s) return asim_fail(ctx, ASIM_ENOMEM, "host allocation failed");
+  if (spec->buckets) {
+    st = bucket_plan(ctx, spec, s, &groups, &allowed);
+    if (st) {
+      delete s;
+      return st;
+    }
+  } else if (spec->num_runs == 0) {
     // Alg. 2 single bucket: D/size equal groups, one config each (C13)
     for (int32_t size = 1; size <= hp.num_devices; ++size) {
       if (hp.num_devices % size) continue;
       for (int32_t p = 0; p < hp.P; ++p) {
         if (hp.cfg_devices[p] != size) continue;
         const int32_t G = hp.num_devices / size;
-        if (G > ASIM_MAX_GROUPS)
+        if (G > ASIM_MAX_GROUPS) {
+          delete s;
           return asim_fail(ctx, ASIM_ERANGE,
                            "Alg. 2 run with more than ASIM_MAX_GROUPS groups; pass explicit runs");
+        }
         groups.emplace_back(G, p);
       }
     }
   } else {
-    if (spec->num_runs < 0 || !spec->run_num_groups || !spec->run_group_cfg)
+    if (spec->num_runs < 0 || !spec->run_num_groups || !spec->run_group_cfg) {
+      delete s;
       return asim_fail(ctx, ASIM_EINVAL, "bad run list");
+    }
     int64_t off = 0;
     for (int32_t r = 0; r < spec->num_runs; ++r) {
       const int32_t G = spec->run_num_groups[r];
-      if (G < 1 || G > ASIM_MAX_GROUPS) return asim_fail(ctx, ASIM_ERANGE, "run_num_groups");
-      std::vector<int32_t> cfg(spec->run_group_cfg + off, spec->run_group_cfg + off + G);
-      off += G;
-      int32_t slots = 0;
-      for (int32_t c : cfg) {
-        if (c < 0 || c >= hp.P) return asim_fail(ctx, ASIM_ERANGE, "run_group_cfg");
-        slots += hp.cfg_stages[c];
+      asim_status bad = ASIM_OK;
+      const char* why = nullptr;
+      if (G < 1 || G > ASIM_MAX_GROUPS) {
+        bad = ASIM_ERANGE;
+        why = "run_num_groups";
+      } else {
+        std::vector<int32_t> cfg(spec->run_group_cfg + off, spec->run_group_cfg + off + G);
+        off += G;
+        int32_t slots = 0;
+        for (int32_t c : cfg) {
+          if (c < 0 || c >= hp.P) {
+            bad = ASIM_ERANGE;
+            why = "run_group_cfg";
+            break;
+          }
+          slots += hp.cfg_stages[c];
+        }
+        if (!bad && slots > ASIM_MAX_SLOTS) {
+          bad = ASIM_ERANGE;
+          why = "run exceeds ASIM_MAX_SLOTS";
+        }
+        if (!bad) groups.push_back(std::move(cfg));
       }
-      if (slots > ASIM_MAX_SLOTS) return asim_fail(ctx, ASIM_ERANGE, "run exceeds ASIM_MAX_SLOTS");
-      groups.push_back(std::move(cfg));
+      if (bad) {
+        delete s;
+        return asim_fail(ctx, bad, why);
+      }
     }
   }
-  asim_search* s = new (std::nothrow) asim_search();
-  if (!s) return asim_fail(ctx, ASIM_ENOMEM, "host allocation failed");
   s->ctx = ctx;
   s->dedup = spec->dedup != 0;
   s->fast = spec->fast != 0;
   int32_t stride = 1;
-  for (auto& cfg : groups) {
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    auto& cfg = groups[gi];
     Run r;
     r.G = (int32_t)cfg.size();
     r.cfg = cfg;
+    if (!allowed.empty()) r.allowed = std::move(allowed[gi]);
     r.sel.assign(hp.M, 0);
     r.best.assign(hp.M, 0);
     r.used.assign(r.G, 0);
@@ -290,6 +554,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
     run.cands.clear();
     if (s->restrict_k) root_masks(run, M);
     for (int32_t m = 0; m < M; ++m) {
+      if (!run.may_place(m)) continue;  // outside this run's bucket
       std::map<std::pair<int32_t, int32_t>, int64_t> seen;  // (cfg, rank among hosts) -> rep
       for (int32_t g = 0; g < run.G; ++g) {
         if ((run.sel[m] >> g) & 1ULL) continue;  // a model at most once per group (C11)
@@ -621,8 +886,18 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
     out.good = s->d_good_all.as<int64_t>();
     out.good_per_model = s->d_pm.as<int64_t>();
     out.busy = s->d_busy.as<int64_t>();
-    asim_status rc = asim_run_batch(ctx, hb, 0, C, out, st);
+    // warp-cooperative whole-trace kernel (uniform configs), else the general one
+    asim_status rc = asim_upload_batch(ctx, hb, st);
     if (rc) return rc;
+    bool done = false;
+    if (ctx->force_path != 1) {
+      rc = asim_run_fast_stats(ctx, hb, out, st, &done);
+      if (rc) return rc;
+    }
+    if (!done) {
+      rc = asim_run_batch(ctx, hb, 0, C, out, st);
+      if (rc) return rc;
+    }
     good.resize(C);
     pm.resize(C * M);
     busy.resize(C * G);
@@ -649,6 +924,7 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
       int32_t bm = -1, bgp = -1;
       int64_t bu = 0;
       for (int32_t m = 0; m < M; ++m) {
+        if (!run.may_place(m)) continue;  // outside this run's bucket
         const int64_t un = ctx->model_n[m] - pm[b * M + m];
         if (un <= 0 || (bm >= 0 && un <= bu)) continue;
         int32_t gbest = -1;
@@ -699,8 +975,71 @@ asim_status asim_search_run(asim_search* s, void* cuda_stream) {
   }
 }
 
+}  // extern "C"
+
+// Bucketed outcome (reading C28): plm_i* per job = its first best run on
+// strict '>' (none if no run serves a request); combo good = sum over its
+// jobs; the first best combo on strict '>'.
+static void bucket_best(const asim_search* s, int32_t* best_combo, int64_t* best_good,
+                        std::vector<int32_t>* job_run) {
+  job_run->assign(s->jobs.size(), -1);
+  std::vector<int64_t> job_good(s->jobs.size(), 0);
+  for (size_t j = 0; j < s->jobs.size(); ++j)
+    for (int32_t r : s->jobs[j].runs)
+      if (s->runs[r].best_good > job_good[j]) {
+        job_good[j] = s->runs[r].best_good;
+        (*job_run)[j] = r;
+      }
+  *best_combo = -1;
+  *best_good = 0;
+  for (size_t c = 0; c < s->combos.size(); ++c) {
+    int64_t g = 0;
+    for (int32_t j : s->combos[c].jobs) g += job_good[j];
+    if (g > *best_good) {
+      *best_good = g;
+      *best_combo = (int32_t)c;
+    }
+  }
+}
+
+extern "C" {
+
 asim_status asim_search_result_get(const asim_search* s, asim_search_result* out) {
   if (!s || !out) return ASIM_EINVAL;
+  const int32_t M = s->ctx->hp.M;
+  out->steps = s->steps;
+  out->candidates = s->candidates;
+  out->evaluated = s->evaluated;
+  out->request_evals = s->evaluated * s->ctx->n;
+  out->memo_hits = s->memo_hits;
+  if (s->bucketed) {  // the concatenated placement (groups of bucket 1 first)
+    int32_t bc = -1;
+    int64_t bg = 0;
+    std::vector<int32_t> job_run;
+    bucket_best(s, &bc, &bg, &job_run);
+    std::vector<int32_t> cfg;
+    std::vector<uint64_t> mask(M, 0);
+    if (bc >= 0)
+      for (int32_t j : s->combos[bc].jobs) {
+        const int32_t r = job_run[j];
+        if (r < 0) continue;
+        const Run& run = s->runs[r];
+        const int32_t off = (int32_t)cfg.size();
+        for (int32_t m = 0; m < M; ++m)
+          if (off < 64) mask[m] |= run.best[m] << off;
+        cfg.insert(cfg.end(), run.cfg.begin(), run.cfg.end());
+      }
+    const bool fits = (int32_t)cfg.size() <= ASIM_MAX_GROUPS;
+    out->best_run = -1;
+    out->best_good = bg;
+    out->num_groups = (int32_t)cfg.size();
+    if (out->group_cfg)
+      for (int32_t g = 0; g < ASIM_MAX_GROUPS; ++g)
+        out->group_cfg[g] = (fits && g < (int32_t)cfg.size()) ? cfg[g] : -1;
+    if (out->host_mask)
+      for (int32_t m = 0; m < M; ++m) out->host_mask[m] = fits ? mask[m] : 0;
+    return ASIM_OK;
+  }
   int32_t best = -1;
   int64_t best_good = 0;
   for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r)
@@ -716,13 +1055,32 @@ asim_status asim_search_result_get(const asim_search* s, asim_search_result* out
       out->group_cfg[g] = (best >= 0 && g < s->runs[best].G) ? s->runs[best].cfg[g] : -1;
   }
   if (out->host_mask)
-    for (int32_t m = 0; m < s->ctx->hp.M; ++m)
-      out->host_mask[m] = best >= 0 ? s->runs[best].best[m] : 0;
-  out->steps = s->steps;
-  out->candidates = s->candidates;
-  out->evaluated = s->evaluated;
-  out->request_evals = s->evaluated * s->ctx->n;
-  out->memo_hits = s->memo_hits;
+    for (int32_t m = 0; m < M; ++m) out->host_mask[m] = best >= 0 ? s->runs[best].best[m] : 0;
+  return ASIM_OK;
+}
+
+asim_status asim_search_buckets_get(const asim_search* s, asim_bucket_result* out) {
+  if (!s || !out) return ASIM_EINVAL;
+  if (!s->bucketed) return asim_fail(s->ctx, ASIM_ESTATE, "not a bucketed search");
+  if (!s->finished) return asim_fail(s->ctx, ASIM_ESTATE, "search not finished");
+  const int32_t M = s->ctx->hp.M;
+  int32_t bc = -1;
+  int64_t bg = 0;
+  std::vector<int32_t> job_run;
+  bucket_best(s, &bc, &bg, &job_run);
+  out->best_good = bg;
+  out->partitions = (int64_t)s->partitions.size();
+  out->considered = (int64_t)s->combos.size();
+  out->num_buckets = bc >= 0 ? (int32_t)s->combos[bc].jobs.size() : 0;
+  if (out->bucket_of_model)
+    for (int32_t m = 0; m < M; ++m) out->bucket_of_model[m] = -1;
+  for (int32_t i = 0; i < out->num_buckets; ++i) {
+    const int32_t j = s->combos[bc].jobs[i];
+    if (out->bucket_of_model)
+      for (int32_t m : s->jobs[j].models) out->bucket_of_model[m] = i;
+    if (out->bucket_devices) out->bucket_devices[i] = s->combos[bc].H[i];
+    if (out->bucket_run) out->bucket_run[i] = job_run[j];
+  }
   return ASIM_OK;
 }
 

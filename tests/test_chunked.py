@@ -180,3 +180,46 @@ def test_epoch_rebase_long_gaps(sim, scale):
     bases = [Placement.from_lists([0, 0], [[0], [1]], 2), Placement.from_lists([2], [[0]], 2),
              Placement.from_lists([1], [[1]], 2)]
     _check(sim, prob, tr, bases, rng, chunk_sizes=(37, 4096), per_base=12)
+
+
+def test_uniform_config_with_empty_group_slot(sim):
+    """A base whose groups share one config but with an unused group id
+    (cfg -1) in between: the uniform kernels address stages at g * S, so such
+    a base must take the group-table path -- results stay oracle-exact."""
+    rng = np.random.default_rng(79)
+    M = 4
+    prob = tiny_problem([(2, 1)], [[list(rng.integers(1, 40, size=2))] for _ in range(M)],
+                        slo=[int(rng.integers(60, 300)) for _ in range(M)])
+    tr = _bursty_trace(rng, M, 3000, 12.0)
+    cfg = np.array([0, -1, 0, 0], np.int32)
+    mask = np.zeros(M, np.uint64)
+    for m in range(M):
+        for g in (0, 2, 3):
+            if rng.random() < 0.5:
+                mask[m] |= np.uint64(1) << np.uint64(g)
+    cb, cm, cg = [], [], []
+    for m in range(-1, M):
+        for g in (0, 2, 3):
+            if m >= 0 and (int(mask[m]) >> g) & 1:
+                continue
+            cb.append(0), cm.append(m), cg.append(g)
+    cb, cm, cg = (np.array(x, np.int32) for x in (cb, cm, cg))
+    fcfg = np.tile(cfg, (len(cb), 1))
+    fmask = np.tile(mask, (len(cb), 1))
+    for c in range(len(cb)):
+        if cm[c] >= 0:
+            fmask[c, cm[c]] |= np.uint64(1) << np.uint64(cg[c])
+    want_g, want_s, _ = oracle.evaluate(prob, tr, fcfg, fmask)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    for path in (0, 2):
+        sim.set_path(path)
+        try:
+            for L in (64, 4096):
+                sim.set_chunk_size(L)
+                got = sim.evaluate_deltas(cfg[None, :], mask[None, :], cb, cm, cg)
+                np.testing.assert_array_equal(got["good"], want_g)
+                np.testing.assert_array_equal(got["sum_latency_ns"], want_s)
+        finally:
+            sim.set_path(0)
+            sim.set_chunk_size(4096)

@@ -343,8 +343,8 @@ def main():
             gpu_launches=int(launches),
             roofline=dict(bound="alu", achieved=achieved, peak=peak,
                           unit="G stage-updates/s", frac=achieved / peak, traffic=traffic,
-                          traffic_unit="GB DRAM per launch of walk_kernel (ncu, profiles/traffic.json)",
-                          kernel="chunked simulation (chunk_kernel passes 1-2 + walk_kernel)",
+                          traffic_unit="GB DRAM per launch of coop_walk_kernel (ncu, profiles/traffic.json)",
+                          kernel="chunked simulation (chunk_kernel passes 1-2 + coop_walk_kernel)",
                           kernel_ms_share=st["sim_ms"] / max(total_ms, 1e-9),
                           stage_updates=st["stage_updates"], sim_launches=st["sim_launches"],
                           peak_basis=f"{sms} SMs x 64 int max/clk x {sm_max:.0f} MHz "

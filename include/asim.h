@@ -280,7 +280,17 @@ double asim_attainment(int64_t good, int64_t n);
  * read with asim_search_buckets_get; asim_search_result_get reports the
  * concatenated placement (best_run = -1) when it has <= ASIM_MAX_GROUPS
  * groups, else num_groups only.
+ *
+ * Beam search (spec->beam = k > 1; Alg. 1's beam_sels; readings
+ * C29-C30): every run keeps up to k member selections; a step lists the
+ * feasible additions of every member (members in beam order, then m, g); a
+ * selection reached from two members counts once (its first occurrence); the
+ * next members are the top-k by good (stable: ties keep list order); sel* =
+ * the first of them and the run's best updates on strict '>'; the run stops
+ * when no member has a feasible addition.  k = 1 is the search above.  Runs
+ * (asim_search_num_runs / run_info) are Alg. 2 runs, not beam members.
  * Errors (asim_search_create): ASIM_EINVAL null latency / bad ratio or bound;
+ * fast = 1 with beam > 1;
  * ASIM_ERANGE latency outside [1, 2^60], a run with > ASIM_MAX_GROUPS groups,
  * or more than 2^20 runs in total. */
 typedef struct {
@@ -296,6 +306,7 @@ typedef struct {
   int64_t ratio_num, ratio_den;  /* bucket latency threshold (SPEC: 4 / 1) */
   int64_t bound_num, bound_den;  /* discrepancy bound (SPEC: 3 / 1) */
   const int64_t* model_latency_ns; /* [M] host; single-device latency (Table 1) */
+  int32_t beam;                  /* Alg. 1 beam size k (<= 1 means 1; see below) */
 } asim_search_spec;
 
 typedef struct {

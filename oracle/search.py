@@ -92,6 +92,62 @@ def greedy(prob, trace, group_cfg, threads: int = 0, record: bool = False, model
     return dict(placement=Placement(cfg, best_sel), good=best_good, steps=steps)
 
 
+def greedy_beam(prob, trace, group_cfg, k: int, threads: int = 0, models=None):
+    """Alg. 1 with beam size k (readings C29-C30): every member of
+    beam_sels is extended by every feasible (m, g) in (member, m, g) order;
+    selections reached twice keep their first occurrence; beam_sels =
+    top-k by good (stable: ties keep new_sels order); sel* = the first of them;
+    best_sel on strict '>'.  k = 1 is `greedy`."""
+    op = prob if isinstance(prob, OracleProblem) else OracleProblem(prob)
+    ot = trace if isinstance(trace, OracleTrace) else OracleTrace(trace)
+    M = op.prob.num_models
+    cfg = np.asarray(group_cfg, dtype=np.int32)
+    G = len(cfg)
+    allowed = range(M) if models is None else sorted(models)
+    beam = [np.zeros(M, dtype=np.uint64)]
+    best_sel, best_good = beam[0].copy(), 0
+    steps = 0
+    while True:
+        new_sels, seen = [], set()
+        for sel in beam:
+            for m in allowed:
+                for g in range(G):
+                    if (int(sel[m]) >> g) & 1:
+                        continue
+                    nm = _add(sel, m, g)
+                    key = nm.tobytes()
+                    if key in seen:
+                        continue  # the same selection reached from another member
+                    if feasible(op, Placement(cfg, nm)):
+                        seen.add(key)
+                        new_sels.append(nm)
+        if not new_sels:
+            break
+        goods, _, _ = evaluate(op, ot, np.tile(cfg, (len(new_sels), 1)), np.stack(new_sels),
+                               threads)
+        order = sorted(range(len(new_sels)), key=lambda i: -int(goods[i]))  # stable
+        beam = [new_sels[i] for i in order[:k]]
+        steps += 1
+        if int(goods[order[0]]) > best_good:  # sel* = pick_highest(beam_sels)
+            best_sel, best_good = beam[0].copy(), int(goods[order[0]])
+    return dict(placement=Placement(cfg, best_sel), good=best_good, steps=steps)
+
+
+def alg2_beam(prob, trace, k: int, threads: int = 0):
+    """Alg. 2 (single bucket) around Alg. 1 with beam size k."""
+    op, ot = OracleProblem(prob), OracleTrace(trace)
+    best = dict(placement=Placement(np.zeros(0, np.int32), np.zeros(prob.num_models, np.uint64)),
+                good=0, run=-1)
+    runs = []
+    for r, (size, p, cfg) in enumerate(alg2_runs(prob)):
+        res = greedy_beam(op, ot, cfg, k, threads)
+        runs.append(res)
+        if res["good"] > best["good"]:
+            best = dict(res, run=r)
+    best["runs"] = runs
+    return best
+
+
 def utilization_busy(prob, model, group_cfg, served_by):
     """Per group g: sum over the requests it served of sum_k stage_ns[m][cfg_g][k]
     (the numerator of its mean stage utilization, reading C23)."""

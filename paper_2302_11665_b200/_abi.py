@@ -55,7 +55,7 @@ class asim_search_spec(ctypes.Structure):
     _fields_ = [("num_runs", i32), ("run_num_groups", vp), ("run_group_cfg", vp),
                 ("dedup", i32), ("fast", i32), ("buckets", i32), ("max_buckets", i32),
                 ("ratio_num", i64), ("ratio_den", i64), ("bound_num", i64), ("bound_den", i64),
-                ("model_latency_ns", vp)]
+                ("model_latency_ns", vp), ("beam", i32)]
 
 
 class asim_bucket_result(ctypes.Structure):

@@ -200,11 +200,12 @@ class Simulator:
                     argmax=int(am[0]) if argmax else None, busy_ns=bz)
 
     # ------------------------------------------------------------- search
-    def search_handle(self, runs=None, dedup=True, fast=False, buckets=None) -> "SearchHandle":
-        return SearchHandle(self, runs, dedup, fast, buckets)
+    def search_handle(self, runs=None, dedup=True, fast=False, buckets=None,
+                      beam=1) -> "SearchHandle":
+        return SearchHandle(self, runs, dedup, fast, buckets, beam)
 
     def search_buckets(self, latency, ratio=4, bound=3, max_buckets=0, fast=False, dedup=True,
-                       pg=None, stream=None) -> BucketResult:
+                       pg=None, stream=None, beam=1) -> BucketResult:
         """Alg. 2 with model and device buckets (include/asim.h).
         latency[m]: single-device latency in ns; ratio / bound: ints or
         fractions.Fraction (threshold 4x and discrepancy bound 3x by default)."""
@@ -214,7 +215,7 @@ class Simulator:
 
         b = dict(latency=_host(latency, np.int64), ratio=Fraction(ratio), bound=Fraction(bound),
                  max_buckets=int(max_buckets))
-        with self.search_handle(None, dedup, fast, b) as sh:
+        with self.search_handle(None, dedup, fast, b, beam) as sh:
             if fast:
                 sh.run(stream=stream)
             else:
@@ -232,7 +233,8 @@ class Simulator:
                                 [int(x) for x in br[:k]], res.group_cfg, res.host_mask,
                                 r.partitions, r.considered, res)
 
-    def search(self, runs=None, dedup=True, pg=None, stream=None, fast=False) -> SearchResult:
+    def search(self, runs=None, dedup=True, pg=None, stream=None, fast=False,
+               beam=1) -> SearchResult:
         """Full Alg. 2 (single bucket) / Alg. 1 search.  With a
         torch.distributed process group the step candidates shard across its
         ranks (dist.run_search).  fast=True runs the fast heuristic of P:737
@@ -240,7 +242,7 @@ class Simulator:
         computes it whole -- there is nothing to shard)."""
         from . import dist
 
-        with self.search_handle(runs, dedup, fast) as sh:
+        with self.search_handle(runs, dedup, fast, None, beam) as sh:
             if fast:
                 sh.run(stream=stream)
             else:
@@ -251,23 +253,28 @@ class Simulator:
 class SearchHandle:
     """Stepwise search protocol of include/asim.h (prepare / evaluate / apply)."""
 
-    def __init__(self, sim: Simulator, runs=None, dedup=True, fast=False, buckets=None):
+    def __init__(self, sim: Simulator, runs=None, dedup=True, fast=False, buckets=None,
+                 beam=1):
         self.sim = sim
+        spec = A.asim_search_spec()
+        spec.dedup = int(bool(dedup))
+        spec.fast = int(bool(fast))
+        spec.beam = int(beam)
+        self._keep = ()
         if buckets is not None:
             lat = buckets["latency"]
-            spec = A.asim_search_spec(0, None, None, int(bool(dedup)), int(bool(fast)), 1,
-                                      buckets["max_buckets"], buckets["ratio"].numerator,
-                                      buckets["ratio"].denominator, buckets["bound"].numerator,
-                                      buckets["bound"].denominator, _ptr(lat))
+            spec.buckets = 1
+            spec.max_buckets = buckets["max_buckets"]
+            spec.ratio_num, spec.ratio_den = buckets["ratio"].numerator, buckets["ratio"].denominator
+            spec.bound_num, spec.bound_den = buckets["bound"].numerator, buckets["bound"].denominator
+            spec.model_latency_ns = _ptr(lat)
             self._keep = (lat,)
-        elif runs is None:
-            spec = A.asim_search_spec(0, None, None, int(bool(dedup)), int(bool(fast)))
-            self._keep = ()
-        else:
+        elif runs is not None:
             ng = np.array([len(r) for r in runs], np.int32)
             cfg = np.concatenate([np.asarray(r, np.int32) for r in runs]).astype(np.int32)
-            spec = A.asim_search_spec(len(runs), _ptr(ng), _ptr(cfg), int(bool(dedup)),
-                                      int(bool(fast)))
+            spec.num_runs = len(runs)
+            spec.run_num_groups = _ptr(ng)
+            spec.run_group_cfg = _ptr(cfg)
             self._keep = (ng, cfg)
         h = ctypes.c_void_p()
         sim._check(A.asim_search_create(sim.h, ctypes.byref(spec), ctypes.byref(h)))

@@ -1049,7 +1049,8 @@ __device__ __forceinline__ void fast_candidate(const ChunkParams& P, const WarpM
   int64_t E = (TT<T>::kRel && P.tr.n > 0) ? P.tr.arrival[0] : 0;
   int64_t good = 0, sum = 0;
   int64_t busy[2] = {0, 0};
-  coop_range<T, S, Q, true>(P, w, 0, P.tr.n, v, E, ~0ull, my_m, my_bit, lastbit, lane, good, sum,
+  const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;  // component restriction
+  coop_range<T, S, Q, true>(P, w, 0, P.tr.n, v, E, kmask, my_m, my_bit, lastbit, lane, good, sum,
                             upd, cnt, busy);
   __syncwarp();
   const int64_t o = c - out.out_offset;

@@ -87,6 +87,7 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   P.bt.cand_model = ctx->d_cand_model.as<int32_t>();
   P.bt.cand_group = ctx->d_cand_group.as<int32_t>();
   P.bt.cand_ok = ctx->d_cand_ok.as<uint8_t>();
+  P.bt.cand_kmask = hb.cand_kmask.empty() ? nullptr : ctx->d_cand_kmask.as<uint64_t>();
   P.bt.C = C;
   P.items = ctx->c_items.as<asim::ItemDesc>();
   P.num_items = (int32_t)items.size();

@@ -52,6 +52,7 @@
 #include <algorithm>
 #include <functional>
 #include <map>
+#include <set>
 #include <new>
 #include <string>
 #include <vector>
@@ -98,6 +99,10 @@ struct Run {
     return x;
   }
   bool may_place(int32_t m) const { return allowed.empty() || allowed[m]; }
+  // fast heuristic: per-model good / per-group busy of `sel`, and the root of
+  // the component changed by the last addition (-1: up to date)
+  std::vector<int64_t> fpm, fbusy;
+  int32_t pending = -1;
 };
 
 // Alg. 2 with buckets: one job per distinct (model bucket, H)
@@ -182,6 +187,11 @@ struct asim_search {
   // fast heuristic: per-model good and per-group busy of each base
   bool fast = false;
   DBuf d_pm, d_busy;
+  // beam search (Alg. 1 with k > 1): run group gi owns slots [gi*beam, gi*beam+beam)
+  int32_t beam = 1;
+  int32_t ngroups = 0;
+  std::vector<std::vector<uint64_t>> gbest;  // [ngroups][M] best selection (beam > 1)
+  std::vector<int64_t> gbest_good, gsteps;
   // Alg. 2 with buckets
   bool bucketed = false;
   std::vector<std::vector<std::vector<int32_t>>> partitions;
@@ -461,13 +471,33 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
   s->ctx = ctx;
   s->dedup = spec->dedup != 0;
   s->fast = spec->fast != 0;
+  s->beam = spec->beam > 1 ? spec->beam : 1;
+  if (s->fast && s->beam > 1) {
+    delete s;
+    return asim_fail(ctx, ASIM_EINVAL, "the fast heuristic has no beam");
+  }
+  if (s->beam > 4096) {
+    delete s;
+    return asim_fail(ctx, ASIM_ERANGE, "beam > 4096");
+  }
   int32_t stride = 1;
-  for (size_t gi = 0; gi < groups.size(); ++gi) {
+  s->ngroups = (int32_t)groups.size();
+  if (groups.size() * (size_t)s->beam > kMaxRuns) {
+    delete s;
+    return asim_fail(ctx, ASIM_ERANGE, "runs x beam > 2^20");
+  }
+  if (s->beam > 1) {
+    s->gbest.assign(groups.size(), std::vector<uint64_t>(hp.M, 0));
+    s->gbest_good.assign(groups.size(), 0);
+    s->gsteps.assign(groups.size(), 0);
+  }
+  for (size_t slot = 0; slot < groups.size() * (size_t)s->beam; ++slot) {
+    const size_t gi = slot / s->beam;
     auto& cfg = groups[gi];
     Run r;
     r.G = (int32_t)cfg.size();
     r.cfg = cfg;
-    if (!allowed.empty()) r.allowed = std::move(allowed[gi]);
+    if (!allowed.empty()) r.allowed = allowed[gi];
     r.sel.assign(hp.M, 0);
     r.best.assign(hp.M, 0);
     r.used.assign(r.G, 0);
@@ -486,6 +516,7 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     }
     stride = std::max(stride, slots);
     if (devices > hp.num_devices) r.active = false;  // the empty placement is already infeasible
+    if (slot % s->beam) r.active = false;  // beam_sels = {{}}: one member to start
     s->G = std::max(s->G, r.G);
     s->runs.push_back(std::move(r));
   }
@@ -525,7 +556,7 @@ void asim_search_destroy(asim_search* s) {
   delete s;
 }
 
-int32_t asim_search_num_runs(const asim_search* s) { return s ? (int32_t)s->runs.size() : 0; }
+int32_t asim_search_num_runs(const asim_search* s) { return s ? s->ngroups : 0; }
 
 asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   if (!s || !num_candidates) return ASIM_EINVAL;
@@ -681,23 +712,28 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
 // simulated are published from their lanes; the others are simulated again,
 // one lane each, restricted to their own component.
 static asim_status update_states(asim_search* s, const std::vector<int32_t>& winner_run,
-                                 const std::vector<const Run::Cand*>& winner, cudaStream_t st) {
+                                 const std::vector<const Run::Cand*>& winner, cudaStream_t st,
+                                 const std::vector<int32_t>* target_rows = nullptr) {
+  // winner_run[i]: the run (old base) the winner extends; target_rows[i]: the
+  // st_next row receiving the new base (default: the same run)
   asim_ctx* ctx = s->ctx;
   std::vector<int64_t> pub_c;
   std::vector<int32_t> pub_r;
   HostBatch hb;
   hb.G = s->G;
-  std::vector<int32_t> rows;
+  std::vector<int32_t> rows, out_rows;
   for (size_t i = 0; i < winner_run.size(); ++i) {
     const Run::Cand& w = *winner[i];
+    const int32_t target = target_rows ? (*target_rows)[i] : winner_run[i];
     if (w.kind == 0 && w.ref >= s->eval_lo && w.ref < s->eval_hi) {
       pub_c.push_back(w.ref);
-      pub_r.push_back(winner_run[i]);
+      pub_r.push_back(target);
       continue;
     }
     Run& run = s->runs[winner_run[i]];  // still the old base here
     const int32_t b = (int32_t)rows.size();
     rows.push_back(winner_run[i]);
+    out_rows.push_back(target);
     for (int32_t g = 0; g < s->G; ++g) hb.base_cfg.push_back(g < run.G ? run.cfg[g] : -1);
     hb.base_mask.insert(hb.base_mask.end(), run.sel.begin(), run.sel.end());
     int32_t slots = 0;
@@ -733,12 +769,114 @@ static asim_status update_states(asim_search* s, const std::vector<int32_t>& win
     if (rc) return rc;
     std::vector<int64_t> all(rows.size());
     for (size_t i = 0; i < rows.size(); ++i) all[i] = (int64_t)i;
-    rc = asim_publish_candidates(ctx, all, rows, s->st_next.as<int64_t>(), st);
+    rc = asim_publish_candidates(ctx, all, out_rows, s->st_next.as<int64_t>(), st);
     if (rc) return rc;
   }
   std::swap(s->st_base, s->st_next);
   return ASIM_OK;
 }
+
+}  // extern "C"
+
+// sel <- sel + (m, g) on a run whose candidates are this step's (memo for
+// the next step, merged component, selection, memory, base good).
+static void apply_winner(Run& run, const Run::Cand w, const HostProblem& hp) {
+  // memo for the next step: candidates whose component avoids the winner's
+  const int64_t shift = w.good - run.base_good;
+  std::fill(run.memo_ok.begin(), run.memo_ok.end(), 0);
+  for (const Run::Cand& c : run.cands)
+    if (c.r1 != w.r1 && c.r1 != w.r2 && c.r2 != w.r1 && c.r2 != w.r2) {
+      const size_t mi = (size_t)c.m * run.G + c.g;
+      run.memo_ok[mi] = 1;
+      run.memo_good[mi] = c.good + shift;
+    }
+  // the merged component's good, from the winner's total alone
+  const int64_t merged =
+      w.good - run.base_good + run.cgood[w.r1] + (w.r2 != w.r1 ? run.cgood[w.r2] : 0);
+  run.parent[w.r1] = w.r2;  // unite comp(g*) and comp(m*)
+  run.cgood[w.r2] = merged;
+  run.sel[w.m] |= 1ULL << w.g;
+  run.used[w.g] += hp.mem_at(w.m, run.cfg[w.g]);
+  run.base_good = w.good;
+  run.history.emplace_back(w.m, w.g);
+  ++run.steps;
+}
+
+// Alg. 1 with beam k > 1 (readings C29-C30): per run group, the
+// candidates of all members in (member, m, g) order, a selection reached
+// twice kept once (first occurrence), stable top-k by good; member i of the
+// next step = its parent member + its addition; sel* = the first; best_sel
+// on strict '>'.  Candidate memory (mixed speculation) is not used here.
+static asim_status apply_beam(asim_search* s, cudaStream_t st) {
+  const HostProblem& hp = s->ctx->hp;
+  const int32_t K = s->beam;
+  struct Pick {
+    int32_t slot, ci;
+    int64_t good;
+  };
+  std::vector<std::pair<int32_t, std::vector<Pick>>> plan;
+  for (size_t b = 0; b < s->base_run.size();) {
+    const int32_t gi = s->base_run[b] / K;
+    std::vector<Pick> all;
+    std::set<std::vector<uint64_t>> seen;
+    for (; b < s->base_run.size() && s->base_run[b] / K == gi; ++b) {
+      const int32_t slot = s->base_run[b];
+      const Run& run = s->runs[slot];
+      for (size_t i = 0; i < run.cands.size(); ++i) {
+        const Run::Cand& c = run.cands[i];
+        std::vector<uint64_t> key = run.sel;
+        key[c.m] |= 1ULL << c.g;
+        if (!seen.insert(std::move(key)).second) continue;  // reached from an earlier member
+        all.push_back(Pick{slot, (int32_t)i, c.good});
+      }
+    }
+    std::stable_sort(all.begin(), all.end(),
+                     [](const Pick& a, const Pick& b) { return a.good > b.good; });
+    if ((int32_t)all.size() > K) all.resize(K);
+    plan.emplace_back(gi, std::move(all));
+  }
+  if (s->use_states) {
+    std::vector<int32_t> parents, targets;
+    std::vector<const Run::Cand*> cands;
+    for (const auto& gp : plan)
+      for (size_t i = 0; i < gp.second.size(); ++i) {
+        const Pick& pk = gp.second[i];
+        parents.push_back(pk.slot);
+        targets.push_back(gp.first * K + (int32_t)i);
+        cands.push_back(&s->runs[pk.slot].cands[pk.ci]);
+      }
+    s->have_prev = false;
+    asim_status rc = update_states(s, parents, cands, st, &targets);
+    if (rc) return rc;
+  }
+  for (const auto& gp : plan) {
+    const int32_t gi = gp.first;
+    std::map<int32_t, Run> snap;  // parents before any child overwrites a slot
+    for (const Pick& pk : gp.second) snap.emplace(pk.slot, s->runs[pk.slot]);
+    for (int32_t i = 0; i < K; ++i) {
+      Run& dst = s->runs[gi * K + i];
+      if (i >= (int32_t)gp.second.size()) {
+        dst.active = false;
+        continue;
+      }
+      const Pick& pk = gp.second[i];
+      Run child = snap.at(pk.slot);
+      const Run::Cand w = child.cands[pk.ci];
+      apply_winner(child, w, hp);
+      child.active = true;
+      dst = std::move(child);
+    }
+    ++s->gsteps[gi];
+    if (gp.second[0].good > s->gbest_good[gi]) {  // sel* = pick_highest(beam_sels)
+      s->gbest_good[gi] = gp.second[0].good;
+      s->gbest[gi] = s->runs[gi * K].sel;
+    }
+  }
+  s->prepared = false;
+  return ASIM_OK;
+}
+
+extern "C" {
 
 asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void* cuda_stream) {
   if (!s) return ASIM_EINVAL;
@@ -755,12 +893,9 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
   }
   const HostProblem& hp = s->ctx->hp;
   const bool restricted = !s->hb.cand_kmask.empty();
-  std::vector<int32_t> winner_run;
-  std::vector<const Run::Cand*> winner;
   for (size_t b = 0; b < s->base_run.size(); ++b) {
     Run& run = s->runs[s->base_run[b]];
     // every candidate's good: simulated, memo, or its duplicate's representative
-    int64_t bi = -1, bg = -1;
     for (size_t i = 0; i < run.cands.size(); ++i) {
       Run::Cand& c = run.cands[i];
       if (c.kind == 0) {
@@ -770,6 +905,16 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
       } else if (c.kind == 2) {
         c.good = run.cands[c.ref].good;
       }
+    }
+  }
+  if (s->beam > 1) return apply_beam(s, st);
+  std::vector<int32_t> winner_run;
+  std::vector<const Run::Cand*> winner;
+  for (size_t b = 0; b < s->base_run.size(); ++b) {
+    Run& run = s->runs[s->base_run[b]];
+    int64_t bi = -1, bg = -1;
+    for (size_t i = 0; i < run.cands.size(); ++i) {
+      const Run::Cand& c = run.cands[i];
       if (c.good > bg) {  // first maximum in (m, g) order: lowest index on ties (C12)
         bg = c.good;
         bi = (int64_t)i;
@@ -813,25 +958,7 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
   for (size_t i = 0; i < winner_run.size(); ++i) {
     Run& run = s->runs[winner_run[i]];
     const Run::Cand w = *winner[i];
-    // memo for the next step: candidates whose component avoids the winner's
-    const int64_t shift = w.good - run.base_good;
-    std::fill(run.memo_ok.begin(), run.memo_ok.end(), 0);
-    for (const Run::Cand& c : run.cands)
-      if (c.r1 != w.r1 && c.r1 != w.r2 && c.r2 != w.r1 && c.r2 != w.r2) {
-        const size_t mi = (size_t)c.m * run.G + c.g;
-        run.memo_ok[mi] = 1;
-        run.memo_good[mi] = c.good + shift;
-      }
-    // the merged component's good, from the winner's total alone
-    const int64_t merged =
-        w.good - run.base_good + run.cgood[w.r1] + (w.r2 != w.r1 ? run.cgood[w.r2] : 0);
-    run.parent[w.r1] = w.r2;  // unite comp(g*) and comp(m*)
-    run.cgood[w.r2] = merged;
-    run.sel[w.m] |= 1ULL << w.g;
-    run.used[w.g] += hp.mem_at(w.m, run.cfg[w.g]);
-    run.base_good = w.good;
-    run.history.emplace_back(w.m, w.g);
-    ++run.steps;
+    apply_winner(run, w, hp);
     if (w.good > run.best_good) {  // "if sel*.slo_att > best_sel.slo_att"
       run.best_good = w.good;
       run.best = run.sel;
@@ -846,27 +973,50 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
 // The fast heuristic (readings C22-C24): one simulation of every active
 // run's current selection per step, then a host decision per run.
 static asim_status run_fast(asim_search* s, cudaStream_t st) {
+  // Per run: per-model good (fpm) and per-group busy (fbusy) of the current
+  // selection.  They only change inside the connected component of the
+  // (group, model) hosting graph that the last addition merged, so each step
+  // simulates that component alone (its models' requests; exact, as in the
+  // greedy driver's component restriction) and keeps the other values.  The
+  // empty selection serves nothing: the first decision needs no simulation.
   asim_ctx* ctx = s->ctx;
   const HostProblem& hp = ctx->hp;
   const int32_t M = hp.M, G = s->G;
+  const bool restrict_ok = M <= 64;
   std::vector<int64_t> good, pm, busy;
+  for (auto& run : s->runs) {
+    run.fpm.assign(M, 0);
+    run.fbusy.assign(run.G, 0);
+    run.pending = -1;
+  }
   for (;;) {
     asim_status rs = asim_ready(ctx);
     if (rs) return rs;
     HostBatch hb;
     hb.G = G;
-    std::vector<int32_t> act;
+    std::vector<int32_t> act, sim_b;
     for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r) {
       Run& run = s->runs[r];
       if (!run.active) continue;
-      const int32_t b = (int32_t)act.size();
       act.push_back(r);
+      if (run.pending < 0) continue;  // nothing changed since its last simulation
+      const int32_t b = (int32_t)sim_b.size();
+      sim_b.push_back(r);
       for (int32_t g = 0; g < G; ++g) hb.base_cfg.push_back(g < run.G ? run.cfg[g] : -1);
       hb.base_mask.insert(hb.base_mask.end(), run.sel.begin(), run.sel.end());
       hb.cand_base.push_back(b);
       hb.cand_model.push_back(-1);  // the selection itself
       hb.cand_group.push_back(0);
       hb.cand_ok.push_back(1);
+      if (restrict_ok) {
+        uint64_t km = 0, gm = 0;
+        for (int32_t x = 0; x < run.G; ++x)
+          if (run.find(x) == run.pending) gm |= 1ULL << x;
+        for (int32_t x = 0; x < M; ++x)
+          if (run.find(run.G + x) == run.pending) km |= 1ULL << x;
+        hb.cand_kmask.push_back(km);
+        hb.cand_gmask.push_back(gm);
+      }
       int32_t slots = 0;
       for (int32_t c : run.cfg) slots += hp.cfg_stages[c];
       hb.slots = std::max(hb.slots, slots);
@@ -875,47 +1025,60 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
       s->finished = true;
       return ASIM_OK;
     }
-    const int64_t C = (int64_t)act.size();
-    cudaError_t e = s->d_good_all.ensure(C * 8 + 8);
-    if (e == cudaSuccess) e = s->d_pm.ensure(C * M * 8 + 8);
-    if (e == cudaSuccess) e = s->d_busy.ensure(C * G * 8 + 8);
-    if (e == cudaSuccess) e = cudaMemsetAsync(s->d_pm.p, 0, C * M * 8, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(s->d_busy.p, 0, C * G * 8, st);
-    if (e != cudaSuccess) return asim_cuda(ctx, e, "fast heuristic buffers");
-    asim::DevOut out{};
-    out.good = s->d_good_all.as<int64_t>();
-    out.good_per_model = s->d_pm.as<int64_t>();
-    out.busy = s->d_busy.as<int64_t>();
-    // warp-cooperative whole-trace kernel (uniform configs), else the general one
-    asim_status rc = asim_upload_batch(ctx, hb, st);
-    if (rc) return rc;
-    bool done = false;
-    if (ctx->force_path != 1) {
-      rc = asim_run_fast_stats(ctx, hb, out, st, &done);
+    const int64_t C = (int64_t)sim_b.size();
+    if (C > 0) {
+      cudaError_t e = s->d_good_all.ensure(C * 8 + 8);
+      if (e == cudaSuccess) e = s->d_pm.ensure(C * M * 8 + 8);
+      if (e == cudaSuccess) e = s->d_busy.ensure(C * G * 8 + 8);
+      if (e == cudaSuccess) e = cudaMemsetAsync(s->d_pm.p, 0, C * M * 8, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(s->d_busy.p, 0, C * G * 8, st);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "fast heuristic buffers");
+      asim::DevOut out{};
+      out.good = s->d_good_all.as<int64_t>();
+      out.good_per_model = s->d_pm.as<int64_t>();
+      out.busy = s->d_busy.as<int64_t>();
+      // warp-cooperative whole-trace kernel (uniform configs, component
+      // restricted), else the general kernel over every model
+      asim_status rc = asim_upload_batch(ctx, hb, st);
       if (rc) return rc;
+      bool done = false;
+      if (ctx->force_path != 1) {
+        rc = asim_run_fast_stats(ctx, hb, out, st, &done);
+        if (rc) return rc;
+      }
+      if (!done) {
+        hb.cand_kmask.clear();
+        hb.cand_gmask.clear();
+        rc = asim_run_batch(ctx, hb, 0, C, out, st);
+        if (rc) return rc;
+      }
+      pm.resize(C * M);
+      busy.resize(C * G);
+      e = cudaMemcpyAsync(pm.data(), out.good_per_model, C * M * 8, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(busy.data(), out.busy, C * G * 8, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "copy fast heuristic results");
+      for (int64_t b = 0; b < C; ++b) {
+        Run& run = s->runs[sim_b[b]];
+        const bool part = done && restrict_ok;
+        for (int32_t m = 0; m < M; ++m)
+          if (!part || ((hb.cand_kmask[b] >> m) & 1ULL)) run.fpm[m] = pm[b * M + m];
+        for (int32_t g = 0; g < run.G; ++g)
+          if (!part || ((hb.cand_gmask[b] >> g) & 1ULL)) run.fbusy[g] = busy[b * G + g];
+        run.pending = -1;
+      }
     }
-    if (!done) {
-      rc = asim_run_batch(ctx, hb, 0, C, out, st);
-      if (rc) return rc;
-    }
-    good.resize(C);
-    pm.resize(C * M);
-    busy.resize(C * G);
-    e = cudaMemcpyAsync(good.data(), out.good, C * 8, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(pm.data(), out.good_per_model, C * M * 8,
-                                              cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(busy.data(), out.busy, C * G * 8, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return asim_cuda(ctx, e, "copy fast heuristic results");
     ++s->steps;
-    s->candidates += C;
+    s->candidates += (int64_t)act.size();
     s->evaluated += C;
-    for (int64_t b = 0; b < C; ++b) {
-      Run& run = s->runs[act[b]];
-      run.base_good = good[b];
-      if (good[b] > run.best_good) {  // best selection so far, strict '>' (C24)
-        run.best_good = good[b];
+    for (int32_t r : act) {
+      Run& run = s->runs[r];
+      int64_t g_total = 0;
+      for (int32_t m = 0; m < M; ++m) g_total += run.fpm[m];
+      run.base_good = g_total;
+      if (g_total > run.best_good) {  // best selection so far, strict '>' (C24)
+        run.best_good = g_total;
         run.best = run.sel;
       }
       // C22: the model with the most unserved requests among those with an
@@ -925,16 +1088,15 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
       int64_t bu = 0;
       for (int32_t m = 0; m < M; ++m) {
         if (!run.may_place(m)) continue;  // outside this run's bucket
-        const int64_t un = ctx->model_n[m] - pm[b * M + m];
+        const int64_t un = ctx->model_n[m] - run.fpm[m];
         if (un <= 0 || (bm >= 0 && un <= bu)) continue;
         int32_t gbest = -1;
         for (int32_t g = 0; g < run.G; ++g) {
           if ((run.sel[m] >> g) & 1ULL) continue;  // a model at most once per group (C11)
           const int64_t mb = hp.mem_at(m, run.cfg[g]);
           if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
-          if (gbest < 0 ||
-              (__int128)busy[b * G + g] * hp.cfg_stages[run.cfg[gbest]] <
-                  (__int128)busy[b * G + gbest] * hp.cfg_stages[run.cfg[g]])
+          if (gbest < 0 || (__int128)run.fbusy[g] * hp.cfg_stages[run.cfg[gbest]] <
+                               (__int128)run.fbusy[gbest] * hp.cfg_stages[run.cfg[g]])
             gbest = g;
         }
         if (gbest < 0) continue;
@@ -950,6 +1112,9 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
       run.used[bgp] += hp.mem_at(bm, run.cfg[bgp]);
       run.history.emplace_back(bm, bgp);
       ++run.steps;
+      const int32_t a = run.find(bgp), c = run.find(run.G + bm);
+      if (a != c) run.parent[a] = c;  // unite comp(g*) and comp(m*)
+      run.pending = c;
     }
   }
 }
@@ -977,6 +1142,22 @@ asim_status asim_search_run(asim_search* s, void* cuda_stream) {
 
 }  // extern "C"
 
+// Outcome of run group gi (one Alg. 2 run; its beam members for beam > 1).
+static void group_best(const asim_search* s, int32_t gi, int64_t* good,
+                       const std::vector<uint64_t>** mask, int64_t* steps) {
+  if (s->beam == 1) {
+    const Run& r = s->runs[gi];
+    *good = r.best_good;
+    *mask = &r.best;
+    *steps = r.steps;
+  } else {
+    *good = s->gbest_good[gi];
+    *mask = &s->gbest[gi];
+    *steps = s->gsteps[gi];
+  }
+}
+static const Run& group_run(const asim_search* s, int32_t gi) { return s->runs[gi * s->beam]; }
+
 // Bucketed outcome (reading C28): plm_i* per job = its first best run on
 // strict '>' (none if no run serves a request); combo good = sum over its
 // jobs; the first best combo on strict '>'.
@@ -985,11 +1166,15 @@ static void bucket_best(const asim_search* s, int32_t* best_combo, int64_t* best
   job_run->assign(s->jobs.size(), -1);
   std::vector<int64_t> job_good(s->jobs.size(), 0);
   for (size_t j = 0; j < s->jobs.size(); ++j)
-    for (int32_t r : s->jobs[j].runs)
-      if (s->runs[r].best_good > job_good[j]) {
-        job_good[j] = s->runs[r].best_good;
+    for (int32_t r : s->jobs[j].runs) {
+      int64_t g = 0, st = 0;
+      const std::vector<uint64_t>* mk = nullptr;
+      group_best(s, r, &g, &mk, &st);
+      if (g > job_good[j]) {
+        job_good[j] = g;
         (*job_run)[j] = r;
       }
+    }
   *best_combo = -1;
   *best_good = 0;
   for (size_t c = 0; c < s->combos.size(); ++c) {
@@ -1023,10 +1208,13 @@ asim_status asim_search_result_get(const asim_search* s, asim_search_result* out
       for (int32_t j : s->combos[bc].jobs) {
         const int32_t r = job_run[j];
         if (r < 0) continue;
-        const Run& run = s->runs[r];
+        const Run& run = group_run(s, r);
+        int64_t g = 0, st = 0;
+        const std::vector<uint64_t>* mk = nullptr;
+        group_best(s, r, &g, &mk, &st);
         const int32_t off = (int32_t)cfg.size();
         for (int32_t m = 0; m < M; ++m)
-          if (off < 64) mask[m] |= run.best[m] << off;
+          if (off < 64) mask[m] |= (*mk)[m] << off;
         cfg.insert(cfg.end(), run.cfg.begin(), run.cfg.end());
       }
     const bool fits = (int32_t)cfg.size() <= ASIM_MAX_GROUPS;
@@ -1042,20 +1230,26 @@ asim_status asim_search_result_get(const asim_search* s, asim_search_result* out
   }
   int32_t best = -1;
   int64_t best_good = 0;
-  for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r)
-    if (s->runs[r].best_good > best_good) {  // Alg. 2: strict '>' keeps the first best run
-      best_good = s->runs[r].best_good;
+  const std::vector<uint64_t>* best_mask = nullptr;
+  for (int32_t r = 0; r < s->ngroups; ++r) {
+    int64_t g = 0, st = 0;
+    const std::vector<uint64_t>* mk = nullptr;
+    group_best(s, r, &g, &mk, &st);
+    if (g > best_good) {  // Alg. 2: strict '>' keeps the first best run
+      best_good = g;
       best = r;
+      best_mask = mk;
     }
+  }
   out->best_run = best;
   out->best_good = best_good;
-  out->num_groups = best >= 0 ? s->runs[best].G : 0;
+  out->num_groups = best >= 0 ? group_run(s, best).G : 0;
   if (out->group_cfg) {
     for (int32_t g = 0; g < ASIM_MAX_GROUPS; ++g)
-      out->group_cfg[g] = (best >= 0 && g < s->runs[best].G) ? s->runs[best].cfg[g] : -1;
+      out->group_cfg[g] = (best >= 0 && g < group_run(s, best).G) ? group_run(s, best).cfg[g] : -1;
   }
   if (out->host_mask)
-    for (int32_t m = 0; m < M; ++m) out->host_mask[m] = best >= 0 ? s->runs[best].best[m] : 0;
+    for (int32_t m = 0; m < M; ++m) out->host_mask[m] = best >= 0 ? (*best_mask)[m] : 0;
   return ASIM_OK;
 }
 
@@ -1087,15 +1281,18 @@ asim_status asim_search_buckets_get(const asim_search* s, asim_bucket_result* ou
 asim_status asim_search_run_info(const asim_search* s, int32_t run, int32_t* num_groups,
                                  int32_t* group_cfg, uint64_t* host_mask, int64_t* best_good,
                                  int64_t* steps) {
-  if (!s || run < 0 || run >= (int32_t)s->runs.size()) return ASIM_EINVAL;
-  const Run& r = s->runs[run];
+  if (!s || run < 0 || run >= s->ngroups) return ASIM_EINVAL;
+  const Run& r = group_run(s, run);
+  int64_t g = 0, st = 0;
+  const std::vector<uint64_t>* mk = nullptr;
+  group_best(s, run, &g, &mk, &st);
   if (num_groups) *num_groups = r.G;
   if (group_cfg)
-    for (int32_t g = 0; g < r.G; ++g) group_cfg[g] = r.cfg[g];
+    for (int32_t k = 0; k < r.G; ++k) group_cfg[k] = r.cfg[k];
   if (host_mask)
-    for (int32_t m = 0; m < s->ctx->hp.M; ++m) host_mask[m] = r.best[m];
-  if (best_good) *best_good = r.best_good;
-  if (steps) *steps = r.steps;
+    for (int32_t m = 0; m < s->ctx->hp.M; ++m) host_mask[m] = (*mk)[m];
+  if (best_good) *best_good = g;
+  if (steps) *steps = st;
   return ASIM_OK;
 }
 

@@ -1,0 +1,109 @@
+"""§8(f3): Alg. 1 with beam size k > 1 (readings C29-C30).
+
+CPU pins: k = 1 is the greedy search step for step; with a beam wider than
+any level of the search, beam search visits every feasible selection of the
+fixed groups, so it must return the brute-force optimum over them (computed
+here by plain enumeration and the DES).  GPU: libasim.so's beam search must
+reproduce the oracle's run by run."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import search as osearch
+from oracle import feasible, simulate
+from tests.helpers import random_instance
+from workloads import Placement, configs, traces
+
+
+def _fixed_groups_optimum(prob, tr, cfg):
+    M, G = prob.num_models, len(cfg)
+    best = 0
+    per_group = [list(itertools.chain.from_iterable(
+        itertools.combinations(range(M), r) for r in range(M + 1))) for _ in range(G)]
+    for choice in itertools.product(*per_group):
+        mask = np.zeros(M, np.uint64)
+        for g, ms in enumerate(choice):
+            for m in ms:
+                mask[m] |= np.uint64(1) << np.uint64(g)
+        pl = Placement(np.asarray(cfg, np.int32), mask)
+        if feasible(prob, pl):
+            best = max(best, simulate(prob, tr, pl)["good"])
+    return best
+
+
+def test_beam_one_is_greedy():
+    rng = np.random.default_rng(90)
+    for _ in range(30):
+        prob, tr, pl = random_instance(rng, n_req=int(rng.integers(1, 60)))
+        prob.budget_bytes = int(rng.integers(1, 4))
+        cfg = list(pl.group_cfg)
+        a = osearch.greedy(prob, tr, cfg)
+        b = osearch.greedy_beam(prob, tr, cfg, 1)
+        assert a["good"] == b["good"]
+        np.testing.assert_array_equal(a["placement"].host_mask, b["placement"].host_mask)
+
+
+def test_wide_beam_is_fixed_group_optimum():
+    """k >= every level's size: the beam holds every feasible selection of
+    each size, so best_sel is the optimum over all selections."""
+    rng = np.random.default_rng(91)
+    checked = 0
+    for _ in range(25):
+        prob, tr, pl = random_instance(rng, M=3, G=2, n_req=int(rng.integers(5, 50)))
+        prob.budget_bytes = int(rng.integers(1, 3))
+        cfg = list(pl.group_cfg)
+        want = _fixed_groups_optimum(prob, tr, cfg)
+        got = osearch.greedy_beam(prob, tr, cfg, 10**6)["good"]
+        assert got == want
+        checked += want > osearch.greedy(prob, tr, cfg)["good"]
+    assert checked >= 1  # some instance where k = 1 is not optimal
+
+
+# ------------------------------------------------------------------ GPU parity
+@pytest.fixture(scope="module")
+def sim():
+    from paper_2302_11665_b200 import Simulator
+    s = Simulator(0)
+    yield s
+    s.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [2, 3, 1000])
+def test_beam_parity_random(sim, k):
+    rng = np.random.default_rng(92 + k)
+    for _ in range(15):
+        prob, tr, pl = random_instance(rng, M=3, G=int(rng.integers(1, 4)),
+                                       n_req=int(rng.integers(1, 120)))
+        prob.budget_bytes = int(rng.integers(1, 4))
+        runs = [list(pl.group_cfg), list(pl.group_cfg[::-1])]
+        sim.set_problem(prob)
+        sim.set_trace(tr.arrival_ns, tr.model)
+        res = sim.search(runs=runs, beam=k)
+        for r_gpu, cfg in zip(res.runs, runs):
+            ref = osearch.greedy_beam(prob, tr, cfg, k)
+            assert r_gpu["best_good"] == ref["good"]
+            np.testing.assert_array_equal(r_gpu["host_mask"], ref["placement"].host_mask)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [2, 4])
+def test_beam_parity_alg2(sim, k):
+    prob = configs.motivating_problem(slo_scale=1.5)
+    tr = configs.motivating_trace(seed=2, n_requests=1000)
+    cases = [(prob, tr)]
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "MoE-5.3B") for i in range(2)]
+    p2 = configs.build_problem(names, 4, 13 * 10**9, slo_scale=3.0)
+    cases.append((p2, traces.maf2_shaped(5, len(names), 6.0, 300.0)))
+    for prob, tr in cases:
+        ref = osearch.alg2_beam(prob, tr, k)
+        sim.set_problem(prob)
+        sim.set_trace(tr.arrival_ns, tr.model)
+        res = sim.search(beam=k)
+        assert res.best_good == ref["good"]
+        assert res.best_run == ref["run"]
+        for r_gpu, r_ref in zip(res.runs, ref["runs"]):
+            assert r_gpu["best_good"] == r_ref["good"]
+            np.testing.assert_array_equal(r_gpu["host_mask"], r_ref["placement"].host_mask)

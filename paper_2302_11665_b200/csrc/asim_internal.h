@@ -118,6 +118,15 @@ struct ChunkParams {
   // c = batch index; when set they replace spec_state for the candidate's own
   // trajectory (spec_state still supplies out-of-component slots when publishing).
   const int64_t* spec_cand;
+  // Fast-heuristic statistics (nullable = off): per (chunk, batch candidate)
+  // rows of per-model good counts [J][C][M] and per-group busy [J][C][G];
+  // spec_* hold pass 1's counts, fix_* the exact corrections (pass 2 / walk),
+  // summed like spec_good / fix_good.  Zeroed before pass 1.
+  int32_t* spec_pm;
+  int32_t* fix_pm;
+  int64_t* spec_busy;
+  int64_t* fix_busy;
+  int64_t stat_C;
 };
 
 // Per-candidate speculation rows for the search (see search.cpp):
@@ -151,6 +160,10 @@ cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStr
 // config, S class != 0) over the whole trace; writes good, sum, per-model good
 // and per-group busy into `out`.  fast_stats_smem: dynamic shared memory.
 size_t fast_stats_smem(int slots_max, int M, bool u32);
+// out.good_per_model[c][m] / out.busy[c][g] = sum over chunks of the spec_*
+// and fix_* statistics rows (after launch_chunk_reduce).
+cudaError_t launch_chunk_stats_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
+                                      int64_t* launches);
 cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32, cudaStream_t st,
                               int64_t* launches);
 // Pass 3: re-simulate every chunk whose start state was wrong (per lane) and

@@ -249,7 +249,7 @@ template <typename T, int S>
 __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& w, T* st, int lane,
                                         int m, int hinfo, int h0, bool mine, int my_g,
                                         bool active, T ar, const T* dv, T tl, T sl,
-                                        unsigned long long& upd) {
+                                        unsigned long long& upd, int& gout) {
   // hinfo = first host | second host << 8 | host count << 16 (the base's
   // hosting list of m, ascending); hosts beyond the second come from w.hid
   T best_f = TT<T>::maxv();
@@ -311,6 +311,7 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
     }
   }
   if (active && best_g < 64 && (T)(best_f - ar) <= sl) {  // reject at receipt if the SLO is missed (C2, C3)
+    gout = best_g;
     if constexpr (S == 1) {
       st[best_g * 32 + lane] = best_f - tl;  // one stage: its departure is f - tail
     } else {
@@ -319,6 +320,43 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
     return (int64_t)(best_f - ar);
   }
   return -1;
+}
+
+// Stage occupancy sum_k d_k of model m on group g (fast-heuristic busy time).
+template <typename T, int S>
+__device__ __forceinline__ int64_t occupancy(const ChunkParams& P, const WarpMem<T>& w, int g,
+                                             int m, const T* dv) {
+  int64_t o = 0;
+  if constexpr (S > 0) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) o += (int64_t)dv[k];
+  } else {
+    const uint32_t e = w.gt[g];
+    const int cfg = (int)(e & 0xFFFFu), s = (int)(e >> 24);
+    const int64_t* d = P.pr.stage + ((int64_t)m * P.pr.P + cfg) * P.pr.S;
+    for (int k = 0; k < s; ++k) o += __ldg(d + k);
+  }
+  return o;
+}
+
+// Statistics row of (chunk j, batch candidate c): counts += sign for model m,
+// busy += sign * occ for group g.  Fire-and-forget reductions (no return).
+__device__ __forceinline__ void stat_add(int32_t* pm, int64_t* busy, const ChunkParams& P, int j,
+                                         int64_t c, int m, int g, int64_t occ, int sign) {
+  const int64_t row = (int64_t)j * P.stat_C + c;
+  atomicAdd(pm + row * P.pr.M + m, sign);
+  atomicAdd(reinterpret_cast<unsigned long long*>(busy + row * P.bt.G + g),
+            (unsigned long long)(sign * occ));
+}
+
+// Walk: the correction row of (j, c) restarts at minus pass 1's counts.
+__device__ __forceinline__ void stat_reset(const ChunkParams& P, int j, int64_t c, int lane,
+                                           int stride) {
+  const int64_t row = (int64_t)j * P.stat_C + c;
+  for (int m = lane; m < P.pr.M; m += stride)
+    P.fix_pm[row * P.pr.M + m] = -P.spec_pm[row * P.pr.M + m];
+  for (int g = lane; g < P.bt.G; g += stride)
+    P.fix_busy[row * P.bt.G + g] = -P.spec_busy[row * P.bt.G + g];
 }
 
 template <typename T>
@@ -447,6 +485,9 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       for (int k = 0; k < slots; ++k) spec_st[k * 32 + lane] = (T)0;
     }
   }
+  if constexpr (MODE == WALK) {
+    if (P.fix_pm && active) stat_reset(P, j, c, 0, 1);  // this lane's own row
+  }
   if constexpr (MODE != SPEC) {  // the true trajectory: true end of chunk j-1 (per lane)
     const int64_t prev = unit - P.num_items;
     const bool src = (srcmask >> lane) & 1u;
@@ -556,18 +597,27 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       }
       const bool live = active && ((kmask >> (cm & 63)) & 1ull);
       const bool mine = live && cm == my_m;
+      int g0 = 0, g1 = 0;
       const int64_t l0 = step<T, S>(P, w, w.st0, lane, cm, chinfo, ch0, mine, my_g, live, car,
-                                    dv, ctl, csl, upd);
+                                    dv, ctl, csl, upd, g0);
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
+        if (P.spec_pm) {  // SPEC: pass-1 counts; DUAL / WALK: the true side of the correction
+          if constexpr (MODE == SPEC)
+            stat_add(P.spec_pm, P.spec_busy, P, j, c, cm, g0, occupancy<T, S>(P, w, g0, cm, dv), 1);
+          else
+            stat_add(P.fix_pm, P.fix_busy, P, j, c, cm, g0, occupancy<T, S>(P, w, g0, cm, dv), 1);
+        }
       }
       if constexpr (MODE == DUAL) {
         const int64_t l1 = step<T, S>(P, w, w.st1, lane, cm, chinfo, ch0, mine, my_g, live,
-                                      car, dv, ctl, csl, upd);
+                                      car, dv, ctl, csl, upd, g1);
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;
+          if (P.spec_pm)  // minus the speculative side
+            stat_add(P.fix_pm, P.fix_busy, P, j, c, cm, g1, occupancy<T, S>(P, w, g1, cm, dv), -1);
         }
       }
       if (!more) break;
@@ -744,15 +794,15 @@ __device__ __forceinline__ T warp_min(T v) {
 
 // One warp simulates ONE candidate over requests [i_begin, i_end): state v
 // (slot = lane + 32 q) in registers, epoch E (uint32 mode).  STATS adds the
-// fast heuristic's outputs: per-model good counts in shared memory (cnt[M])
-// and per-group busy time in registers (busy[q2] = group lane + 32 q2).
+// fast heuristic's outputs: per-model good counts (pm_row[M]) and per-group
+// busy time (busy_row[G]), global rows updated by fire-and-forget atomics.
 template <typename T, int S, int Q, bool STATS>
 __device__ __forceinline__ void coop_range(const ChunkParams& P, const WarpMem<T>& w,
                                            int64_t i_begin, int64_t i_end, T (&v)[Q], int64_t& E,
                                            uint64_t kmask, int my_m, uint64_t my_bit,
                                            const uint64_t (&lastbit)[Q], int lane, int64_t& good,
                                            int64_t& sum, unsigned long long& upd,
-                                           int32_t* cnt, int64_t (&busy)[2]) {
+                                           int32_t* pm_row, int64_t* busy_row) {
   for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
     const bool valid = i0 + lane < i_end;
     const int64_t al = valid ? P.tr.arrival[i0 + lane] : 0;
@@ -854,10 +904,9 @@ __device__ __forceinline__ void coop_range(const ChunkParams& P, const WarpMem<T
       sum += (int64_t)(fmin - ar);
       if constexpr (STATS) {
         const int64_t occ = __shfl_sync(FULL, occl, jj);
-        if (lane == 0) cnt[m] += 1;
-        if (lane == (gw & 31)) {  // constant indices keep busy[] in registers
-          if (gw >> 5) busy[1] += occ;
-          else busy[0] += occ;
+        if (lane == 0) {
+          atomicAdd(pm_row + m, 1);
+          atomicAdd(reinterpret_cast<unsigned long long*>(busy_row + gw), (unsigned long long)occ);
         }
       }
     }
@@ -920,9 +969,17 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
       }
     }
     int64_t good = 0, sum = 0;
-    int64_t busy_unused[2] = {0, 0};
-    coop_range<T, S, Q, false>(P, w, i_begin, i_end, v, E, kmask, my_m, my_bit, lastbit, lane,
-                               good, sum, upd, nullptr, busy_unused);
+    if (P.fix_pm) {  // fast-heuristic statistics: this chunk's correction row restarts
+      stat_reset(P, j, c, lane, 32);
+      __syncwarp();
+      const int64_t row = (int64_t)j * P.stat_C + c;
+      coop_range<T, S, Q, true>(P, w, i_begin, i_end, v, E, kmask, my_m, my_bit, lastbit, lane,
+                                good, sum, upd, P.fix_pm + row * P.pr.M,
+                                P.fix_busy + row * P.bt.G);
+    } else {
+      coop_range<T, S, Q, false>(P, w, i_begin, i_end, v, E, kmask, my_m, my_bit, lastbit, lane,
+                                 good, sum, upd, nullptr, nullptr);
+    }
     // the chunk's exact correction, and equivalence with the speculative end
     if (lane == 0) {
       P.fix_good[j * cstride + (int64_t)item * 32 + cl] =
@@ -1032,7 +1089,7 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
 // per-group busy.  Items hold one candidate each (cl = 0).
 template <typename T, int S, int Q>
 __device__ __forceinline__ void fast_candidate(const ChunkParams& P, const WarpMem<T>& w,
-                                               const ItemDesc& it, int lane, int32_t* cnt,
+                                               const ItemDesc& it, int lane,
                                                const DevOut& out, unsigned long long& upd) {
   const int64_t c = it.first;
   const int slots = it.slots;
@@ -1048,33 +1105,31 @@ __device__ __forceinline__ void fast_candidate(const ChunkParams& P, const WarpM
   const uint64_t my_bit = my_m >= 0 ? (1ull << my_g) : 0ull;
   int64_t E = (TT<T>::kRel && P.tr.n > 0) ? P.tr.arrival[0] : 0;
   int64_t good = 0, sum = 0;
-  int64_t busy[2] = {0, 0};
   const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;  // component restriction
-  coop_range<T, S, Q, true>(P, w, 0, P.tr.n, v, E, kmask, my_m, my_bit, lastbit, lane, good, sum,
-                            upd, cnt, busy);
-  __syncwarp();
   const int64_t o = c - out.out_offset;
+  // per-model good counts are int32 rows here; out.good_per_model is int64:
+  // accumulate into the int32 scratch P.spec_pm row, copied below
+  int32_t* pm_row = P.spec_pm + o * P.pr.M;
+  coop_range<T, S, Q, true>(P, w, 0, P.tr.n, v, E, kmask, my_m, my_bit, lastbit, lane, good, sum,
+                            upd, pm_row, out.busy + o * P.bt.G);
+  __syncwarp();
+  __threadfence_block();
   if (lane == 0) {
     out.good[o] = good;
     if (out.sum_latency) out.sum_latency[o] = sum;
   }
-  if (out.good_per_model)
-    for (int m = lane; m < P.pr.M; m += 32) out.good_per_model[o * P.pr.M + m] = cnt[m];
-  if (out.busy) {
-    if (lane < P.bt.G) out.busy[o * P.bt.G + lane] = busy[0];
-    if (lane + 32 < P.bt.G) out.busy[o * P.bt.G + lane + 32] = busy[1];
-  }
+  for (int m = lane; m < P.pr.M; m += 32) out.good_per_model[o * P.pr.M + m] = pm_row[m];
 }
 
 template <typename T, int S>
 __device__ __forceinline__ void fast_dispatch_q(const ChunkParams& P, const WarpMem<T>& w,
-                                                const ItemDesc& it, int lane, int32_t* cnt,
+                                                const ItemDesc& it, int lane,
                                                 const DevOut& out, unsigned long long& upd) {
   switch ((it.slots + 31) / 32) {
-    case 1: fast_candidate<T, S, 1>(P, w, it, lane, cnt, out, upd); break;
-    case 2: fast_candidate<T, S, 2>(P, w, it, lane, cnt, out, upd); break;
-    case 3: fast_candidate<T, S, 3>(P, w, it, lane, cnt, out, upd); break;
-    default: fast_candidate<T, S, 4>(P, w, it, lane, cnt, out, upd); break;
+    case 1: fast_candidate<T, S, 1>(P, w, it, lane, out, upd); break;
+    case 2: fast_candidate<T, S, 2>(P, w, it, lane, out, upd); break;
+    case 3: fast_candidate<T, S, 3>(P, w, it, lane, out, upd); break;
+    default: fast_candidate<T, S, 4>(P, w, it, lane, out, upd); break;
   }
 }
 
@@ -1083,22 +1138,18 @@ __global__ void __launch_bounds__(kWarps * 32) fast_stats_kernel(ChunkParams P, 
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
-  const size_t cb = ((size_t)P.pr.M * 4 + 15) & ~size_t(15);
-  unsigned char* mine = smem + warp * (wb + cb);
-  WarpMem<T> w = carve<T>(mine, P, false);
-  int32_t* cnt = reinterpret_cast<int32_t*>(mine + wb);
+  WarpMem<T> w = carve<T>(smem + warp * wb, P, false);
   const int item = blockIdx.x * kWarps + warp;
   if (item >= P.num_items) return;
   const ItemDesc it = P.items[item];
-  for (int m = lane; m < P.pr.M; m += 32) cnt[m] = 0;
   load_base<T>(P, it, w, lane);
   unsigned long long upd = 0;
   switch (it.S) {
-    case 1: fast_dispatch_q<T, 1>(P, w, it, lane, cnt, out, upd); break;
-    case 2: fast_dispatch_q<T, 2>(P, w, it, lane, cnt, out, upd); break;
-    case 4: fast_dispatch_q<T, 4>(P, w, it, lane, cnt, out, upd); break;
-    case 8: fast_dispatch_q<T, 8>(P, w, it, lane, cnt, out, upd); break;
-    default: fast_dispatch_q<T, 16>(P, w, it, lane, cnt, out, upd); break;
+    case 1: fast_dispatch_q<T, 1>(P, w, it, lane, out, upd); break;
+    case 2: fast_dispatch_q<T, 2>(P, w, it, lane, out, upd); break;
+    case 4: fast_dispatch_q<T, 4>(P, w, it, lane, out, upd); break;
+    case 8: fast_dispatch_q<T, 8>(P, w, it, lane, out, upd); break;
+    default: fast_dispatch_q<T, 16>(P, w, it, lane, out, upd); break;
   }
   if (lane == 0 && P.stage_updates && upd) atomicAdd(P.stage_updates, upd);
 }
@@ -1294,8 +1345,40 @@ cudaError_t launch_mix_states(int64_t C0, int64_t C1, int32_t J, int32_t stride,
 }
 
 size_t fast_stats_smem(int slots_max, int M, bool u32) {
-  const size_t wb = warp_bytes(slots_max, M, u32 ? 4 : 8, false);
-  return kWarps * (wb + (((size_t)M * 4 + 15) & ~size_t(15)));
+  return kWarps * warp_bytes(slots_max, M, u32 ? 4 : 8, false);
+}
+
+// out.good_per_model[c][m] = sum_j spec_pm[j][c][m] + sum_{j>=1} fix_pm[j][c][m];
+// out.busy likewise.  One thread per (c, m) and per (c, g).
+__global__ void chunk_stats_reduce_kernel(ChunkParams P, DevOut out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t M = P.pr.M, G = P.bt.G, C = P.stat_C;
+  if (t < C * M) {
+    const int64_t c = t / M, m = t % M;
+    int64_t v = 0;
+    for (int j = 0; j < P.J; ++j) {
+      v += P.spec_pm[((int64_t)j * C + c) * M + m];
+      if (j > 0) v += P.fix_pm[((int64_t)j * C + c) * M + m];
+    }
+    out.good_per_model[(c - out.out_offset) * M + m] = v;
+  } else if (t < C * M + C * G) {
+    const int64_t u = t - C * M, c = u / G, g = u % G;
+    int64_t v = 0;
+    for (int j = 0; j < P.J; ++j) {
+      v += P.spec_busy[((int64_t)j * C + c) * G + g];
+      if (j > 0) v += P.fix_busy[((int64_t)j * C + c) * G + g];
+    }
+    out.busy[(c - out.out_offset) * G + g] = v;
+  }
+}
+
+cudaError_t launch_chunk_stats_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
+                                      int64_t* launches) {
+  const int64_t n = P.stat_C * (P.pr.M + P.bt.G);
+  if (n == 0) return cudaSuccess;
+  chunk_stats_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32, cudaStream_t st,

@@ -76,6 +76,8 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   const bool u32 = theta > 0;
   if (asim::fast_stats_smem(slots_max, hp.M, u32) > 227 * 1024) return ASIM_OK;
   cudaError_t e = upload(ctx->c_items, items, st);
+  if (e == cudaSuccess) e = ctx->c_spm.ensure((size_t)C * hp.M * 4 + 8);  // int32 count rows
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_spm.p, 0, (size_t)C * hp.M * 4, st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload fast items");
   asim::ChunkParams P{};
   P.pr = ctx->dev_problem();
@@ -94,6 +96,8 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   P.J = 1;
   P.theta = theta;
   P.slots_max = slots_max;
+  P.spec_pm = ctx->c_spm.as<int32_t>();
+  P.stat_C = C;
   P.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (ctx->profiling) {
@@ -225,6 +229,28 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.state_stride = (opt && opt->state_stride > 0) ? opt->state_stride : slots_max;
   if (P.spec_state && P.state_stride < slots_max)
     return asim_fail(ctx, ASIM_ERANGE, "internal: state stride below slots");
+  // fast-heuristic statistics (per-model good, per-group busy) of every candidate
+  const bool stats = out.good_per_model != nullptr || out.busy != nullptr;
+  if (stats) {
+    if (!out.good_per_model || !out.busy || begin != 0 || end != P.bt.C)
+      return asim_fail(ctx, ASIM_ESTATE, "internal: statistics need both outputs, whole batch");
+    const int64_t C = P.bt.C;
+    const size_t npm = (size_t)J * C * hp.M, nb = (size_t)J * C * std::max(hb.G, 1);
+    e = ctx->c_spm.ensure(npm * 4 + 8);
+    if (e == cudaSuccess) e = ctx->c_fpm.ensure(npm * 4 + 8);
+    if (e == cudaSuccess) e = ctx->c_sbusy.ensure(nb * 8 + 8);
+    if (e == cudaSuccess) e = ctx->c_fbusy.ensure(nb * 8 + 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_spm.p, 0, npm * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_fpm.p, 0, npm * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_sbusy.p, 0, nb * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_fbusy.p, 0, nb * 8, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "statistics buffers");
+    P.spec_pm = ctx->c_spm.as<int32_t>();
+    P.fix_pm = ctx->c_fpm.as<int32_t>();
+    P.spec_busy = ctx->c_sbusy.as<int64_t>();
+    P.fix_busy = ctx->c_fbusy.as<int64_t>();
+    P.stat_C = C;
+  }
 
   // ---- pass 1: every (item, chunk) from the speculative start
   P.num_units = (int32_t)(J * I);
@@ -250,6 +276,10 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   }
   e = asim::launch_chunk_reduce(P, out, st, &ctx->launches);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk reduce");
+  if (stats) {
+    e = asim::launch_chunk_stats_reduce(P, out, st, &ctx->launches);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "statistics reduce");
+  }
   ctx->last_valid = true;
   ctx->last_u32 = u32;
   ctx->last_params = P;

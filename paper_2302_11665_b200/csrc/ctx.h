@@ -80,6 +80,7 @@ struct asim_ctx {
   asim::ChunkParams last_params{};
   std::vector<asim::ItemDesc> last_items;
   DBuf c_pub;
+  DBuf c_spm, c_fpm, c_sbusy, c_fbusy;  // fast-heuristic statistics rows
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
 
   // scratch for evaluate()

@@ -527,8 +527,8 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     probe_hb.slots = stride;
     asim::DevOut probe{};
     const bool eligible = asim_chunked_eligible(ctx, probe_hb, probe);
-    // the general kernel has no time chunks; the fast heuristic only uses it
-    s->use_states = ctx->force_path != 1 && eligible && !s->fast;
+    // the general kernel has no time chunks
+    s->use_states = ctx->force_path != 1 && eligible;
     s->restrict_k = s->use_states && hp.M <= 64;
   }
   if (s->use_states && !s->runs.empty()) {
@@ -1037,12 +1037,44 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
       out.good = s->d_good_all.as<int64_t>();
       out.good_per_model = s->d_pm.as<int64_t>();
       out.busy = s->d_busy.as<int64_t>();
-      // warp-cooperative whole-trace kernel (uniform configs, component
-      // restricted), else the general kernel over every model
+      // chunked kernels speculating from the run's previous boundary states
+      // (component restricted); else the warp-cooperative whole-trace kernel
+      // (uniform configs); else the general kernel over every model
       asim_status rc = asim_upload_batch(ctx, hb, st);
       if (rc) return rc;
       bool done = false;
-      if (ctx->force_path != 1) {
+      if (s->use_states) {
+        e = upload(s->d_rows, sim_b, st);
+        if (e != cudaSuccess) return asim_cuda(ctx, e, "upload rows");
+        ChunkOptions opt;
+        opt.J = s->J;
+        opt.state_stride = s->stride;
+        opt.spec_state = s->st_base.as<int64_t>();
+        opt.spec_row = s->d_rows.as<int32_t>();
+        asim::DevOut o2 = out;
+        o2.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        if (ctx->profiling) {
+          if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
+            return asim_cuda(ctx, cudaGetLastError(), "event create");
+          cudaEventRecord(ev0, st);
+        }
+        rc = asim_run_chunked(ctx, hb, 0, C, o2, st, &opt);
+        if (rc) return rc;
+        if (ctx->profiling) {
+          cudaEventRecord(ev1, st);
+          ctx->events.emplace_back(ev0, ev1);
+          ++ctx->sim_launches;
+          ctx->request_evals += C * ctx->n;
+        }
+        // the new selections' boundary states replace the old ones in place
+        std::vector<int64_t> cs(C);
+        for (int64_t b = 0; b < C; ++b) cs[b] = b;
+        rc = asim_publish_candidates(ctx, cs, sim_b, s->st_base.as<int64_t>(), st);
+        if (rc) return rc;
+        done = true;
+      }
+      if (!done && ctx->force_path != 1) {
         rc = asim_run_fast_stats(ctx, hb, out, st, &done);
         if (rc) return rc;
       }

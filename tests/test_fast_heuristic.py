@@ -181,3 +181,27 @@ def test_fast_parity_s1_s3_shaped(sim):
                                   "MoE-2.4B", "MoE-5.3B") for i in range(2)]
     prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=5.0)
     _compare_fast(sim, prob, traces.maf2_shaped(4, len(names), 20.0, 300.0))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path,chunk", [(1, 4096), (0, 37), (0, 500), (3, 211)])
+def test_fast_parity_all_paths(sim, path, chunk):
+    """The same heuristic through every kernel: the general kernel (path 1),
+    the chunked passes with per-chunk statistics and speculation from the
+    previous step's states (small chunks: many fix-ups and walks), int64
+    times (path 3)."""
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "MoE-5.3B") for i in range(2)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=2.0)
+    tr = traces.maf2_shaped(9, len(names), 15.0, 400.0)
+    sim.set_path(path)
+    sim.set_chunk_size(chunk)
+    try:
+        _compare_fast(sim, prob, tr)
+        rng = np.random.default_rng(73)
+        for _ in range(6):
+            p2, t2, pl = random_instance(rng, n_req=int(rng.integers(50, 400)), tmax=400)
+            p2.budget_bytes = int(rng.integers(1, 4))
+            _compare_fast(sim, p2, t2, runs=[list(pl.group_cfg)])
+    finally:
+        sim.set_path(0)
+        sim.set_chunk_size(4096)

@@ -127,6 +127,7 @@ struct ChunkParams {
   int64_t* spec_busy;
   int64_t* fix_busy;
   int64_t stat_C;
+  int32_t scalar_walk;  // 1 = small components walk with the register-state scalar walker
 };
 
 // Per-candidate speculation rows for the search (see search.cpp):

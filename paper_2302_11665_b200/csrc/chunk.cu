@@ -1025,6 +1025,304 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pass 3, small components: the scalar walker.  When the candidate's own
+// component (cand_gmask) spans NG <= 32 groups with NG * S <= 32 stage slots,
+// its state fits in registers of every lane (all lanes hold the same values
+// and run the same code: no cross-lane operation sits on the per-request
+// dependency chain).  Per request: S max-plus steps per group, an
+// adjacent-pair argmin tree (blocks of ascending group ids, so the lower index
+// wins ties as in C1), and predicated commits.  Requests of other components
+// are skipped 32 at a time by a ballot, exactly as in the cooperative walker.
+template <typename T, int S, int NG>
+__device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const WarpMem<T>& w,
+                                                 const ItemDesc& it, int item, int cl, int lane,
+                                                 uint32_t* end_src, unsigned long long& walked,
+                                                 unsigned long long& upd) {
+  constexpr int R = NG * S;
+  const int64_t c = (int64_t)it.first + cl;
+  const int my_m = P.bt.cand_model[c], my_g = P.bt.cand_group[c];
+  const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;
+  const int ngroups = it.slots / S;
+  const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
+  const uint64_t gmask = (P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all;
+  // compact group i -> group id (ascending), -1 = padding
+  int cg[NG];
+  {
+    uint64_t b = gmask;
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      cg[i] = b ? (__ffsll((long long)b) - 1) : -1;
+      b &= b - 1;
+    }
+  }
+  // compact hosting mask of every model (the cooperative walker leaves the
+  // hosting-list region w.hid unused: it serves as scratch here)
+  uint32_t* hmc = reinterpret_cast<uint32_t*>(w.hid);
+  for (int m = lane; m < P.pr.M; m += 32) {
+    const uint64_t hm = w.hmask[m] | (m == my_m ? (1ull << my_g) : 0ull);
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < NG; ++i)
+      if (cg[i] >= 0 && ((hm >> cg[i]) & 1ull)) x |= 1u << i;
+    hmc[m] = x;
+  }
+  __syncwarp();
+  const int64_t cstride = (int64_t)P.num_items * 32;
+  bool start_ok = true;
+  for (int j = 1; j < P.J; ++j) {
+    const int64_t u = (int64_t)j * P.num_items + item;
+    if (start_ok) {
+      if ((P.fix_flag[u] >> cl) & 1u) {  // pass 2 exact; true end of j is its fix_end
+        if (lane == 0) atomicOr(end_src + u, 1u << cl);
+        start_ok = false;
+      }
+      continue;
+    }
+    ++walked;
+    const int64_t i_begin = P.chunk_begin[j], i_end = P.chunk_begin[j + 1];
+    int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
+    // true start: chunk j-1's true end (fix_end), component slots only
+    const int64_t prev = u - P.num_items;
+    const T* s0 = reinterpret_cast<const T*>(P.fix_end) + prev * P.slots_max * 32;
+    const int64_t Ep = P.fix_epoch[prev];
+    T v[R];
+#pragma unroll
+    for (int i = 0; i < NG; ++i)
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        T x = 0;
+        if (cg[i] >= 0) {
+          const T raw = s0[(cg[i] * S + k) * 32 + cl];
+          if constexpr (TT<T>::kRel) {
+            const int64_t r = (int64_t)raw - (E - Ep);
+            x = r > 0 ? (T)r : (T)0;
+          } else {
+            x = raw;
+          }
+        }
+        v[i * S + k] = x;
+      }
+    int32_t* pm_row = nullptr;
+    int64_t* busy_row = nullptr;
+    if (P.fix_pm) {  // fast-heuristic statistics: this chunk's correction row restarts
+      stat_reset(P, j, c, lane, 32);
+      __syncwarp();
+      const int64_t row = (int64_t)j * P.stat_C + c;
+      pm_row = P.fix_pm + row * P.pr.M;
+      busy_row = P.fix_busy + row * P.bt.G;
+    }
+    int64_t good = 0, sum = 0;
+    for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
+      const bool valid = i0 + lane < i_end;
+      const int64_t al = valid ? P.tr.arrival[i0 + lane] : 0;
+      const int ml = valid ? (int)P.tr.model[i0 + lane] : 0;
+      unsigned todo = __ballot_sync(FULL, valid && ((kmask >> (ml & 63)) & 1ull));
+      if (!todo) continue;
+      bool per_req = false;
+      if constexpr (TT<T>::kRel) {
+        const int64_t a_last = __shfl_sync(FULL, al, 31 - __clz(todo));
+        if (a_last - E > P.theta) {  // move the epoch to the tile's first request
+          const int64_t a_first = __shfl_sync(FULL, al, __ffs(todo) - 1);
+          const int64_t gap = a_first - E;
+          const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+          for (int r = 0; r < R; ++r) v[r] = v[r] > delta ? v[r] - delta : (T)0;
+          E = a_first;
+          per_req = a_last - E > P.theta;
+        }
+      }
+      const T arl = (T)(al - E);
+      const uint32_t hml = hmc[ml];
+      const T tll = w.tail[ml], sll = w.slo[ml];
+      {
+        const bool rel = (todo >> lane) & 1u;
+        upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popc(hml) : 0u) * S;
+      }
+      while (todo) {
+        const int jj = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int m = __shfl_sync(FULL, ml, jj);
+        T ar = __shfl_sync(FULL, arl, jj);
+        const uint32_t hm = __shfl_sync(FULL, hml, jj);
+        const T tl = __shfl_sync(FULL, tll, jj), sl = __shfl_sync(FULL, sll, jj);
+        if constexpr (TT<T>::kRel) {
+          if (per_req) {
+            const int64_t a = __shfl_sync(FULL, al, jj);
+            if (a - E > P.theta) {
+              const int64_t gap = a - E;
+              const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+              for (int r = 0; r < R; ++r) v[r] = v[r] > delta ? v[r] - delta : (T)0;
+              E = a;
+            }
+            ar = (T)(a - E);
+          }
+        }
+        T d[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) d[k] = w.d[m * kSTab + k];
+        // predicted finish f of every compact group (departures y for S > 1;
+        // a single stage departs at f - tail)
+        T f[NG];
+        T y[S > 1 ? R : 1];
+#pragma unroll
+        for (int i = 0; i < NG; ++i) {
+          T x = ar;
+#pragma unroll
+          for (int k = 0; k < S; ++k) {
+            x = tmax(x, v[i * S + k]) + d[k];
+            if constexpr (S > 1) y[i * S + k] = x;
+          }
+          f[i] = ((hm >> i) & 1u) ? x + tl : TT<T>::maxv();
+        }
+        T fmin = f[0];
+#pragma unroll
+        for (int i = 1; i < NG; ++i) fmin = tmin(fmin, f[i]);
+        if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) continue;  // no host / misses the SLO
+        // the lowest compact index among the minima = the lowest group id (C1)
+        uint32_t eqm = 0;
+#pragma unroll
+        for (int i = 0; i < NG; ++i) eqm |= (f[i] == fmin ? 1u : 0u) << i;
+        const int wi = __ffs(eqm) - 1;
+#pragma unroll
+        for (int i = 0; i < NG; ++i) {
+          if constexpr (S == 1) {
+            if (i == wi) v[i] = fmin - tl;
+          } else {
+#pragma unroll
+            for (int k = 0; k < S; ++k)
+              if (i == wi) v[i * S + k] = y[i * S + k];
+          }
+        }
+        ++good;
+        sum += (int64_t)(fmin - ar);
+        if (pm_row && lane == 0) {
+          int gw = 0;
+          int64_t occ = 0;
+#pragma unroll
+          for (int i = 0; i < NG; ++i)
+            if (i == wi) gw = cg[i];
+#pragma unroll
+          for (int k = 0; k < S; ++k) occ += (int64_t)d[k];
+          atomicAdd(pm_row + m, 1);
+          atomicAdd(reinterpret_cast<unsigned long long*>(busy_row + gw), (unsigned long long)occ);
+        }
+      }
+    }
+    // the chunk's exact correction, and equivalence with the speculative end
+    if (lane == 0) {
+      P.fix_good[j * cstride + (int64_t)item * 32 + cl] =
+          (int32_t)(good - P.spec_good[j * cstride + (int64_t)item * 32 + cl]);
+      P.fix_sum[j * cstride + (int64_t)item * 32 + cl] =
+          sum - P.spec_sum[j * cstride + (int64_t)item * 32 + cl];
+    }
+    if (j + 1 < P.J) {
+      const int64_t a_next = P.tr.arrival[i_end];
+      const T* se = reinterpret_cast<const T*>(P.spec_end) + u * P.slots_max * 32;
+      const int64_t Es = P.spec_epoch[u];
+      bool eq = true;
+#pragma unroll
+      for (int i = 0; i < NG; ++i)
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          if (cg[i] < 0) continue;
+          const int64_t t0 = (TT<T>::kRel ? E : 0) + (int64_t)v[i * S + k];
+          const int64_t t1 = (TT<T>::kRel ? Es : 0) + (int64_t)se[(cg[i] * S + k) * 32 + cl];
+          eq &= (t0 > a_next ? t0 : a_next) == (t1 > a_next ? t1 : a_next);
+        }
+      start_ok = eq;  // identical in every lane
+      if (!start_ok) {  // publish column cl at the unit's canonical epoch
+        const int64_t Ec = P.tr.arrival[i_end - 1];
+        T* out = reinterpret_cast<T*>(P.fix_end) + u * P.slots_max * 32;
+        // slots outside the component keep their start values
+        for (int t = lane; t < it.slots; t += 32) {
+          if ((gmask >> ((t / S) & 63)) & 1ull) continue;
+          const T raw = s0[t * 32 + cl];
+          if constexpr (TT<T>::kRel) {
+            const int64_t r = (int64_t)raw + Ep - Ec;
+            out[t * 32 + cl] = r > 0 ? (T)r : (T)0;
+          } else {
+            out[t * 32 + cl] = raw;
+          }
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int i = 0; i < NG; ++i)
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+              if (cg[i] < 0) continue;
+              T x;
+              if constexpr (TT<T>::kRel) {
+                const int64_t r = (int64_t)v[i * S + k] - (Ec - E);
+                x = r > 0 ? (T)r : (T)0;
+              } else {
+                x = v[i * S + k];
+              }
+              out[(cg[i] * S + k) * 32 + cl] = x;
+            }
+          P.fix_epoch[u] = Ec;
+          atomicOr(end_src + u, 1u << cl);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename T, int S>
+__device__ __forceinline__ bool scalar_dispatch_ng(const ChunkParams& P, const WarpMem<T>& w,
+                                                   const ItemDesc& it, int item, int cl, int lane,
+                                                   uint32_t* end_src, unsigned long long& walked,
+                                                   unsigned long long& upd, int ng) {
+  // NG = the next power of two >= ng, with NG * S <= 32
+  if (ng <= 1) {
+    scalar_candidate<T, S, 1>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 2 && 2 * S <= 32) {
+    scalar_candidate<T, S, (2 * S <= 32 ? 2 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 4 && 4 * S <= 32) {
+    scalar_candidate<T, S, (4 * S <= 32 ? 4 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 8 && 8 * S <= 32) {
+    scalar_candidate<T, S, (8 * S <= 32 ? 8 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 16 && 16 * S <= 32) {
+    scalar_candidate<T, S, (16 * S <= 32 ? 16 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 32 && S == 1) {
+    scalar_candidate<T, S, (S == 1 ? 32 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else {
+    return false;
+  }
+  return true;
+}
+
+// Does candidate c's component fit the scalar walker (NG * S <= 32)?
+__device__ __forceinline__ bool scalar_fits(const ChunkParams& P, const ItemDesc& it, int64_t c) {
+  const int ngroups = it.slots / it.S;
+  const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
+  const uint64_t gmask = (P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all;
+  int ng = __popcll(gmask), np2 = 1;
+  while (np2 < ng) np2 <<= 1;
+  return np2 * it.S <= 32;
+}
+
+template <typename T>
+__device__ __forceinline__ bool scalar_dispatch(const ChunkParams& P, const WarpMem<T>& w,
+                                                const ItemDesc& it, int item, int cl, int lane,
+                                                uint32_t* end_src, unsigned long long& walked,
+                                                unsigned long long& upd) {
+  const int64_t c = (int64_t)it.first + cl;
+  const int ngroups = it.slots / it.S;
+  const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
+  const uint64_t gmask = (P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all;
+  const int ng = __popcll(gmask);
+  switch (it.S) {
+    case 1: return scalar_dispatch_ng<T, 1>(P, w, it, item, cl, lane, end_src, walked, upd, ng);
+    case 2: return scalar_dispatch_ng<T, 2>(P, w, it, item, cl, lane, end_src, walked, upd, ng);
+    case 4: return scalar_dispatch_ng<T, 4>(P, w, it, item, cl, lane, end_src, walked, upd, ng);
+    case 8: return scalar_dispatch_ng<T, 8>(P, w, it, item, cl, lane, end_src, walked, upd, ng);
+    default: return scalar_dispatch_ng<T, 16>(P, w, it, item, cl, lane, end_src, walked, upd, ng);
+  }
+}
+
 template <typename T, int S>
 __device__ __forceinline__ void coop_dispatch_q(const ChunkParams& P, const WarpMem<T>& w,
                                                 const ItemDesc& it, int item, int cl, int lane,
@@ -1052,7 +1350,10 @@ __device__ __forceinline__ void coop_dispatch(const ChunkParams& P, const WarpMe
   }
 }
 
-template <typename T>
+// SCALAR = false: the cooperative walker for every candidate the scalar one
+// does not take; SCALAR = true: the scalar walker (separate kernel: its
+// register arrays would otherwise spill the cooperative walker).
+template <typename T, bool SCALAR>
 __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, uint32_t* end_src) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1066,6 +1367,8 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     const int item = u >> 5, cl = u & 31;
     const ItemDesc it = P.items[item];
     if (it.S == 0 || cl >= it.count || !P.bt.cand_ok[(int64_t)it.first + cl]) continue;
+    const bool fits = P.scalar_walk && scalar_fits(P, it, (int64_t)it.first + cl);
+    if (fits != SCALAR) continue;  // the other walker's candidate
     // any chunk of this candidate flagged by pass 2?  (else nothing to walk)
     bool any = false;
     for (int j = 1 + lane; j < P.J; j += 32)
@@ -1075,7 +1378,10 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
       load_base<T>(P, it, w, lane);
       cur_base = it.base;
     }
-    coop_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
+    if constexpr (SCALAR)
+      scalar_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
+    else
+      coop_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
   }
   if (lane == 0) {
     if (P.walked && walked) atomicAdd(P.walked, walked);
@@ -1280,10 +1586,19 @@ cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, cudaStream_t 
   int64_t blocks = 1;
   cudaError_t e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
-  e = grid_for(coop_walk_kernel<T>, smem, (int64_t)P.num_items * 32, sms, &blocks);
+  e = grid_for(coop_walk_kernel<T, false>, smem, (int64_t)P.num_items * 32, sms, &blocks);
   if (e != cudaSuccess) return e;
-  coop_walk_kernel<T><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
+  coop_walk_kernel<T, false><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
   e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (P.scalar_walk) {
+    e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    e = grid_for(coop_walk_kernel<T, true>, smem, (int64_t)P.num_items * 32, sms, &blocks);
+    if (e != cudaSuccess) return e;
+    coop_walk_kernel<T, true><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess || !any_dynamic) return e;
   e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
@@ -1314,7 +1629,7 @@ cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32,
   if (e != cudaSuccess) return e;
   e = u32 ? launch_walk_t<uint32_t>(P, end_src, st, sms, any_dynamic)
           : launch_walk_t<int64_t>(P, end_src, st, sms, any_dynamic);
-  if (launches) *launches += any_dynamic ? 2 : 1;
+  if (launches) *launches += 1 + (any_dynamic ? 1 : 0) + (P.scalar_walk ? 1 : 0);
   return e;
 }
 

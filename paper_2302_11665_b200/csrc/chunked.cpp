@@ -223,6 +223,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.fix_flag = ctx->c_flag.as<uint32_t>();
   P.stage_updates = out.stage_updates;
   P.walked = ctx->profiling ? ctx->d_walked.as<unsigned long long>() : nullptr;
+  P.scalar_walk = ctx->scalar_walk ? 1 : 0;
   P.spec_state = opt ? opt->spec_state : nullptr;
   P.spec_row = opt ? opt->spec_row : nullptr;
   P.spec_cand = opt ? opt->spec_cand : nullptr;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <new>
@@ -268,6 +269,7 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   if (!ctx) return asim_fail(nullptr, ASIM_ENOMEM, "host allocation failed");
   ctx->device = cuda_device;
   ctx->sms = prop.multiProcessorCount;
+  if (const char* sw = getenv("ASIM_SCALAR_WALK")) ctx->scalar_walk = sw[0] != '0';
   *out = ctx;
   return ASIM_OK;
 }

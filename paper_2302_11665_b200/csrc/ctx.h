@@ -82,6 +82,7 @@ struct asim_ctx {
   DBuf c_pub;
   DBuf c_spm, c_fpm, c_sbusy, c_fbusy;  // fast-heuristic statistics rows
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
+  bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
 
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;

@@ -223,3 +223,33 @@ def test_uniform_config_with_empty_group_slot(sim):
         finally:
             sim.set_path(0)
             sim.set_chunk_size(4096)
+
+
+@pytest.fixture(scope="module")
+def sim_coop():
+    """A context whose walk uses only the cooperative walker (the scalar
+    register walker switched off), so both walkers stay covered."""
+    import os
+    from paper_2302_11665_b200 import Simulator
+    old = os.environ.get("ASIM_SCALAR_WALK")
+    os.environ["ASIM_SCALAR_WALK"] = "0"
+    try:
+        s = Simulator(0)
+    finally:
+        if old is None:
+            del os.environ["ASIM_SCALAR_WALK"]
+        else:
+            os.environ["ASIM_SCALAR_WALK"] = old
+    yield s
+    s.close()
+
+
+@pytest.mark.parametrize("S", [1, 2, 8])
+@pytest.mark.parametrize("u32", [True, False])
+def test_stage_classes_cooperative_walker(sim_coop, S, u32):
+    test_stage_classes(sim_coop, S, u32)
+
+
+def test_overload_chains_cooperative_walker(sim_coop):
+    test_overload_rerun_chains(sim_coop)
+    test_search_same_on_both_paths(sim_coop)

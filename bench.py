@@ -49,6 +49,8 @@ def parse():
                     help="Alg. 1 inside Alg. 2 (the headline) or the fast heuristic of P:737")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prune", action="store_true",
+                    help="disable exact run pruning (capacity bound, include/asim.h)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -239,7 +241,8 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def one_search(s):
-        with s.search_handle(dedup=args.dedup, fast=args.search == "fast") as sh:
+        with s.search_handle(dedup=args.dedup, fast=args.search == "fast",
+                             prune=not args.no_prune) as sh:
             if args.search == "fast":
                 sh.run(stream=stream)  # every rank computes the whole heuristic
             else:
@@ -338,6 +341,8 @@ def main():
                         simulated_per_search=res.evaluated, memo_hits=res.memo_hits,
                         dedup=bool(args.dedup), search=args.search,
                         best_run=res.best_run, best_attainment=res.best_good / max(N, 1),
+                        prune=not args.no_prune,
+                        pruned_runs=sum(1 for r in res.runs if r["pruned_at"] >= 0),
                         l2="flushed between timed steps (256 MB write)",
                         parallelism=f"candidate-sharded x{world}"),
             gpu_launches=int(launches),

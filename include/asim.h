@@ -99,6 +99,9 @@ typedef struct {
   int64_t stage_updates;
   int64_t request_evals;
   int64_t chunk_reruns;  /* chunks re-simulated because their start state was wrong */
+  int64_t walk_candidates;      /* candidates (items for mixed configs) that walked >= 1 chunk */
+  int64_t walk_critical_chunks; /* sum over walk launches of the longest single walk (chunks):
+                                   the sequential critical path of the walk pass */
 } asim_stats;
 asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
 asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);
@@ -289,6 +292,19 @@ double asim_attainment(int64_t good, int64_t n);
  * the first of them and the run's best updates on strict '>'; the run stops
  * when no member has a feasible addition.  k = 1 is the search above.  Runs
  * (asim_search_num_runs / run_info) are Alg. 2 runs, not beam members.
+ * Exact run pruning (spec->prune = 1; not in the paper): every run group r
+ * gets a capacity bound UB(r) on the good of ANY selection on its groups --
+ * an accepted request of model m on a group with config p occupies the
+ * group's stages for sum_k d_k(m, p) within [first arrival, last arrival +
+ * max SLO], so sum_m x_m * floor(min_p sum_k d_k(m, p) / s_p) <= G * H with
+ * x_m <= requests of m (0 for models that fit on none of the groups or lie
+ * outside the run's bucket), bounded by the floor of the fractional
+ * knapsack.  Before each step, a group whose UB is below the best good some
+ * group of its competition (all runs; the bucket job with buckets = 1)
+ * already reached stops: it can never be the first best, so best_run,
+ * best_good and the placement are exactly those of prune = 0.  A pruned
+ * run's asim_search_run_info reports its best up to the step it stopped
+ * (asim_search_run_pruned).
  * Errors (asim_search_create): ASIM_EINVAL null latency / bad ratio or bound;
  * fast = 1 with beam > 1;
  * ASIM_ERANGE latency outside [1, 2^60], a run with > ASIM_MAX_GROUPS groups,
@@ -307,6 +323,7 @@ typedef struct {
   int64_t bound_num, bound_den;  /* discrepancy bound (SPEC: 3 / 1) */
   const int64_t* model_latency_ns; /* [M] host; single-device latency (Table 1) */
   int32_t beam;                  /* Alg. 1 beam size k (<= 1 means 1; see below) */
+  int32_t prune;                 /* 1 = exact run pruning (see below) */
 } asim_search_spec;
 
 typedef struct {
@@ -335,6 +352,9 @@ asim_status asim_search_run_info(const asim_search* s, int32_t run, int32_t* num
                                  int32_t* group_cfg, uint64_t* host_mask, int64_t* best_good,
                                  int64_t* steps);
 int32_t asim_search_num_runs(const asim_search* s);
+/* Step at which run r was pruned (spec->prune), -1 if it never was or r is
+ * out of range. */
+int64_t asim_search_run_pruned(const asim_search* s, int32_t run);
 
 /* Bucketed result (spec->buckets = 1), after the search finished.  Arrays are
  * caller-provided host arrays of M entries (a partition has <= M buckets).

@@ -48,14 +48,15 @@ class asim_results(ctypes.Structure):
 
 class asim_stats(ctypes.Structure):
     _fields_ = [("launches", i64), ("sim_launches", i64), ("sim_ms", ctypes.c_double),
-                ("stage_updates", i64), ("request_evals", i64), ("chunk_reruns", i64)]
+                ("stage_updates", i64), ("request_evals", i64), ("chunk_reruns", i64),
+                ("walk_candidates", i64), ("walk_critical_chunks", i64)]
 
 
 class asim_search_spec(ctypes.Structure):
     _fields_ = [("num_runs", i32), ("run_num_groups", vp), ("run_group_cfg", vp),
                 ("dedup", i32), ("fast", i32), ("buckets", i32), ("max_buckets", i32),
                 ("ratio_num", i64), ("ratio_den", i64), ("bound_num", i64), ("bound_den", i64),
-                ("model_latency_ns", vp), ("beam", i32)]
+                ("model_latency_ns", vp), ("beam", i32), ("prune", i32)]
 
 
 class asim_bucket_result(ctypes.Structure):
@@ -112,6 +113,7 @@ asim_search_result_get = _bind("asim_search_result_get", i32, [vp, _P(asim_searc
 asim_search_run_info = _bind("asim_search_run_info", i32,
                              [vp, i32, _P(i32), vp, vp, _P(i64), _P(i64)])
 asim_search_num_runs = _bind("asim_search_num_runs", i32, [vp])
+asim_search_run_pruned = _bind("asim_search_run_pruned", i64, [vp, i32])
 asim_search_buckets_get = _bind("asim_search_buckets_get", i32, [vp, _P(asim_bucket_result)])
 
 EXPORTED = [n for n in dir() if n.startswith("asim_") and callable(globals()[n])

@@ -132,7 +132,8 @@ class Simulator:
         self._check(A.asim_get_stats(self.h, ctypes.byref(s)))
         return dict(launches=s.launches, sim_launches=s.sim_launches, sim_ms=s.sim_ms,
                     stage_updates=s.stage_updates, request_evals=s.request_evals,
-                    chunk_reruns=s.chunk_reruns)
+                    chunk_reruns=s.chunk_reruns, walk_candidates=s.walk_candidates,
+                    walk_critical_chunks=s.walk_critical_chunks)
 
     def set_chunk_size(self, min_requests: int) -> None:
         self._check(A.asim_set_chunk_size(self.h, int(min_requests)))
@@ -201,11 +202,11 @@ class Simulator:
 
     # ------------------------------------------------------------- search
     def search_handle(self, runs=None, dedup=True, fast=False, buckets=None,
-                      beam=1) -> "SearchHandle":
-        return SearchHandle(self, runs, dedup, fast, buckets, beam)
+                      beam=1, prune=True) -> "SearchHandle":
+        return SearchHandle(self, runs, dedup, fast, buckets, beam, prune)
 
     def search_buckets(self, latency, ratio=4, bound=3, max_buckets=0, fast=False, dedup=True,
-                       pg=None, stream=None, beam=1) -> BucketResult:
+                       pg=None, stream=None, beam=1, prune=True) -> BucketResult:
         """Alg. 2 with model and device buckets (include/asim.h).
         latency[m]: single-device latency in ns; ratio / bound: ints or
         fractions.Fraction (threshold 4x and discrepancy bound 3x by default)."""
@@ -215,7 +216,7 @@ class Simulator:
 
         b = dict(latency=_host(latency, np.int64), ratio=Fraction(ratio), bound=Fraction(bound),
                  max_buckets=int(max_buckets))
-        with self.search_handle(None, dedup, fast, b, beam) as sh:
+        with self.search_handle(None, dedup, fast, b, beam, prune) as sh:
             if fast:
                 sh.run(stream=stream)
             else:
@@ -234,7 +235,7 @@ class Simulator:
                                 r.partitions, r.considered, res)
 
     def search(self, runs=None, dedup=True, pg=None, stream=None, fast=False,
-               beam=1) -> SearchResult:
+               beam=1, prune=True) -> SearchResult:
         """Full Alg. 2 (single bucket) / Alg. 1 search.  With a
         torch.distributed process group the step candidates shard across its
         ranks (dist.run_search).  fast=True runs the fast heuristic of P:737
@@ -242,7 +243,7 @@ class Simulator:
         computes it whole -- there is nothing to shard)."""
         from . import dist
 
-        with self.search_handle(runs, dedup, fast, None, beam) as sh:
+        with self.search_handle(runs, dedup, fast, None, beam, prune) as sh:
             if fast:
                 sh.run(stream=stream)
             else:
@@ -254,12 +255,13 @@ class SearchHandle:
     """Stepwise search protocol of include/asim.h (prepare / evaluate / apply)."""
 
     def __init__(self, sim: Simulator, runs=None, dedup=True, fast=False, buckets=None,
-                 beam=1):
+                 beam=1, prune=True):
         self.sim = sim
         spec = A.asim_search_spec()
         spec.dedup = int(bool(dedup))
         spec.fast = int(bool(fast))
         spec.beam = int(beam)
+        spec.prune = int(bool(prune))
         self._keep = ()
         if buckets is not None:
             lat = buckets["latency"]
@@ -328,7 +330,8 @@ class SearchHandle:
             self.sim._check(A.asim_search_run_info(self.h, i, ctypes.byref(ng), _ptr(rc), _ptr(rm),
                                                    ctypes.byref(bg), ctypes.byref(stp)))
             runs.append(dict(num_groups=ng.value, group_cfg=rc[:ng.value].copy(), host_mask=rm,
-                             best_good=bg.value, steps=stp.value))
+                             best_good=bg.value, steps=stp.value,
+                             pruned_at=int(A.asim_search_run_pruned(self.h, i))))
         return SearchResult(r.best_run, r.best_good, r.num_groups, cfg[:r.num_groups].copy(),
                             mask, r.steps, r.candidates, r.evaluated, r.request_evals,
                             r.memo_hits, runs)

@@ -113,7 +113,7 @@ struct ChunkParams {
   const int64_t* spec_state;
   const int32_t* spec_row;     // [B] row of base b in spec_state
   int32_t state_stride;        // slots per boundary row of spec_state / published states
-  unsigned long long* walked;  // nullable statistics: chunks re-simulated by the walk pass
+  unsigned long long* walked;  // nullable statistics [4]: chunks walked, walking candidates, longest walk of this run, sum of longest walks
   // Per-candidate speculation rows (nullable): spec_cand[(c * J + j) * state_stride + k],
   // c = batch index; when set they replace spec_state for the candidate's own
   // trajectory (spec_state still supplies out-of-component slots when publishing).
@@ -128,6 +128,7 @@ struct ChunkParams {
   int64_t* fix_busy;
   int64_t stat_C;
   int32_t scalar_walk;  // 1 = small components walk with the register-state scalar walker
+  int64_t walk_log;     // diagnostics (ASIM_WALK_LOG=cycles): printf every walk longer than this
 };
 
 // Per-candidate speculation rows for the search (see search.cpp):
@@ -170,7 +171,14 @@ cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32,
 // Pass 3: re-simulate every chunk whose start state was wrong (per lane) and
 // record in bit `lane` of end_src[j * items + item] whether that lane's true
 // end of chunk j is in spec_end (0) or fix_end (1).
+// The three walkers run concurrently: fork from `main` onto the side
+// streams, join back before returning (stream-ordered for the caller).
+struct WalkStreams {
+  cudaStream_t main;
+  cudaStream_t side[2];
+  cudaEvent_t fork, join[2];
+};
 cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32, bool any_dynamic,
-                              cudaStream_t st, int sms, int64_t* launches);
+                              const WalkStreams& ws, int sms, int64_t* launches);
 
 }  // namespace asim

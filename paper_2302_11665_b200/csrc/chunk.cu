@@ -96,7 +96,22 @@ struct WarpMem {
   uint8_t* rel;    // [M]   some lane of the unit hosts model m
   uint8_t* sgrp;   // [128] group of each stage slot
   uint64_t* hmask; // [M]   hosting groups of model m (bit set; warp-cooperative walker)
+  unsigned char* tile;  // [kTileBytes] one trace tile's per-request fields (scalar walker)
 };
+
+// The scalar walker stages a tile's per-request fields here: every lane
+// writes its request, then the per-request loop reads them with broadcast
+// loads whose addresses do not depend on the simulation state.
+template <typename T>
+struct alignas(16) TileReq {
+  T ar;          // arrival, relative to the epoch
+  T lim;         // accept iff the last departure <= lim (= ar + slo - tail, saturated)
+  T d0;          // first stage latency of the request's model (S == 1)
+  T tl;          // tail
+  uint32_t hm;   // compact hosting mask (0: no host in the component, or never acceptable)
+  int32_t m;     // model
+};
+constexpr size_t kTileBytes = 32 * sizeof(TileReq<int64_t>);
 
 __host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, bool dual) {
   size_t b = (size_t)slots_max * 32 * tsz * (dual ? 2 : 1);
@@ -105,6 +120,8 @@ __host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, b
   b += (size_t)M * 64 + ((M + 15) & ~15) + 128;
   b = (b + 15) & ~size_t(15);
   b += (size_t)M * 8;
+  b = (b + 15) & ~size_t(15);
+  b += kTileBytes;
   return (b + 15) & ~size_t(15);
 }
 
@@ -139,6 +156,9 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   off += 128;
   off = (off + 15) & ~size_t(15);
   w.hmask = reinterpret_cast<uint64_t*>(base + off);
+  off += M * 8;
+  off = (off + 15) & ~size_t(15);
+  w.tile = base + off;
   return w;
 }
 
@@ -764,7 +784,11 @@ __global__ void __launch_bounds__(kWarps * 32) walk_kernel(ChunkParams P, uint32
       start_ok = eq;
       __syncwarp();
     }
-    if (P.walked && lane == 0 && walked) atomicAdd(P.walked, walked);
+    if (P.walked && lane == 0 && walked) {
+      atomicAdd(P.walked, walked);
+      atomicAdd(P.walked + 1, 1ull);
+      atomicMax(P.walked + 2, walked);
+    }
   }
 }
 
@@ -834,7 +858,7 @@ __device__ __forceinline__ void coop_range(const ChunkParams& P, const WarpMem<T
 #pragma unroll
       for (int k = 0; k < S; ++k) occl += (int64_t)w.d[ml * kSTab + k];
     }
-    {
+    if (P.stage_updates) {  // statistics only (warp-uniform)
       const bool rel = (todo >> lane) & 1u;
       upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popcll(hml) : 0u) * S;
     }
@@ -1113,10 +1137,17 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
       busy_row = P.fix_busy + row * P.bt.G;
     }
     int64_t good = 0, sum = 0;
+    // request fields one tile ahead (the tile loads leave the per-request chain)
+    int64_t al_n = i_begin + lane < i_end ? P.tr.arrival[i_begin + lane] : 0;
+    int ml_n = i_begin + lane < i_end ? (int)P.tr.model[i_begin + lane] : 0;
     for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
       const bool valid = i0 + lane < i_end;
-      const int64_t al = valid ? P.tr.arrival[i0 + lane] : 0;
-      const int ml = valid ? (int)P.tr.model[i0 + lane] : 0;
+      const int64_t al = al_n;
+      const int ml = ml_n;
+      if (i0 + 32 + lane < i_end) {
+        al_n = P.tr.arrival[i0 + 32 + lane];
+        ml_n = (int)P.tr.model[i0 + 32 + lane];
+      }
       unsigned todo = __ballot_sync(FULL, valid && ((kmask >> (ml & 63)) & 1ull));
       if (!todo) continue;
       bool per_req = false;
@@ -1135,9 +1166,80 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
       const T arl = (T)(al - E);
       const uint32_t hml = hmc[ml];
       const T tll = w.tail[ml], sll = w.slo[ml];
-      {
+      if (P.stage_updates) {  // statistics only (warp-uniform)
         const bool rel = (todo >> lane) & 1u;
         upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popc(hml) : 0u) * S;
+      }
+      if (!per_req && !pm_row) {
+        // Dense tile: all 32 requests in a fixed order.  Each lane stages its
+        // request's fields in shared memory; the per-request loop reads them
+        // with broadcast loads that do not depend on the state, so they issue
+        // ahead of the dependent chain.  A request outside the component has
+        // no host here (hm = 0) and leaves the state untouched, exactly like
+        // a rejection.  Accept iff the last departure x satisfies
+        // x + tail - a <= slo, i.e. x <= lim = a + slo - tail (never when
+        // slo < tail, since x >= a).
+        TileReq<T>* tq = reinterpret_cast<TileReq<T>*>(w.tile);
+        {
+          TileReq<T> q;
+          q.ar = arl;
+          q.hm = (((todo >> lane) & 1u) && sll >= tll) ? hml : 0u;
+          q.lim = 0;
+          if (sll >= tll) {  // saturating: an unbounded SLO must not wrap
+            const T room = sll - tll;
+            q.lim = room > (T)(TT<T>::maxv() - 1 - arl) ? (T)(TT<T>::maxv() - 1) : (T)(arl + room);
+          }
+          q.d0 = w.d[ml * kSTab];
+          q.tl = tll;
+          q.m = ml;
+          tq[lane] = q;
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (int jj = 0; jj < 32; ++jj) {
+          const TileReq<T> q = tq[jj];
+          T d[S];
+          if constexpr (S == 1) {
+            d[0] = q.d0;
+          } else {
+#pragma unroll
+            for (int k = 0; k < S; ++k) d[k] = w.d[q.m * kSTab + k];
+          }
+          T y[R];
+          T val[NG];
+          uint32_t oh[NG];  // one-hot winner (an index would turn the commit into local memory)
+#pragma unroll
+          for (int i = 0; i < NG; ++i) {
+            T x = q.ar;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+              x = tmax(x, v[i * S + k]) + d[k];
+              y[i * S + k] = x;
+            }
+            val[i] = (NG == 1 || ((q.hm >> i) & 1u)) ? x : TT<T>::maxv();
+            oh[i] = 1u << i;
+          }
+          // argmin, lowest index on ties (blocks of ascending indices, C1)
+#pragma unroll
+          for (int st = 1; st < NG; st <<= 1)
+#pragma unroll
+            for (int i = 0; i + st < NG; i += 2 * st) {
+              const bool p = val[i + st] < val[i];
+              val[i] = p ? val[i + st] : val[i];
+              oh[i] = p ? oh[i + st] : oh[i];
+            }
+          const bool acc = (NG > 1 || (q.hm & 1u)) && val[0] <= q.lim;
+          const uint32_t win = acc ? oh[0] : 0u;
+#pragma unroll
+          for (int i = 0; i < NG; ++i)
+#pragma unroll
+            for (int k = 0; k < S; ++k)
+              v[i * S + k] = (win & (1u << i)) ? y[i * S + k] : v[i * S + k];
+          good += acc ? 1 : 0;
+          sum += acc ? (int64_t)(val[0] - q.ar) + (int64_t)q.tl : 0;
+        }
+        __syncwarp();
+        continue;
       }
       while (todo) {
         const int jj = __ffs(todo) - 1;
@@ -1270,38 +1372,41 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
   }
 }
 
+// Does candidate c's component fit the scalar walker (NG * S <= kScalarSlots)?
+// Its per-request work grows with NG * S in every lane; larger components
+// go to the cooperative walker, whose per-lane work does not.
+constexpr int kScalarSlots = 16;
+
 template <typename T, int S>
 __device__ __forceinline__ bool scalar_dispatch_ng(const ChunkParams& P, const WarpMem<T>& w,
                                                    const ItemDesc& it, int item, int cl, int lane,
                                                    uint32_t* end_src, unsigned long long& walked,
                                                    unsigned long long& upd, int ng) {
-  // NG = the next power of two >= ng, with NG * S <= 32
+  // NG = the next power of two >= ng, with NG * S <= kScalarSlots
+  constexpr int K = kScalarSlots;
   if (ng <= 1) {
     scalar_candidate<T, S, 1>(P, w, it, item, cl, lane, end_src, walked, upd);
-  } else if (ng <= 2 && 2 * S <= 32) {
-    scalar_candidate<T, S, (2 * S <= 32 ? 2 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
-  } else if (ng <= 4 && 4 * S <= 32) {
-    scalar_candidate<T, S, (4 * S <= 32 ? 4 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
-  } else if (ng <= 8 && 8 * S <= 32) {
-    scalar_candidate<T, S, (8 * S <= 32 ? 8 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
-  } else if (ng <= 16 && 16 * S <= 32) {
-    scalar_candidate<T, S, (16 * S <= 32 ? 16 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
-  } else if (ng <= 32 && S == 1) {
-    scalar_candidate<T, S, (S == 1 ? 32 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 2 && 2 * S <= K) {
+    scalar_candidate<T, S, (2 * S <= K ? 2 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 4 && 4 * S <= K) {
+    scalar_candidate<T, S, (4 * S <= K ? 4 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 8 && 8 * S <= K) {
+    scalar_candidate<T, S, (8 * S <= K ? 8 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
+  } else if (ng <= 16 && 16 * S <= K) {
+    scalar_candidate<T, S, (16 * S <= K ? 16 : 1)>(P, w, it, item, cl, lane, end_src, walked, upd);
   } else {
     return false;
   }
   return true;
 }
 
-// Does candidate c's component fit the scalar walker (NG * S <= 32)?
 __device__ __forceinline__ bool scalar_fits(const ChunkParams& P, const ItemDesc& it, int64_t c) {
   const int ngroups = it.slots / it.S;
   const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
   const uint64_t gmask = (P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all;
   int ng = __popcll(gmask), np2 = 1;
   while (np2 < ng) np2 <<= 1;
-  return np2 * it.S <= 32;
+  return np2 * it.S <= kScalarSlots;
 }
 
 template <typename T>
@@ -1378,10 +1483,24 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
       load_base<T>(P, it, w, lane);
       cur_base = it.base;
     }
+    const unsigned long long w0 = walked, u0 = upd;
+    const long long t0 = clock64();
     if constexpr (SCALAR)
       scalar_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
     else
       coop_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
+    if (P.walked && lane == 0 && walked > w0) {  // statistics: walking candidates, longest walk
+      atomicAdd(P.walked + 1, 1ull);
+      atomicMax(P.walked + 2, walked - w0);
+      const long long cyc = clock64() - t0;
+      if (P.walk_log > 0 && cyc > P.walk_log) {
+        const int64_t c = (int64_t)it.first + cl;
+        printf("walk scalar=%d S=%d slots=%d ng=%d models=%d chunks=%llu cycles=%lld upd=%llu\n",
+               (int)SCALAR, it.S, it.slots,
+               __popcll(P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull),
+               __popcll(P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull), walked - w0, cyc, upd - u0);
+      }
+    }
   }
   if (lane == 0) {
     if (P.walked && walked) atomicAdd(P.walked, walked);
@@ -1463,6 +1582,10 @@ __global__ void __launch_bounds__(kWarps * 32) fast_stats_kernel(ChunkParams P, 
 // good[c] = sum_j spec_good[j][c] + sum_{j>=1} fix_good[j][c] (same for sums)
 __global__ void chunk_reduce_kernel(ChunkParams P, DevOut out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0 && P.walked) {  // statistics: fold this run's longest walk (stream-ordered after it)
+    P.walked[3] += P.walked[2];
+    P.walked[2] = 0;
+  }
   if (t >= (int64_t)P.num_items * 32) return;
   const int item = (int)(t >> 5), lane = (int)(t & 31);
   const ItemDesc it = P.items[item];
@@ -1579,33 +1702,46 @@ cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
   return cudaGetLastError();
 }
 
+// The walkers take disjoint candidates (coop: uniform configs not taken by
+// the scalar walker; scalar: small uniform components; item walker: mixed
+// configs), so they run concurrently: the walk's critical path is the
+// longest single walk, not the sum of the three kernels' tails.
 template <typename T>
-cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, cudaStream_t st, int sms,
+cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, const WalkStreams& ws, int sms,
                           bool any_dynamic) {
   const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
   int64_t blocks = 1;
-  cudaError_t e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
+  cudaError_t e = cudaMemsetAsync(P.counter, 0, 3 * sizeof(uint32_t), ws.main);
   if (e != cudaSuccess) return e;
+  const bool fork = P.scalar_walk || any_dynamic;
+  if (fork && (e = cudaEventRecord(ws.fork, ws.main)) != cudaSuccess) return e;
   e = grid_for(coop_walk_kernel<T, false>, smem, (int64_t)P.num_items * 32, sms, &blocks);
   if (e != cudaSuccess) return e;
-  coop_walk_kernel<T, false><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  coop_walk_kernel<T, false><<<(unsigned)blocks, kWarps * 32, smem, ws.main>>>(P, end_src);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (P.scalar_walk) {
-    e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
-    if (e != cudaSuccess) return e;
+    ChunkParams Q = P;
+    Q.counter = P.counter + 1;
+    if ((e = cudaStreamWaitEvent(ws.side[0], ws.fork, 0)) != cudaSuccess) return e;
     e = grid_for(coop_walk_kernel<T, true>, smem, (int64_t)P.num_items * 32, sms, &blocks);
     if (e != cudaSuccess) return e;
-    coop_walk_kernel<T, true><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
-    e = cudaGetLastError();
+    coop_walk_kernel<T, true><<<(unsigned)blocks, kWarps * 32, smem, ws.side[0]>>>(Q, end_src);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(ws.join[0], ws.side[0])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ws.main, ws.join[0], 0)) != cudaSuccess) return e;
   }
-  if (e != cudaSuccess || !any_dynamic) return e;
-  e = cudaMemsetAsync(P.counter, 0, sizeof(uint32_t), st);
-  if (e != cudaSuccess) return e;
-  e = grid_for(walk_kernel<T>, smem, P.num_items, sms, &blocks);
-  if (e != cudaSuccess) return e;
-  walk_kernel<T><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P, end_src);
-  return cudaGetLastError();
+  if (any_dynamic) {
+    ChunkParams Q = P;
+    Q.counter = P.counter + 2;
+    if ((e = cudaStreamWaitEvent(ws.side[1], ws.fork, 0)) != cudaSuccess) return e;
+    e = grid_for(walk_kernel<T>, smem, P.num_items, sms, &blocks);
+    if (e != cudaSuccess) return e;
+    walk_kernel<T><<<(unsigned)blocks, kWarps * 32, smem, ws.side[1]>>>(Q, end_src);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(ws.join[1], ws.side[1])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ws.main, ws.join[1], 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -1624,11 +1760,11 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
 }
 
 cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32, bool any_dynamic,
-                              cudaStream_t st, int sms, int64_t* launches) {
-  cudaError_t e = cudaMemsetAsync(end_src, 0, (size_t)P.J * P.num_items * 4, st);
+                              const WalkStreams& ws, int sms, int64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(end_src, 0, (size_t)P.J * P.num_items * 4, ws.main);
   if (e != cudaSuccess) return e;
-  e = u32 ? launch_walk_t<uint32_t>(P, end_src, st, sms, any_dynamic)
-          : launch_walk_t<int64_t>(P, end_src, st, sms, any_dynamic);
+  e = u32 ? launch_walk_t<uint32_t>(P, end_src, ws, sms, any_dynamic)
+          : launch_walk_t<int64_t>(P, end_src, ws, sms, any_dynamic);
   if (launches) *launches += 1 + (any_dynamic ? 1 : 0) + (P.scalar_walk ? 1 : 0);
   return e;
 }

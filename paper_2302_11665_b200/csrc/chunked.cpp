@@ -21,7 +21,7 @@ bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim:
   if (out.good_per_model || out.busy) return false;  // per-model / per-group outputs: sim.cu
   if (hb.slots > ASIM_MAX_SLOTS) return false;
   const size_t M = (size_t)ctx->hp.M;
-  const size_t per_warp = (size_t)hb.slots * 32 * 8 * 2 + M * (8 + 8 * (kSTab + 2)) + 256;
+  const size_t per_warp = (size_t)hb.slots * 32 * 8 * 2 + M * (8 + 8 * (kSTab + 2)) + 256 + 1536;
   return 4 * per_warp <= 220 * 1024;
 }
 
@@ -224,6 +224,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.stage_updates = out.stage_updates;
   P.walked = ctx->profiling ? ctx->d_walked.as<unsigned long long>() : nullptr;
   P.scalar_walk = ctx->scalar_walk ? 1 : 0;
+  P.walk_log = ctx->walk_log;
   P.spec_state = opt ? opt->spec_state : nullptr;
   P.spec_row = opt ? opt->spec_row : nullptr;
   P.spec_cand = opt ? opt->spec_cand : nullptr;
@@ -269,7 +270,9 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 2");
     // ---- pass 3: walk the chunks whose start state was wrong (exact chains)
-    e = asim::launch_chunk_walk(P, end_src, u32, any_dynamic, st, ctx->sms, &ctx->launches);
+    const asim::WalkStreams ws{st, {ctx->side[0], ctx->side[1]}, ctx->ev_fork,
+                               {ctx->ev_join[0], ctx->ev_join[1]}};
+    e = asim::launch_chunk_walk(P, end_src, u32, any_dynamic, ws, ctx->sms, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk walk");
   } else {
     e = cudaMemsetAsync(end_src, 0, J * I * 4, st);

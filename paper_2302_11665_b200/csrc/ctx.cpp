@@ -270,6 +270,20 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   ctx->device = cuda_device;
   ctx->sms = prop.multiProcessorCount;
   if (const char* sw = getenv("ASIM_SCALAR_WALK")) ctx->scalar_walk = sw[0] != '0';
+  if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
+  {
+    DeviceGuard dg(cuda_device);
+    e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      asim_destroy(ctx);
+      return asim_fail(nullptr, ASIM_ECUDA, std::string("side streams: ") + cudaGetErrorString(e));
+    }
+  }
   *out = ctx;
   return ASIM_OK;
 }
@@ -290,6 +304,11 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
                     &ctx->c_fbusy};
     for (DBuf* b : bufs) b->release();
+    for (int i = 0; i < 2; ++i) {
+      if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
+      if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   }
   delete ctx;
 }
@@ -314,7 +333,7 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   ctx->request_evals = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 8);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 8);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return asim_cuda(ctx, e, "reset stats");
   }
@@ -340,9 +359,9 @@ asim_status asim_set_profiling(asim_ctx* ctx, int32_t on) {
   DeviceGuard dg(ctx->device);
   if (on && !ctx->d_counter.p) {
     cudaError_t e = ctx->d_counter.ensure(8);
-    if (e == cudaSuccess) e = ctx->d_walked.ensure(8);
+    if (e == cudaSuccess) e = ctx->d_walked.ensure(32);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 8);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 8);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "profiling counter");
   }
   ctx->profiling = on != 0;
@@ -362,10 +381,10 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
     cudaEventDestroy(ev.second);
   }
   ctx->events.clear();
-  unsigned long long upd = 0, walked = 0;
+  unsigned long long upd = 0, walked[4] = {0, 0, 0, 0};
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemcpy(&upd, ctx->d_counter.p, 8, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess) e = cudaMemcpy(&walked, ctx->d_walked.p, 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(walked, ctx->d_walked.p, 32, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "stats counter");
   }
   out->launches = ctx->launches;
@@ -373,7 +392,9 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->sim_ms = ctx->sim_ms;
   out->stage_updates = (int64_t)upd;
   out->request_evals = ctx->request_evals;
-  out->chunk_reruns = (int64_t)walked;
+  out->chunk_reruns = (int64_t)walked[0];
+  out->walk_candidates = (int64_t)walked[1];
+  out->walk_critical_chunks = (int64_t)walked[3];
   return ASIM_OK;
 }
 
@@ -481,6 +502,7 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload trace");
   ctx->n = n;
   ctx->max_arrival = n ? a[n - 1] : 0;
+  ctx->min_arrival = n ? a[0] : 0;
   ctx->model_n.assign(ctx->hp.M, 0);
   for (int64_t i = 0; i < n; ++i) ++ctx->model_n[m[i]];
   ctx->has_trace = true;

@@ -57,6 +57,7 @@ struct asim_ctx {
   bool has_trace = false;
   int64_t n = 0;
   int64_t max_arrival = 0;
+  int64_t min_arrival = 0;
   std::vector<int64_t> model_n;  // [M] requests per model in the trace
   DBuf d_arrival, d_model;
 
@@ -70,6 +71,9 @@ struct asim_ctx {
   DBuf d_walked;   // unsigned long long walked-chunk counter
 
   int sms = 148;
+  // side streams / events of the concurrent walk pass (created by asim_create)
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   // chunked path buffers (chunked.cpp)
   DBuf c_items, c_begin, c_spec_good, c_spec_sum, c_fix_good, c_fix_sum, c_spec_end, c_fix_end,
       c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_end_src;
@@ -82,6 +86,7 @@ struct asim_ctx {
   DBuf c_pub;
   DBuf c_spm, c_fpm, c_sbusy, c_fbusy;  // fast-heuristic statistics rows
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
+  int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
 
   // scratch for evaluate()

@@ -197,6 +197,11 @@ struct asim_search {
   std::vector<std::vector<std::vector<int32_t>>> partitions;
   std::vector<BucketJob> jobs;
   std::vector<BucketCombo> combos;
+  // exact run pruning (spec->prune): per run group a bound on the good of ANY
+  // selection on its groups, and the step at which it was pruned (-1: never)
+  bool prune = false;
+  std::vector<int64_t> gub;
+  std::vector<int64_t> gpruned;
   // statistics
   int64_t steps = 0, candidates = 0, evaluated = 0, memo_hits = 0, base_passes = 0;
   bool finished = false;
@@ -204,6 +209,10 @@ struct asim_search {
 
 // candidate memory is skipped when a step's rows would exceed this
 static constexpr size_t kMixBytesCap = size_t(6) << 30;
+
+static void prune_runs(asim_search* s);
+static int64_t run_capacity_bound(const asim_ctx* ctx, const Run& run);
+static const Run& group_run(const asim_search* s, int32_t gi);
 
 static asim_status sfail(asim_search* s, asim_status code, const std::string& m) {
   return asim_fail(s ? s->ctx : nullptr, code, m);
@@ -521,6 +530,11 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     s->runs.push_back(std::move(r));
   }
   s->stride = stride;
+  s->prune = spec->prune != 0;
+  s->gpruned.assign(s->ngroups, -1);
+  s->gub.assign(s->ngroups, 0);
+  if (s->prune)
+    for (int32_t gi = 0; gi < s->ngroups; ++gi) s->gub[gi] = run_capacity_bound(ctx, group_run(s, gi));
   s->J = std::max<int64_t>(1, std::min<int64_t>(1024, ctx->n / std::max<int64_t>(1, ctx->min_chunk)));
   {
     HostBatch probe_hb;
@@ -573,6 +587,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   s->eval_lo = s->eval_hi = 0;
   s->rows_uploaded = false;
   s->mixrows.clear();
+  prune_runs(s);
   int64_t full = 0;
   for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r) {
     Run& run = s->runs[r];
@@ -994,6 +1009,7 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
     if (rs) return rs;
     HostBatch hb;
     hb.G = G;
+    prune_runs(s);
     std::vector<int32_t> act, sim_b;
     for (int32_t r = 0; r < (int32_t)s->runs.size(); ++r) {
       Run& run = s->runs[r];
@@ -1190,6 +1206,90 @@ static void group_best(const asim_search* s, int32_t gi, int64_t* good,
 }
 static const Run& group_run(const asim_search* s, int32_t gi) { return s->runs[gi * s->beam]; }
 
+// Capacity bound on the good of ANY selection on a run's groups (exact run
+// pruning; not in the paper, results unchanged).  An accepted request of
+// model m on a group with config p occupies stage k of that group for
+// d_k(m, p), inside [first arrival, last arrival + max SLO] (it starts after
+// its arrival and its last stage ends before its deadline).  Summing the
+// per-stage constraints of a group and dividing by its stage count s:
+//   sum over accepted requests of c(m, p) <= H,  c(m, p) = sum_k d_k(m, p) / s,
+// so over the run's G groups sum_m x_m * min_p c(m, p) <= G * H with
+// 0 <= x_m <= n_m (requests of m in the trace; models that fit on none of the
+// groups, or lie outside the run's bucket, have x_m = 0).  The floor of the
+// fractional-knapsack optimum (cheapest models first) bounds sum_m x_m; the
+// costs are rounded down, which only loosens it.
+static int64_t run_capacity_bound(const asim_ctx* ctx, const Run& run) {
+  const HostProblem& hp = ctx->hp;
+  if (ctx->n == 0) return 0;
+  int64_t slo_max = 0;
+  std::vector<std::pair<int64_t, int32_t>> cost;  // (cost, model)
+  int64_t free_requests = 0;                      // models of cost 0: no capacity limit
+  for (int32_t m = 0; m < hp.M; ++m) {
+    if (!run.may_place(m) || ctx->model_n[m] == 0) continue;
+    int64_t c = -1;
+    for (int32_t p : run.cfg) {
+      const int64_t mb = hp.mem_at(m, p);
+      if (mb < 0 || mb > hp.budget) continue;
+      const int32_t st = hp.cfg_stages[p];
+      __int128 sum = 0;
+      for (int32_t k = 0; k < st; ++k) sum += hp.stage[((int64_t)m * hp.P + p) * hp.S + k];
+      const int64_t ck = (int64_t)(sum / st);
+      c = c < 0 ? ck : std::min(c, ck);
+    }
+    if (c < 0) continue;  // fits on none of the run's groups
+    slo_max = std::max(slo_max, hp.slo[m]);
+    if (c == 0) free_requests += ctx->model_n[m];
+    else cost.emplace_back(c, m);
+  }
+  std::sort(cost.begin(), cost.end());
+  const __int128 H = (__int128)ctx->max_arrival - ctx->min_arrival + slo_max;
+  __int128 cap = (__int128)run.G * H;
+  __int128 ub = free_requests;
+  for (const auto& cm : cost) {
+    const __int128 take = std::min<__int128>(ctx->model_n[cm.second], cap / cm.first);
+    ub += take;
+    cap -= take * cm.first;
+    if (take < ctx->model_n[cm.second]) break;
+  }
+  return (int64_t)std::min<__int128>(ub, ctx->n);
+}
+
+static void group_best(const asim_search* s, int32_t gi, int64_t* good,
+                       const std::vector<uint64_t>** mask, int64_t* steps);
+
+// Stop every run group whose capacity bound is below the best good another
+// group of its competition (all runs, or its bucket job) already reached: it
+// can never become the (first) best, so the search's result is unchanged.
+static void prune_runs(asim_search* s) {
+  if (!s->prune) return;
+  auto sweep = [&](const std::vector<int32_t>& grp) {
+    int64_t lb = 0;
+    for (int32_t gi : grp) {
+      int64_t g = 0, st = 0;
+      const std::vector<uint64_t>* mk = nullptr;
+      group_best(s, gi, &g, &mk, &st);
+      lb = std::max(lb, g);
+    }
+    for (int32_t gi : grp) {
+      if (s->gpruned[gi] >= 0 || s->gub[gi] >= lb) continue;
+      bool any = false;
+      for (int32_t k = 0; k < s->beam; ++k) {
+        Run& r = s->runs[(size_t)gi * s->beam + k];
+        any |= r.active;
+        r.active = false;
+      }
+      if (any) s->gpruned[gi] = s->steps;
+    }
+  };
+  if (s->bucketed) {
+    for (const auto& job : s->jobs) sweep(job.runs);
+  } else {
+    std::vector<int32_t> all(s->ngroups);
+    for (int32_t i = 0; i < s->ngroups; ++i) all[i] = i;
+    sweep(all);
+  }
+}
+
 // Bucketed outcome (reading C28): plm_i* per job = its first best run on
 // strict '>' (none if no run serves a request); combo good = sum over its
 // jobs; the first best combo on strict '>'.
@@ -1283,6 +1383,11 @@ asim_status asim_search_result_get(const asim_search* s, asim_search_result* out
   if (out->host_mask)
     for (int32_t m = 0; m < M; ++m) out->host_mask[m] = best >= 0 ? (*best_mask)[m] : 0;
   return ASIM_OK;
+}
+
+int64_t asim_search_run_pruned(const asim_search* s, int32_t run) {
+  if (!s || run < 0 || run >= (int32_t)s->gpruned.size()) return -1;
+  return s->gpruned[run];
 }
 
 asim_status asim_search_buckets_get(const asim_search* s, asim_bucket_result* out) {

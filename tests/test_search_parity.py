@@ -23,10 +23,14 @@ def _compare(sim, prob, tr, dedup_modes=(False, True)):
     ref = osearch.alg2(prob, tr)
     sim.set_problem(prob)
     sim.set_trace(tr.arrival_ns, tr.model)
-    for dedup in dedup_modes:
-        res = sim.search(dedup=dedup)
+    for dedup, prune in [(d, p) for d in dedup_modes for p in (False, True)]:
+        res = sim.search(dedup=dedup, prune=prune)
         assert len(res.runs) == len(ref["runs"])
         for r_gpu, r_ref in zip(res.runs, ref["runs"]):
+            if r_gpu["pruned_at"] >= 0:  # stopped early: provably never the best run
+                assert prune and r_ref["good"] < ref["good"]
+                assert r_gpu["best_good"] <= r_ref["good"]
+                continue
             assert r_gpu["best_good"] == r_ref["good"]
             np.testing.assert_array_equal(r_gpu["host_mask"], r_ref["placement"].host_mask)
             np.testing.assert_array_equal(r_gpu["group_cfg"], r_ref["placement"].group_cfg)
@@ -77,3 +81,24 @@ def test_search_small_chunks_base_speculation(sim, chunk):
         _compare(sim, prob, tr)
     finally:
         sim.set_chunk_size(4096)
+
+
+def test_pruning_stops_hopeless_runs(sim):
+    """Exact run pruning (include/asim.h, spec->prune): runs of large
+    intra-op-only groups cannot serve the trace (capacity bound below the
+    best good another run reaches), are stopped, and the result is that of
+    the unpruned search."""
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "MoE-2.4B") for i in range(3)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=5.0)
+    tr = traces.maf2_shaped(6, len(names), 60.0, 240.0)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    full = sim.search(dedup=False, prune=False)
+    pr = sim.search(dedup=False, prune=True)
+    assert (pr.best_run, pr.best_good) == (full.best_run, full.best_good)
+    np.testing.assert_array_equal(pr.host_mask, full.host_mask)
+    pruned = [i for i, r in enumerate(pr.runs) if r["pruned_at"] >= 0]
+    assert pruned, "expected at least one hopeless run on this instance"
+    for i in pruned:
+        assert full.runs[i]["best_good"] < full.best_good
+    assert pr.evaluated < full.evaluated

@@ -93,7 +93,14 @@ struct ChunkParams {
   const int64_t* chunk_begin;  // [J+1] request index boundaries
   int64_t theta;               // uint32 epoch threshold (see chunk.cu)
   int32_t slots_max;
+  int32_t hid_cap;             // bytes of each warp's hosting-list region (host: hid_cap_for)
   int32_t num_units;
+  // passes 1-2 visit items class by class (one stage count S per class) so
+  // the warps in flight run the same code: class c = items
+  // item_perm[class_off[c] .. class_off[c] + class_items[c]) (nullable: identity)
+  const int32_t* item_perm;
+  int32_t nclass;
+  int32_t class_off[8], class_items[8];
   uint32_t* counter;           // dynamic work counter
   int32_t* spec_good;          // [J][items*32]
   int64_t* spec_sum;
@@ -161,7 +168,7 @@ cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStr
 // Fast heuristic statistics: one warp per item (one candidate each, uniform
 // config, S class != 0) over the whole trace; writes good, sum, per-model good
 // and per-group busy into `out`.  fast_stats_smem: dynamic shared memory.
-size_t fast_stats_smem(int slots_max, int M, bool u32);
+size_t fast_stats_smem(int slots_max, int M, int hid_cap, bool u32);
 // out.good_per_model[c][m] / out.busy[c][g] = sum over chunks of the spec_*
 // and fix_* statistics rows (after launch_chunk_reduce).
 cudaError_t launch_chunk_stats_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,

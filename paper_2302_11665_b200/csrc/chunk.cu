@@ -113,15 +113,24 @@ struct alignas(16) TileReq {
 };
 constexpr size_t kTileBytes = 32 * sizeof(TileReq<int64_t>);
 
-__host__ __device__ inline size_t warp_bytes(int slots_max, int M, size_t tsz, bool dual) {
+// hid_cap: bytes of the hosting-list region = max(hostings of any base in the
+// launch, 4 M) -- the scalar walker reuses it as M uint32 compact masks.
+// The scalar walker's tile staging aliases the state region st0 (it keeps
+// its state in registers) when st0 is large enough.
+__host__ __device__ inline size_t tile_extra(int slots_max, size_t tsz) {
+  return (size_t)slots_max * 32 * tsz >= kTileBytes ? 0 : kTileBytes;
+}
+
+__host__ __device__ inline size_t warp_bytes(int slots_max, int M, int hid_cap, size_t tsz,
+                                             bool dual) {
   size_t b = (size_t)slots_max * 32 * tsz * (dual ? 2 : 1);
   b += (size_t)M * tsz * (kSTab + 2) + 64 * 4 + 2 * (size_t)(M + 1);
   b = (b + 15) & ~size_t(15);
-  b += (size_t)M * 64 + ((M + 15) & ~15) + 128;
+  b += (size_t)hid_cap + ((M + 15) & ~15) + 128;
   b = (b + 15) & ~size_t(15);
   b += (size_t)M * 8;
   b = (b + 15) & ~size_t(15);
-  b += kTileBytes;
+  b += tile_extra(slots_max, tsz);
   return (b + 15) & ~size_t(15);
 }
 
@@ -149,7 +158,7 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   off += 2 * (M + 1);
   off = (off + 15) & ~size_t(15);
   w.hid = base + off;
-  off += M * 64;
+  off += (size_t)P.hid_cap;
   w.rel = base + off;
   off += (M + 15) & ~size_t(15);
   w.sgrp = base + off;
@@ -158,7 +167,7 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   w.hmask = reinterpret_cast<uint64_t*>(base + off);
   off += M * 8;
   off = (off + 15) & ~size_t(15);
-  w.tile = base + off;
+  w.tile = tile_extra(P.slots_max, sizeof(T)) ? base + off : reinterpret_cast<unsigned char*>(w.st0);
   return w;
 }
 
@@ -309,11 +318,11 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
         best_g = g;
       }
     }
-    upd += (unsigned long long)cnt * S;
+    if (active) upd += (unsigned long long)cnt * S;  // algorithmic work: live lanes only
   } else {
     for (int h = h0; h < h0 + cnt; ++h) {
       const int g = w.hid[h];
-      upd += (w.gt[g] >> 24);
+      if (active) upd += (w.gt[g] >> 24);
       const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
       if (f < best_f) {
         best_f = f;
@@ -322,7 +331,7 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
     }
   }
   if (mine) {  // this lane's added replica; ties resolved by group index
-    if (S > 0) upd += S;
+    if (S > 0) upd += S;  // (mine implies a live lane)
     else upd += (w.gt[my_g] >> 24);
     const T f = predict<T, S>(P, w, st, lane, my_g, m, ar, dv, tl);
     if (f < best_f || (f == best_f && my_g < best_g)) {
@@ -730,14 +739,22 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(kWarps * 32) chunk_kernel(ChunkParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), MODE == DUAL);
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL);
   WarpMem<T> w = carve<T>(smem + warp * wb, P, MODE == DUAL);
   int cur_base = -1;
   for (;;) {
     const int u = next_unit(P, lane);
     if (u >= P.num_units) break;
-    const int item = u % P.num_items;
-    const int j = (MODE == DUAL ? 1 : 0) + u / P.num_items;  // chunk-major
+    int item = u % P.num_items;
+    int j = (MODE == DUAL ? 1 : 0) + u / P.num_items;  // chunk-major
+    if (P.item_perm) {  // class by class, chunk-major inside a class
+      const int jn = P.J - (MODE == DUAL ? 1 : 0);
+      int c = 0;
+      while (c + 1 < P.nclass && u >= jn * (P.class_off[c] + P.class_items[c])) ++c;
+      const int local = u - jn * P.class_off[c];
+      j = (MODE == DUAL ? 1 : 0) + local / P.class_items[c];
+      item = P.item_perm[P.class_off[c] + local % P.class_items[c]];
+    }
     const ItemDesc it = P.items[item];
     if (it.base != cur_base) {
       load_base<T>(P, it, w, lane);
@@ -756,7 +773,7 @@ template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) walk_kernel(ChunkParams P, uint32_t* end_src) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), false);
   WarpMem<T> w = carve<T>(smem + warp * wb, P, false);
   int cur_base = -1;
   for (;;) {
@@ -1462,7 +1479,7 @@ template <typename T, bool SCALAR>
 __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, uint32_t* end_src) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), false);
   WarpMem<T> w = carve<T>(smem + warp * wb, P, false);
   int cur_base = -1;
   unsigned long long walked = 0, upd = 0;
@@ -1562,7 +1579,7 @@ template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) fast_stats_kernel(ChunkParams P, DevOut out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t wb = warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), false);
   WarpMem<T> w = carve<T>(smem + warp * wb, P, false);
   const int item = blockIdx.x * kWarps + warp;
   if (item >= P.num_items) return;
@@ -1694,7 +1711,7 @@ cudaError_t grid_for(K kernel, size_t smem, int64_t units, int sms, int64_t* blo
 
 template <typename T, int MODE>
 cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
-  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, sizeof(T), MODE == DUAL);
+  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL);
   int64_t blocks = 1;
   cudaError_t e = grid_for(chunk_kernel<T, MODE>, smem, P.num_units, sms, &blocks);
   if (e != cudaSuccess) return e;
@@ -1709,7 +1726,7 @@ cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
 template <typename T>
 cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, const WalkStreams& ws, int sms,
                           bool any_dynamic) {
-  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, sizeof(T), false);
+  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), false);
   int64_t blocks = 1;
   cudaError_t e = cudaMemsetAsync(P.counter, 0, 3 * sizeof(uint32_t), ws.main);
   if (e != cudaSuccess) return e;
@@ -1795,8 +1812,8 @@ cudaError_t launch_mix_states(int64_t C0, int64_t C1, int32_t J, int32_t stride,
   return cudaGetLastError();
 }
 
-size_t fast_stats_smem(int slots_max, int M, bool u32) {
-  return kWarps * warp_bytes(slots_max, M, u32 ? 4 : 8, false);
+size_t fast_stats_smem(int slots_max, int M, int hid_cap, bool u32) {
+  return kWarps * warp_bytes(slots_max, M, hid_cap, u32 ? 4 : 8, false);
 }
 
 // out.good_per_model[c][m] = sum_j spec_pm[j][c][m] + sum_{j>=1} fix_pm[j][c][m];
@@ -1835,7 +1852,7 @@ cudaError_t launch_chunk_stats_reduce(const ChunkParams& P, const DevOut& out, c
 cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32, cudaStream_t st,
                               int64_t* launches) {
   if (P.num_items <= 0) return cudaSuccess;
-  const size_t smem = fast_stats_smem(P.slots_max, P.pr.M, u32);
+  const size_t smem = fast_stats_smem(P.slots_max, P.pr.M, P.hid_cap, u32);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const unsigned blocks = (unsigned)((P.num_items + kWarps - 1) / kWarps);
   cudaError_t e;

@@ -25,6 +25,20 @@ bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim:
   return 4 * per_warp <= 220 * 1024;
 }
 
+// Hosting-list bytes per warp: the most (model, group) hostings of any base
+// in the batch, at least 4 M (the scalar walker's compact masks), rounded.
+static int32_t hid_cap_for(const asim_ctx* ctx, const HostBatch& hb) {
+  const int32_t M = ctx->hp.M;
+  int64_t cap = 4 * (int64_t)M;
+  const size_t B = M ? hb.base_mask.size() / M : 0;
+  for (size_t b = 0; b < B; ++b) {
+    int64_t n = 0;
+    for (int32_t m = 0; m < M; ++m) n += __builtin_popcountll(hb.base_mask[b * M + m]);
+    cap = std::max(cap, n);
+  }
+  return (int32_t)((cap + 15) & ~int64_t(15));
+}
+
 // uint32 relative time is exact when 2^32 - 1 - max slo - max service > 0
 // (chunk.cu header); require some headroom so epochs move rarely.
 static int64_t theta_for(const asim_ctx* ctx) {
@@ -74,7 +88,8 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   }
   const int64_t theta = ctx->force_path == 3 ? -1 : theta_for(ctx);
   const bool u32 = theta > 0;
-  if (asim::fast_stats_smem(slots_max, hp.M, u32) > 227 * 1024) return ASIM_OK;
+  const int32_t hid_cap = hid_cap_for(ctx, hb);
+  if (asim::fast_stats_smem(slots_max, hp.M, hid_cap, u32) > 227 * 1024) return ASIM_OK;
   cudaError_t e = upload(ctx->c_items, items, st);
   if (e == cudaSuccess) e = ctx->c_spm.ensure((size_t)C * hp.M * 4 + 8);  // int32 count rows
   if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_spm.p, 0, (size_t)C * hp.M * 4, st);
@@ -96,6 +111,7 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   P.J = 1;
   P.theta = theta;
   P.slots_max = slots_max;
+  P.hid_cap = hid_cap;
   P.spec_pm = ctx->c_spm.as<int32_t>();
   P.stat_C = C;
   P.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
@@ -211,6 +227,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.chunk_begin = ctx->c_begin.as<int64_t>();
   P.theta = theta;
   P.slots_max = slots_max;
+  P.hid_cap = hid_cap_for(ctx, hb);
   P.counter = ctx->c_counter.as<uint32_t>();
   P.spec_good = ctx->c_spec_good.as<int32_t>();
   P.spec_sum = ctx->c_spec_sum.as<int64_t>();
@@ -254,6 +271,25 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     P.stat_C = C;
   }
 
+  // ---- item classes by stage count (passes 1-2 run one class after another)
+  {
+    const int order[6] = {1, 2, 4, 8, 16, 0};
+    std::vector<int32_t> perm;
+    P.nclass = 0;
+    for (int S : order) {
+      const int32_t off = (int32_t)perm.size();
+      for (int32_t i = 0; i < I; ++i)
+        if (items[i].S == S) perm.push_back(i);
+      if ((int32_t)perm.size() > off) {
+        P.class_off[P.nclass] = off;
+        P.class_items[P.nclass] = (int32_t)perm.size() - off;
+        ++P.nclass;
+      }
+    }
+    e = upload(ctx->c_perm, perm, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "item classes");
+    P.item_perm = ctx->c_perm.as<int32_t>();
+  }
   // ---- pass 1: every (item, chunk) from the speculative start
   P.num_units = (int32_t)(J * I);
   e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);

@@ -301,9 +301,10 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
                     &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src, &ctx->d_cand_kmask,
-                    &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
+                    &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_perm, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
                     &ctx->c_fbusy};
     for (DBuf* b : bufs) b->release();
+    for (DBuf& b : ctx->spool) b.release();
     for (int i = 0; i < 2; ++i) {
       if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
       if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);

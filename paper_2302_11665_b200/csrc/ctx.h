@@ -9,6 +9,8 @@
 #include "../../include/asim.h"
 #include "asim_internal.h"
 
+constexpr int kSearchPool = 12;  // device scratch buffers an asim_search borrows
+
 // Grow-only device buffer.
 struct DBuf {
   void* p = nullptr;
@@ -71,6 +73,7 @@ struct asim_ctx {
   DBuf d_walked;   // unsigned long long walked-chunk counter
 
   int sms = 148;
+  DBuf spool[kSearchPool];  // search scratch kept across searches (search.cpp)
   // side streams / events of the concurrent walk pass (created by asim_create)
   cudaStream_t side[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
@@ -83,7 +86,7 @@ struct asim_ctx {
   bool last_u32 = false;
   asim::ChunkParams last_params{};
   std::vector<asim::ItemDesc> last_items;
-  DBuf c_pub;
+  DBuf c_pub, c_perm;
   DBuf c_spm, c_fpm, c_sbusy, c_fbusy;  // fast-heuristic statistics rows
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)

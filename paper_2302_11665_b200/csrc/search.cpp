@@ -406,6 +406,16 @@ static asim_status bucket_plan(asim_ctx* ctx, const asim_search_spec* spec, asim
   return ASIM_OK;
 }
 
+// The search's device scratch is lent by its context's pool (kept across
+// searches, like a caching allocator: repeated searches do not pay
+// cudaMalloc / cudaFree, which synchronise the device).
+static void search_buffers(asim_search* s, DBuf* (&bufs)[kSearchPool]) {
+  DBuf* b[kSearchPool] = {&s->d_good_all, &s->st_base, &s->st_next, &s->d_rows, &s->d_rows2,
+                          &s->d_scratch, &s->cs_prev, &s->cs_cur, &s->spec_mix, &s->d_mixrows,
+                          &s->d_pm, &s->d_busy};
+  for (int i = 0; i < kSearchPool; ++i) bufs[i] = b[i];
+}
+
 extern "C" {
 
 asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim_search** out) {
@@ -530,6 +540,11 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     s->runs.push_back(std::move(r));
   }
   s->stride = stride;
+  {
+    DBuf* bufs[kSearchPool];
+    search_buffers(s, bufs);
+    for (int i = 0; i < kSearchPool; ++i) std::swap(*bufs[i], ctx->spool[i]);  // borrow the pool
+  }
   s->prune = spec->prune != 0;
   s->gpruned.assign(s->ngroups, -1);
   s->gub.assign(s->ngroups, 0);
@@ -563,10 +578,16 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
 
 void asim_search_destroy(asim_search* s) {
   if (!s) return;
-  DBuf* bufs[] = {&s->d_good_all, &s->st_base, &s->st_next, &s->d_rows, &s->d_rows2,
-                  &s->d_scratch, &s->cs_prev, &s->cs_cur, &s->spec_mix, &s->d_mixrows,
-                  &s->d_pm, &s->d_busy};
-  for (DBuf* b : bufs) b->release();
+  DBuf* bufs[kSearchPool];
+  search_buffers(s, bufs);
+  for (int i = 0; i < kSearchPool; ++i) {
+    DBuf& pool = s->ctx ? s->ctx->spool[i] : *bufs[i];
+    if (&pool != bufs[i] && pool.cap < bufs[i]->cap) std::swap(pool, *bufs[i]);  // keep the larger
+    if (&pool != bufs[i]) bufs[i]->release();
+  }
+  if (!s->ctx) {
+    for (DBuf* b : bufs) b->release();
+  }
   delete s;
 }
 

@@ -92,7 +92,8 @@ struct WarpMem {
   T* slo;          // [M]   (clipped to T's range: exact, see header)
   uint32_t* gt;    // [64]  group table: cfg | off<<16 | s<<24
   uint16_t* hoff;  // [M+1] hosting list of model m in the base: hid[hoff[m] .. hoff[m+1])
-  uint8_t* hid;    // [M*64] group ids, ascending
+  uint16_t* hid;  // uniform items (S > 0): byte offset g * S * 32 * sizeof(T) of each
+                  // host's first stage slot; mixed items (S == 0): group ids    // [M*64] group ids, ascending
   uint8_t* rel;    // [M]   some lane of the unit hosts model m
   uint8_t* sgrp;   // [128] group of each stage slot
   uint64_t* hmask; // [M]   hosting groups of model m (bit set; warp-cooperative walker)
@@ -157,7 +158,7 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   w.hoff = reinterpret_cast<uint16_t*>(base + off);
   off += 2 * (M + 1);
   off = (off + 15) & ~size_t(15);
-  w.hid = base + off;
+  w.hid = reinterpret_cast<uint16_t*>(base + off);
   off += (size_t)P.hid_cap;
   w.rel = base + off;
   off += (M + 15) & ~size_t(15);
@@ -192,7 +193,8 @@ __device__ __forceinline__ void load_base(const ChunkParams& P, const ItemDesc& 
       w.hoff[m] = (uint16_t)start;
       uint64_t b = bits;
       for (int r = start; b; ++r) {
-        w.hid[r] = (uint8_t)(__ffsll((long long)b) - 1);
+        const int g = __ffsll((long long)b) - 1;
+        w.hid[r] = (uint16_t)(it.S > 0 ? g * it.S * 32 * (int)sizeof(T) : g);
         b &= b - 1;
       }
     }
@@ -274,52 +276,80 @@ __device__ __forceinline__ void commit(const ChunkParams& P, const WarpMem<T>& w
 
 // One request on one trajectory: dispatch (earliest predicted finish, lowest
 // index on ties), admission at receipt, commit.  Returns latency or -1.
+// S > 0 (uniform config): hinfo = byte offsets of the first two hosts
+// (off0 | off1 << 16), h0 = list start | host count << 16, further hosts'
+// offsets in w.hid; every host runs the same stage latencies dv, so for
+// S == 1 the argmin of max(v, a) is the argmin of the finish.  S == 0:
+// hinfo = first host | second host << 8 | count << 16 (group ids), h0 =
+// list start, group tables in w.gt.
 template <typename T, int S>
 __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& w, T* st, int lane,
                                         int m, int hinfo, int h0, bool mine, int my_g,
                                         bool active, T ar, const T* dv, T tl, T sl,
-                                        unsigned long long& upd, int& gout) {
-  // hinfo = first host | second host << 8 | host count << 16 (the base's
-  // hosting list of m, ascending); hosts beyond the second come from w.hid
-  T best_f = TT<T>::maxv();
-  int best_g = 64;
-  const int cnt = hinfo >> 16;
-  // ascending hosts, strict '<': the lowest index wins ties (C1)
+                                        uint32_t& upd, int& gout) {
   if constexpr (S > 0) {
-    const int g0 = hinfo & 0xFF, g1 = (hinfo >> 8) & 0xFF;
-    T v0[S], v1[S];
+    constexpr int kStride = 32 * (int)sizeof(T);  // bytes between a group's stages
+    const int cnt = h0 >> 16, hs = h0 & 0xFFFF;
+    const char* stl = reinterpret_cast<const char*>(st + lane);
+    T best = TT<T>::maxv();
+    int bo = 0x7FFFFFFF;  // byte offset of the best host (ascending = group order)
+    auto host = [&](int off) {
+      T x;
+      if constexpr (S == 1) {
+        x = tmax(*reinterpret_cast<const T*>(stl + off), ar);
+      } else {
+        x = ar;
 #pragma unroll
-    for (int k = 0; k < S; ++k) {  // both hosts' loads in flight together
-      v0[k] = cnt >= 1 ? st[(g0 * S + k) * 32 + lane] : (T)0;
-      v1[k] = cnt >= 2 ? st[(g1 * S + k) * 32 + lane] : (T)0;
-    }
-    if (cnt >= 1) {
-      T x = ar;
+        for (int k = 0; k < S; ++k) x = tmax(x, *reinterpret_cast<const T*>(stl + off + k * kStride)) + dv[k];
+      }
+      const bool lt = x < best;  // strict: the lowest index wins ties (C1)
+      best = lt ? x : best;
+      bo = lt ? off : bo;
+    };
+    if (cnt >= 1) host(hinfo & 0xFFFF);
+    if (cnt >= 2) host((int)((unsigned)hinfo >> 16));
+    for (int h = hs + 2; h < hs + cnt; ++h) host(w.hid[h]);
+    if (active) upd += (uint32_t)cnt;  // algorithmic work (x S at the flush): live lanes only
+    if (mine) {  // this lane's added replica; ties resolved by group index
+      upd += 1u;
+      const int off = my_g * S * kStride;
+      T x;
+      if constexpr (S == 1) {
+        x = tmax(*reinterpret_cast<const T*>(stl + off), ar);
+      } else {
+        x = ar;
 #pragma unroll
-      for (int k = 0; k < S; ++k) x = tmax(x, v0[k]) + dv[k];
-      best_f = x + tl;
-      best_g = g0;
-    }
-    if (cnt >= 2) {
-      T x = ar;
-#pragma unroll
-      for (int k = 0; k < S; ++k) x = tmax(x, v1[k]) + dv[k];
-      const T f = x + tl;
-      if (f < best_f) {
-        best_f = f;
-        best_g = g1;
+        for (int k = 0; k < S; ++k) x = tmax(x, *reinterpret_cast<const T*>(stl + off + k * kStride)) + dv[k];
+      }
+      if (x < best || (x == best && off < bo)) {
+        best = x;
+        bo = off;
       }
     }
-    for (int h = h0 + 2; h < h0 + cnt; ++h) {
-      const int g = w.hid[h];
-      const T f = predict<T, S>(P, w, st, lane, g, m, ar, dv, tl);
-      if (f < best_f) {
-        best_f = f;
-        best_g = g;
+    // S == 1: best = max(v, a), the finish is best + d0 + tail
+    const T dep = S == 1 ? (T)(best + dv[0]) : best;  // last stage departure of the winner
+    const T f = dep + tl;
+    if (active && bo != 0x7FFFFFFF && (T)(f - ar) <= sl) {  // reject at receipt if the SLO is missed (C2, C3)
+      gout = bo / (S * kStride);
+      char* stw = reinterpret_cast<char*>(st + lane);
+      if constexpr (S == 1) {
+        *reinterpret_cast<T*>(stw + bo) = dep;
+      } else {
+        T x = ar;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          T* p = reinterpret_cast<T*>(stw + bo + k * kStride);
+          x = tmax(x, *p) + dv[k];
+          *p = x;
+        }
       }
+      return (int64_t)(f - ar);
     }
-    if (active) upd += (unsigned long long)cnt * S;  // algorithmic work: live lanes only
+    return -1;
   } else {
+    T best_f = TT<T>::maxv();
+    int best_g = 64;
+    const int cnt = hinfo >> 16;
     for (int h = h0; h < h0 + cnt; ++h) {
       const int g = w.hid[h];
       if (active) upd += (w.gt[g] >> 24);
@@ -329,26 +359,21 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
         best_g = g;
       }
     }
-  }
-  if (mine) {  // this lane's added replica; ties resolved by group index
-    if (S > 0) upd += S;  // (mine implies a live lane)
-    else upd += (w.gt[my_g] >> 24);
-    const T f = predict<T, S>(P, w, st, lane, my_g, m, ar, dv, tl);
-    if (f < best_f || (f == best_f && my_g < best_g)) {
-      best_f = f;
-      best_g = my_g;
+    if (mine) {  // this lane's added replica; ties resolved by group index
+      upd += (w.gt[my_g] >> 24);
+      const T f = predict<T, S>(P, w, st, lane, my_g, m, ar, dv, tl);
+      if (f < best_f || (f == best_f && my_g < best_g)) {
+        best_f = f;
+        best_g = my_g;
+      }
     }
-  }
-  if (active && best_g < 64 && (T)(best_f - ar) <= sl) {  // reject at receipt if the SLO is missed (C2, C3)
-    gout = best_g;
-    if constexpr (S == 1) {
-      st[best_g * 32 + lane] = best_f - tl;  // one stage: its departure is f - tail
-    } else {
+    if (active && best_g < 64 && (T)(best_f - ar) <= sl) {  // reject at receipt if the SLO is missed (C2, C3)
+      gout = best_g;
       commit<T, S>(P, w, st, lane, best_g, m, ar, dv);
+      return (int64_t)(best_f - ar);
     }
-    return (int64_t)(best_f - ar);
+    return -1;
   }
-  return -1;
 }
 
 // Stage occupancy sum_k d_k of model m on group g (fast-heuristic busy time).
@@ -527,6 +552,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
 
   int64_t good0 = 0, sum0 = 0, good1 = 0, sum1 = 0;
   unsigned long long upd = 0;
+  uint32_t upd32 = 0;  // hosts evaluated (S > 0) / stage updates (S == 0) by this lane
   bool coalesced = false;
   T dv[S > 0 ? S : 1];
   // 4-deep ring of trace tiles in registers: a lone warp (the walk) would
@@ -580,8 +606,12 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
     const T ar_l = (T)(ai - E);
     const int h0_l = w.hoff[mi];
     const int cnt_l = w.hoff[mi + 1] - h0_l;
-    const int hinfo_l = (cnt_l >= 1 ? (int)w.hid[h0_l] : 0) |
-                        (cnt_l >= 2 ? (int)w.hid[h0_l + 1] << 8 : 0) | (cnt_l << 16);
+    // S > 0: the first two hosts' byte offsets; S == 0: their group ids
+    const int hinfo_l = S > 0 ? ((cnt_l >= 1 ? (int)w.hid[h0_l] : 0) |
+                                 (cnt_l >= 2 ? (int)w.hid[h0_l + 1] << 16 : 0))
+                              : ((cnt_l >= 1 ? (int)w.hid[h0_l] : 0) |
+                                 (cnt_l >= 2 ? (int)w.hid[h0_l + 1] << 8 : 0) | (cnt_l << 16));
+    const int h0c_l = S > 0 ? (h0_l | (cnt_l << 16)) : h0_l;  // S > 0: list start | count
     const T sl_l = w.slo[mi];
     T tl_l = 0, d0_l = 0;
     if constexpr (S > 0) tl_l = w.tail[mi];
@@ -591,7 +621,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
     todo &= todo - 1;
     int m = __shfl_sync(FULL, mi, jj);
     T ar = __shfl_sync(FULL, ar_l, jj);
-    int hinfo = __shfl_sync(FULL, hinfo_l, jj), h0 = __shfl_sync(FULL, h0_l, jj);
+    int hinfo = __shfl_sync(FULL, hinfo_l, jj), h0 = __shfl_sync(FULL, h0c_l, jj);
     T sl = __shfl_sync(FULL, sl_l, jj), tl = 0, d0 = 0;
     if constexpr (S > 0) tl = __shfl_sync(FULL, tl_l, jj);
     if constexpr (S == 1) d0 = __shfl_sync(FULL, d0_l, jj);
@@ -606,7 +636,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
         m = __shfl_sync(FULL, mi, jj);
         ar = __shfl_sync(FULL, ar_l, jj);
         hinfo = __shfl_sync(FULL, hinfo_l, jj);
-        h0 = __shfl_sync(FULL, h0_l, jj);
+        h0 = __shfl_sync(FULL, h0c_l, jj);
         sl = __shfl_sync(FULL, sl_l, jj);
         if constexpr (S > 0) tl = __shfl_sync(FULL, tl_l, jj);
       }
@@ -628,7 +658,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       const bool mine = live && cm == my_m;
       int g0 = 0, g1 = 0;
       const int64_t l0 = step<T, S>(P, w, w.st0, lane, cm, chinfo, ch0, mine, my_g, live, car,
-                                    dv, ctl, csl, upd, g0);
+                                    dv, ctl, csl, upd32, g0);
       if (l0 >= 0) {
         ++good0;
         sum0 += l0;
@@ -641,7 +671,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       }
       if constexpr (MODE == DUAL) {
         const int64_t l1 = step<T, S>(P, w, w.st1, lane, cm, chinfo, ch0, mine, my_g, live,
-                                      car, dv, ctl, csl, upd, g1);
+                                      car, dv, ctl, csl, upd32, g1);
         if (l1 >= 0) {
           ++good1;
           sum1 += l1;
@@ -654,6 +684,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
   }
 
   if (P.stage_updates) {
+    upd += (unsigned long long)upd32 * (S > 0 ? S : 1);
     for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(FULL, upd, o);
     if (lane == 0) atomicAdd(P.stage_updates, upd);
   }
@@ -1099,7 +1130,7 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
   }
   // compact hosting mask of every model (the cooperative walker leaves the
   // hosting-list region w.hid unused: it serves as scratch here)
-  uint32_t* hmc = reinterpret_cast<uint32_t*>(w.hid);
+  uint32_t* hmc = reinterpret_cast<uint32_t*>(w.hid);  // region >= 4 M bytes (hid_cap)
   for (int m = lane; m < P.pr.M; m += 32) {
     const uint64_t hm = w.hmask[m] | (m == my_m ? (1ull << my_g) : 0ull);
     uint32_t x = 0;

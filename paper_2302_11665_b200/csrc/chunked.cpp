@@ -25,8 +25,9 @@ bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim:
   return 4 * per_warp <= 220 * 1024;
 }
 
-// Hosting-list bytes per warp: the most (model, group) hostings of any base
-// in the batch, at least 4 M (the scalar walker's compact masks), rounded.
+// Hosting-list bytes per warp: 2 bytes per (model, group) hosting of the
+// largest base in the batch, at least 4 M (the scalar walker's compact
+// masks), rounded.
 static int32_t hid_cap_for(const asim_ctx* ctx, const HostBatch& hb) {
   const int32_t M = ctx->hp.M;
   int64_t cap = 4 * (int64_t)M;
@@ -34,7 +35,7 @@ static int32_t hid_cap_for(const asim_ctx* ctx, const HostBatch& hb) {
   for (size_t b = 0; b < B; ++b) {
     int64_t n = 0;
     for (int32_t m = 0; m < M; ++m) n += __builtin_popcountll(hb.base_mask[b * M + m]);
-    cap = std::max(cap, n);
+    cap = std::max(cap, 2 * n);  // uint16 entries
   }
   return (int32_t)((cap + 15) & ~int64_t(15));
 }

@@ -102,6 +102,8 @@ typedef struct {
   int64_t walk_candidates;      /* candidates (items for mixed configs) that walked >= 1 chunk */
   int64_t walk_critical_chunks; /* sum over walk launches of the longest single walk (chunks):
                                    the sequential critical path of the walk pass */
+  double spec_ms;               /* summed device time of the chunked path's pass-1 launches */
+  int64_t spec_stage_updates;   /* stage updates performed by pass 1 (part of stage_updates) */
 } asim_stats;
 asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
 asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);
@@ -305,6 +307,17 @@ double asim_attainment(int64_t good, int64_t n);
  * best_good and the placement are exactly those of prune = 0.  A pruned
  * run's asim_search_run_info reports its best up to the step it stopped
  * (asim_search_run_pruned).
+ * Exact candidate bounding (spec->cand_bound = 1; not in the paper): a step only
+ * needs its argmax.  With K_c the hosting-graph component a candidate
+ * changes, good(c) = good(base) - good_base(K_c) + good_c(K_c) <= good(base)
+ * - good_base(K_c) + n(K_c), n(K_c) = trace requests of K_c's models.  A
+ * candidate whose bound is below the best exact value known (or equal to it
+ * with a later (m, g) index) is never simulated; a step simulates the
+ * candidates that may gain (bound above the base's good) and the first few
+ * others first, and lists the remaining undecided ones in a second round
+ * (the next prepare returns them; the run does not advance meanwhile).
+ * Every run's winner, and so every result, is that of cand_bound = 0; `steps`
+ * counts rounds, `evaluated` only simulated candidates.
  * Errors (asim_search_create): ASIM_EINVAL null latency / bad ratio or bound;
  * fast = 1 with beam > 1;
  * ASIM_ERANGE latency outside [1, 2^60], a run with > ASIM_MAX_GROUPS groups,
@@ -324,6 +337,8 @@ typedef struct {
   const int64_t* model_latency_ns; /* [M] host; single-device latency (Table 1) */
   int32_t beam;                  /* Alg. 1 beam size k (<= 1 means 1; see below) */
   int32_t prune;                 /* 1 = exact run pruning (see below) */
+  int32_t cand_bound;            /* 1 = exact candidate bounding (see below; beam = 1,
+                                    not with fast) */
 } asim_search_spec;
 
 typedef struct {
@@ -337,6 +352,7 @@ typedef struct {
   int64_t evaluated;       /* candidates actually simulated (after dedup)     */
   int64_t request_evals;   /* sum over evaluated candidates of n (requests)   */
   int64_t memo_hits;       /* candidates whose good came from the component memo */
+  int64_t bounded;         /* candidates never simulated (spec->cand_bound) */
 } asim_search_result;
 
 asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim_search** out);

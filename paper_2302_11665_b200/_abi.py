@@ -49,14 +49,16 @@ class asim_results(ctypes.Structure):
 class asim_stats(ctypes.Structure):
     _fields_ = [("launches", i64), ("sim_launches", i64), ("sim_ms", ctypes.c_double),
                 ("stage_updates", i64), ("request_evals", i64), ("chunk_reruns", i64),
-                ("walk_candidates", i64), ("walk_critical_chunks", i64)]
+                ("walk_candidates", i64), ("walk_critical_chunks", i64),
+                ("spec_ms", ctypes.c_double), ("spec_stage_updates", i64)]
 
 
 class asim_search_spec(ctypes.Structure):
     _fields_ = [("num_runs", i32), ("run_num_groups", vp), ("run_group_cfg", vp),
                 ("dedup", i32), ("fast", i32), ("buckets", i32), ("max_buckets", i32),
                 ("ratio_num", i64), ("ratio_den", i64), ("bound_num", i64), ("bound_den", i64),
-                ("model_latency_ns", vp), ("beam", i32), ("prune", i32)]
+                ("model_latency_ns", vp), ("beam", i32), ("prune", i32),
+                ("cand_bound", i32)]
 
 
 class asim_bucket_result(ctypes.Structure):
@@ -68,7 +70,7 @@ class asim_bucket_result(ctypes.Structure):
 class asim_search_result(ctypes.Structure):
     _fields_ = [("best_run", i32), ("best_good", i64), ("num_groups", i32), ("group_cfg", vp),
                 ("host_mask", vp), ("steps", i64), ("candidates", i64), ("evaluated", i64),
-                ("request_evals", i64), ("memo_hits", i64)]
+                ("request_evals", i64), ("memo_hits", i64), ("bounded", i64)]
 
 
 if not os.path.exists(LIB_PATH):

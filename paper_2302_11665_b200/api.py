@@ -62,6 +62,7 @@ class SearchResult:
     request_evals: int
     memo_hits: int
     runs: list
+    bounded: int = 0
 
 
 @dataclass
@@ -133,7 +134,8 @@ class Simulator:
         return dict(launches=s.launches, sim_launches=s.sim_launches, sim_ms=s.sim_ms,
                     stage_updates=s.stage_updates, request_evals=s.request_evals,
                     chunk_reruns=s.chunk_reruns, walk_candidates=s.walk_candidates,
-                    walk_critical_chunks=s.walk_critical_chunks)
+                    walk_critical_chunks=s.walk_critical_chunks, spec_ms=s.spec_ms,
+                    spec_stage_updates=s.spec_stage_updates)
 
     def set_chunk_size(self, min_requests: int) -> None:
         self._check(A.asim_set_chunk_size(self.h, int(min_requests)))
@@ -202,11 +204,12 @@ class Simulator:
 
     # ------------------------------------------------------------- search
     def search_handle(self, runs=None, dedup=True, fast=False, buckets=None,
-                      beam=1, prune=True) -> "SearchHandle":
-        return SearchHandle(self, runs, dedup, fast, buckets, beam, prune)
+                      beam=1, prune=True, bounding=False) -> "SearchHandle":
+        return SearchHandle(self, runs, dedup, fast, buckets, beam, prune, bounding)
 
     def search_buckets(self, latency, ratio=4, bound=3, max_buckets=0, fast=False, dedup=True,
-                       pg=None, stream=None, beam=1, prune=True) -> BucketResult:
+                       pg=None, stream=None, beam=1, prune=True,
+                       bounding=False) -> BucketResult:
         """Alg. 2 with model and device buckets (include/asim.h).
         latency[m]: single-device latency in ns; ratio / bound: ints or
         fractions.Fraction (threshold 4x and discrepancy bound 3x by default)."""
@@ -216,7 +219,7 @@ class Simulator:
 
         b = dict(latency=_host(latency, np.int64), ratio=Fraction(ratio), bound=Fraction(bound),
                  max_buckets=int(max_buckets))
-        with self.search_handle(None, dedup, fast, b, beam, prune) as sh:
+        with self.search_handle(None, dedup, fast, b, beam, prune, bounding) as sh:
             if fast:
                 sh.run(stream=stream)
             else:
@@ -235,7 +238,7 @@ class Simulator:
                                 r.partitions, r.considered, res)
 
     def search(self, runs=None, dedup=True, pg=None, stream=None, fast=False,
-               beam=1, prune=True) -> SearchResult:
+               beam=1, prune=True, bounding=False) -> SearchResult:
         """Full Alg. 2 (single bucket) / Alg. 1 search.  With a
         torch.distributed process group the step candidates shard across its
         ranks (dist.run_search).  fast=True runs the fast heuristic of P:737
@@ -243,7 +246,7 @@ class Simulator:
         computes it whole -- there is nothing to shard)."""
         from . import dist
 
-        with self.search_handle(runs, dedup, fast, None, beam, prune) as sh:
+        with self.search_handle(runs, dedup, fast, None, beam, prune, bounding) as sh:
             if fast:
                 sh.run(stream=stream)
             else:
@@ -255,13 +258,14 @@ class SearchHandle:
     """Stepwise search protocol of include/asim.h (prepare / evaluate / apply)."""
 
     def __init__(self, sim: Simulator, runs=None, dedup=True, fast=False, buckets=None,
-                 beam=1, prune=True):
+                 beam=1, prune=True, bounding=False):
         self.sim = sim
         spec = A.asim_search_spec()
         spec.dedup = int(bool(dedup))
         spec.fast = int(bool(fast))
         spec.beam = int(beam)
         spec.prune = int(bool(prune))
+        spec.cand_bound = int(bool(bounding))
         self._keep = ()
         if buckets is not None:
             lat = buckets["latency"]
@@ -318,7 +322,7 @@ class SearchHandle:
         M = self.sim.M
         cfg = np.full(A.ASIM_MAX_GROUPS, -1, np.int32)
         mask = np.zeros(M, np.uint64)
-        r = A.asim_search_result(0, 0, 0, _ptr(cfg), _ptr(mask), 0, 0, 0, 0, 0)
+        r = A.asim_search_result(0, 0, 0, _ptr(cfg), _ptr(mask), 0, 0, 0, 0, 0, 0)
         self.sim._check(A.asim_search_result_get(self.h, ctypes.byref(r)))
         runs = []
         for i in range(A.asim_search_num_runs(self.h)):
@@ -334,4 +338,4 @@ class SearchHandle:
                              pruned_at=int(A.asim_search_run_pruned(self.h, i))))
         return SearchResult(r.best_run, r.best_good, r.num_groups, cfg[:r.num_groups].copy(),
                             mask, r.steps, r.candidates, r.evaluated, r.request_evals,
-                            r.memo_hits, runs)
+                            r.memo_hits, runs, r.bounded)

@@ -293,8 +293,24 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   }
   // ---- pass 1: every (item, chunk) from the speculative start
   P.num_units = (int32_t)(J * I);
-  e = asim::launch_chunk_pass(P, false, u32, st, ctx->sms, &ctx->launches);
-  if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
+  {
+    // profiling: pass 1 alone (the dominant kernel) gets its own events and
+    // work counter (d_counter[1]; the total is d_counter[0] + d_counter[1])
+    asim::ChunkParams P1 = P;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (ctx->profiling && P.stage_updates) {
+      P1.stage_updates = ctx->d_counter.as<unsigned long long>() + 1;
+      if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
+        return asim_cuda(ctx, cudaGetLastError(), "event create");
+      cudaEventRecord(ev0, st);
+    }
+    e = asim::launch_chunk_pass(P1, false, u32, st, ctx->sms, &ctx->launches);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
+    if (ev0) {
+      cudaEventRecord(ev1, st);
+      ctx->spec_events.emplace_back(ev0, ev1);
+    }
+  }
 
   e = ctx->c_end_src.ensure(J * I * 4 + 8);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src buffer");

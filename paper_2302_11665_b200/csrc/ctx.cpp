@@ -323,17 +323,20 @@ int64_t asim_launch_count(const asim_ctx* ctx) { return ctx ? ctx->launches : 0;
 asim_status asim_reset_stats(asim_ctx* ctx) {
   if (!ctx) return ASIM_EINVAL;
   DeviceGuard dg(ctx->device);
-  for (auto& ev : ctx->events) {
-    cudaEventSynchronize(ev.second);
-    cudaEventDestroy(ev.first);
-    cudaEventDestroy(ev.second);
+  for (auto* evs : {&ctx->events, &ctx->spec_events}) {
+    for (auto& ev : *evs) {
+      cudaEventSynchronize(ev.second);
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+    evs->clear();
   }
-  ctx->events.clear();
   ctx->sim_launches = 0;
   ctx->sim_ms = 0.0;
+  ctx->spec_ms = 0.0;
   ctx->request_evals = 0;
   if (ctx->d_counter.p) {
-    cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 8);
+    cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 16);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return asim_cuda(ctx, e, "reset stats");
@@ -359,9 +362,9 @@ asim_status asim_set_profiling(asim_ctx* ctx, int32_t on) {
   if (!ctx) return ASIM_EINVAL;
   DeviceGuard dg(ctx->device);
   if (on && !ctx->d_counter.p) {
-    cudaError_t e = ctx->d_counter.ensure(8);
+    cudaError_t e = ctx->d_counter.ensure(16);
     if (e == cudaSuccess) e = ctx->d_walked.ensure(32);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 8);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 16);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "profiling counter");
   }
@@ -382,16 +385,28 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
     cudaEventDestroy(ev.second);
   }
   ctx->events.clear();
-  unsigned long long upd = 0, walked[4] = {0, 0, 0, 0};
+  for (auto& ev : ctx->spec_events) {
+    cudaError_t e = cudaEventSynchronize(ev.second);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev.first, ev.second);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "stats events");
+    ctx->spec_ms += ms;
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
+  ctx->spec_events.clear();
+  unsigned long long upd2[2] = {0, 0}, walked[4] = {0, 0, 0, 0};
   if (ctx->d_counter.p) {
-    cudaError_t e = cudaMemcpy(&upd, ctx->d_counter.p, 8, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(upd2, ctx->d_counter.p, 16, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(walked, ctx->d_walked.p, 32, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "stats counter");
   }
   out->launches = ctx->launches;
   out->sim_launches = ctx->sim_launches;
   out->sim_ms = ctx->sim_ms;
-  out->stage_updates = (int64_t)upd;
+  out->stage_updates = (int64_t)(upd2[0] + upd2[1]);
+  out->spec_stage_updates = (int64_t)upd2[1];
+  out->spec_ms = ctx->spec_ms;
   out->request_evals = ctx->request_evals;
   out->chunk_reruns = (int64_t)walked[0];
   out->walk_candidates = (int64_t)walked[1];

@@ -66,10 +66,12 @@ struct asim_ctx {
   // statistics (asim_set_profiling)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spec_events;  // pass 1 launches only
+  double spec_ms = 0.0;
   int64_t sim_launches = 0;
   double sim_ms = 0.0;
   int64_t request_evals = 0;
-  DBuf d_counter;  // unsigned long long stage-update counter
+  DBuf d_counter;  // unsigned long long stage-update counters [2]: other kernels, pass 1
   DBuf d_walked;   // unsigned long long walked-chunk counter
 
   int sms = 148;

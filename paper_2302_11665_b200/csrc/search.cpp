@@ -75,13 +75,20 @@ struct Run {
   // components of the base: union-find over G groups + M models (node G + m)
   std::vector<int32_t> parent;
   std::vector<int64_t> cgood;  // good of the component rooted at a node
+  std::vector<int64_t> cn;     // requests (in the trace) of the models of that component
+  int32_t round = 0;           // candidate bounding: 1 = deferred candidates still to simulate
   // this step's full candidate list, in (m, g) order
   struct Cand {
     int32_t m, g;
-    int8_t kind;  // 0 simulated (ref = batch index), 1 memo (value), 2 duplicate (ref = rep)
+    // 0 simulated in this sub-step (ref = batch index), 1 memo (value),
+    // 2 duplicate (ref = rep), 3 deferred (bounding: may still be needed),
+    // 4 bounded out (provably not the argmax; no value), 5 simulated in an
+    // earlier round of this step (value)
+    int8_t kind;
     int64_t ref;
     int64_t good;
     int32_t r1, r2;  // roots of comp(g) and comp(m) in the base
+    int64_t ub = 0;  // upper bound on good (bounding)
   };
   std::vector<Cand> cands;
   // memo for the next step, flat over (m, g): good and validity
@@ -200,6 +207,8 @@ struct asim_search {
   // exact run pruning (spec->prune): per run group a bound on the good of ANY
   // selection on its groups, and the step at which it was pruned (-1: never)
   bool prune = false;
+  bool bound = false;   // exact candidate bounding (spec->cand_bound)
+  int64_t bounded = 0;  // candidates never simulated thanks to it
   std::vector<int64_t> gub;
   std::vector<int64_t> gpruned;
   // statistics
@@ -523,6 +532,8 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     r.parent.resize(r.G + hp.M);
     for (size_t i = 0; i < r.parent.size(); ++i) r.parent[i] = (int32_t)i;
     r.cgood.assign(r.G + hp.M, 0);
+    r.cn.assign(r.G + hp.M, 0);
+    for (int32_t m = 0; m < hp.M; ++m) r.cn[r.G + m] = ctx->model_n[m];
     r.memo_good.assign((size_t)hp.M * r.G, 0);
     r.memo_ok.assign((size_t)hp.M * r.G, 0);
     r.prev_idx.assign((size_t)hp.M * r.G, -1);
@@ -546,6 +557,7 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     for (int i = 0; i < kSearchPool; ++i) std::swap(*bufs[i], ctx->spool[i]);  // borrow the pool
   }
   s->prune = spec->prune != 0;
+  s->bound = spec->cand_bound != 0 && s->beam == 1 && !s->fast;
   s->gpruned.assign(s->ngroups, -1);
   s->gub.assign(s->ngroups, 0);
   if (s->prune)
@@ -614,57 +626,100 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
     Run& run = s->runs[r];
     if (!run.active) continue;
     const int32_t b = (int32_t)s->base_run.size();
-    std::vector<uint8_t> empty(run.G, 1);
-    for (int32_t m = 0; m < M; ++m)
-      for (int32_t g = 0; g < run.G; ++g)
-        if ((run.sel[m] >> g) & 1ULL) empty[g] = 0;
-    run.cands.clear();
-    if (s->restrict_k) root_masks(run, M);
-    for (int32_t m = 0; m < M; ++m) {
-      if (!run.may_place(m)) continue;  // outside this run's bucket
-      std::map<std::pair<int32_t, int32_t>, int64_t> seen;  // (cfg, rank among hosts) -> rep
-      for (int32_t g = 0; g < run.G; ++g) {
-        if ((run.sel[m] >> g) & 1ULL) continue;  // a model at most once per group (C11)
-        const int64_t mb = hp.mem_at(m, run.cfg[g]);
-        if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
-        ++full;
-        Run::Cand c{m, g, 0, 0, 0, run.find(g), run.find(run.G + m)};
-        const size_t mi = (size_t)m * run.G + g;
-        if (run.memo_ok[mi]) {  // component untouched by the last winner
-          c.kind = 1;
-          c.good = run.memo_good[mi];
-          ++s->memo_hits;
-        } else if (s->dedup && empty[g]) {
-          const uint64_t below = g ? (run.sel[m] & ((1ULL << g) - 1)) : 0ULL;
-          auto key = std::make_pair(run.cfg[g], (int32_t)__builtin_popcountll(below));
-          auto sit = seen.find(key);
-          if (sit != seen.end()) {
-            c.kind = 2;
-            c.ref = sit->second;
-          } else {
-            seen[key] = (int64_t)run.cands.size();
-          }
-        }
-        if (c.kind == 0) {
-          c.ref = (int64_t)hb.cand_base.size();
-          hb.cand_base.push_back(b);
-          hb.cand_model.push_back(m);
-          hb.cand_group.push_back(g);
-          hb.cand_ok.push_back(1);
-          if (s->restrict_k) {
-            uint64_t km = 0, gm = 0;
-            component_masks(run, m, g, c.r1, c.r2, &km, &gm);
-            hb.cand_kmask.push_back(km);
-            hb.cand_gmask.push_back(gm);
-          }
-          s->mixrows.push_back(asim::MixRow{r, run.prev_idx[(size_t)m * run.G + g]});
-        }
-        run.cands.push_back(c);
+    // candidate c of this run goes to the batch (kind 0)
+    auto emit = [&](Run::Cand& c, int32_t prev) {
+      c.kind = 0;
+      c.ref = (int64_t)hb.cand_base.size();
+      hb.cand_base.push_back(b);
+      hb.cand_model.push_back(c.m);
+      hb.cand_group.push_back(c.g);
+      hb.cand_ok.push_back(1);
+      if (s->restrict_k) {
+        uint64_t km = 0, gm = 0;
+        component_masks(run, c.m, c.g, c.r1, c.r2, &km, &gm);
+        hb.cand_kmask.push_back(km);
+        hb.cand_gmask.push_back(gm);
       }
-    }
-    if (run.cands.empty()) {  // no feasible addition: this run's Alg. 1 loop ends
-      run.active = false;
-      continue;
+      s->mixrows.push_back(asim::MixRow{r, prev});
+    };
+    if (run.round == 1) {  // the same step, second round: deferred candidates
+      if (s->restrict_k) root_masks(run, M);
+      for (Run::Cand& c : run.cands)
+        if (c.kind == 3) emit(c, -1);
+    } else {
+      std::vector<uint8_t> empty(run.G, 1);
+      for (int32_t m = 0; m < M; ++m)
+        for (int32_t g = 0; g < run.G; ++g)
+          if ((run.sel[m] >> g) & 1ULL) empty[g] = 0;
+      run.cands.clear();
+      if (s->restrict_k) root_masks(run, M);
+      for (int32_t m = 0; m < M; ++m) {
+        if (!run.may_place(m)) continue;  // outside this run's bucket
+        std::map<std::pair<int32_t, int32_t>, int64_t> seen;  // (cfg, rank among hosts) -> rep
+        for (int32_t g = 0; g < run.G; ++g) {
+          if ((run.sel[m] >> g) & 1ULL) continue;  // a model at most once per group (C11)
+          const int64_t mb = hp.mem_at(m, run.cfg[g]);
+          if (mb < 0 || run.used[g] + mb > hp.budget) continue;  // memory constraint
+          ++full;
+          Run::Cand c{m, g, 0, 0, 0, run.find(g), run.find(run.G + m)};
+          const size_t mi = (size_t)m * run.G + g;
+          if (run.memo_ok[mi]) {  // component untouched by the last winner
+            c.kind = 1;
+            c.good = run.memo_good[mi];
+            ++s->memo_hits;
+          } else if (s->dedup && empty[g]) {
+            const uint64_t below = g ? (run.sel[m] & ((1ULL << g) - 1)) : 0ULL;
+            auto key = std::make_pair(run.cfg[g], (int32_t)__builtin_popcountll(below));
+            auto sit = seen.find(key);
+            if (sit != seen.end()) {
+              c.kind = 2;
+              c.ref = sit->second;
+            } else {
+              seen[key] = (int64_t)run.cands.size();
+            }
+          }
+          run.cands.push_back(c);
+        }
+      }
+      if (run.cands.empty()) {  // no feasible addition: this run's Alg. 1 loop ends
+        run.active = false;
+        continue;
+      }
+      if (s->bound) {
+        // Exact candidate bounding (not in the paper; the step's argmax is
+        // unchanged).  good(c) = good(base) - good_base(K_c) + good_c(K_c)
+        // and good_c(K_c) <= n(K_c), the trace's requests of K_c's models.
+        // Candidates that cannot beat the best exact value known (memo) are
+        // dropped; this round simulates the possible gainers (ub > good of
+        // the base) and the first kFirst others in (m, g) order, the rest
+        // wait for apply, which drops every one the round's best excludes.
+        constexpr int kFirst = 4;
+        int64_t bg = -1, bi = -1;
+        for (size_t i = 0; i < run.cands.size(); ++i) {
+          const Run::Cand& c = run.cands[i];
+          if (c.kind == 1 && c.good > bg) {
+            bg = c.good;
+            bi = (int64_t)i;
+          }
+        }
+        int first = 0;
+        for (size_t i = 0; i < run.cands.size(); ++i) {
+          Run::Cand& c = run.cands[i];
+          if (c.kind != 0) continue;
+          const bool two = c.r2 != c.r1;
+          c.ub = run.base_good - run.cgood[c.r1] - (two ? run.cgood[c.r2] : 0) + run.cn[c.r1] +
+                 (two ? run.cn[c.r2] : 0);
+          if (c.ub < bg || (c.ub == bg && (int64_t)i > bi)) {
+            c.kind = 4;
+          } else if (!(c.ub > run.base_good || first < kFirst)) {
+            c.kind = 3;
+          } else if (c.ub <= run.base_good) {
+            ++first;
+          }
+        }
+      }
+      for (Run::Cand& c : run.cands)
+        if (c.kind == 0) emit(c, run.prev_idx[(size_t)c.m * run.G + c.g]);
     }
     s->base_run.push_back(r);
     for (int32_t g = 0; g < G; ++g) hb.base_cfg.push_back(g < run.G ? run.cfg[g] : -1);
@@ -749,7 +804,8 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
 // one lane each, restricted to their own component.
 static asim_status update_states(asim_search* s, const std::vector<int32_t>& winner_run,
                                  const std::vector<const Run::Cand*>& winner, cudaStream_t st,
-                                 const std::vector<int32_t>* target_rows = nullptr) {
+                                 const std::vector<int32_t>* target_rows = nullptr,
+                                 const std::vector<int32_t>* keep_rows = nullptr) {
   // winner_run[i]: the run (old base) the winner extends; target_rows[i]: the
   // st_next row receiving the new base (default: the same run)
   asim_ctx* ctx = s->ctx;
@@ -808,6 +864,15 @@ static asim_status update_states(asim_search* s, const std::vector<int32_t>& win
     rc = asim_publish_candidates(ctx, all, out_rows, s->st_next.as<int64_t>(), st);
     if (rc) return rc;
   }
+  if (keep_rows) {  // runs whose base did not change (a pending round): carry their rows over
+    const size_t row = (size_t)s->J * s->stride * 8;
+    for (int32_t r : *keep_rows) {
+      cudaError_t e = cudaMemcpyAsync(s->st_next.as<char>() + (size_t)r * row,
+                                      s->st_base.as<char>() + (size_t)r * row, row,
+                                      cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "carry base states");
+    }
+  }
   std::swap(s->st_base, s->st_next);
   return ASIM_OK;
 }
@@ -821,7 +886,8 @@ static void apply_winner(Run& run, const Run::Cand w, const HostProblem& hp) {
   const int64_t shift = w.good - run.base_good;
   std::fill(run.memo_ok.begin(), run.memo_ok.end(), 0);
   for (const Run::Cand& c : run.cands)
-    if (c.r1 != w.r1 && c.r1 != w.r2 && c.r2 != w.r1 && c.r2 != w.r2) {
+    if (c.kind != 3 && c.kind != 4 &&  // values only for candidates that were evaluated
+        c.r1 != w.r1 && c.r1 != w.r2 && c.r2 != w.r1 && c.r2 != w.r2) {
       const size_t mi = (size_t)c.m * run.G + c.g;
       run.memo_ok[mi] = 1;
       run.memo_good[mi] = c.good + shift;
@@ -831,6 +897,8 @@ static void apply_winner(Run& run, const Run::Cand w, const HostProblem& hp) {
       w.good - run.base_good + run.cgood[w.r1] + (w.r2 != w.r1 ? run.cgood[w.r2] : 0);
   run.parent[w.r1] = w.r2;  // unite comp(g*) and comp(m*)
   run.cgood[w.r2] = merged;
+  if (w.r1 != w.r2) run.cn[w.r2] += run.cn[w.r1];
+  run.round = 0;
   run.sel[w.m] |= 1ULL << w.g;
   run.used[w.g] += hp.mem_at(w.m, run.cfg[w.g]);
   run.base_good = w.good;
@@ -938,23 +1006,55 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
         c.good = s->h_good[c.ref];
         if (restricted)  // good(base) - good_base(comp(g)) - good_base(comp(m)) + good_c(K_c)
           c.good += run.base_good - run.cgood[c.r1] - (c.r2 != c.r1 ? run.cgood[c.r2] : 0);
-      } else if (c.kind == 2) {
-        c.good = run.cands[c.ref].good;
       }
     }
   }
-  if (s->beam > 1) return apply_beam(s, st);
+  if (s->beam > 1) {
+    for (size_t b = 0; b < s->base_run.size(); ++b) {
+      Run& run = s->runs[s->base_run[b]];
+      for (Run::Cand& c : run.cands)
+        if (c.kind == 2) c.good = run.cands[c.ref].good;
+    }
+    return apply_beam(s, st);
+  }
   std::vector<int32_t> winner_run;
   std::vector<const Run::Cand*> winner;
+  std::vector<int32_t> pending;  // runs whose step needs another round (bounding)
   for (size_t b = 0; b < s->base_run.size(); ++b) {
     Run& run = s->runs[s->base_run[b]];
     int64_t bi = -1, bg = -1;
     for (size_t i = 0; i < run.cands.size(); ++i) {
       const Run::Cand& c = run.cands[i];
-      if (c.good > bg) {  // first maximum in (m, g) order: lowest index on ties (C12)
+      // evaluated candidates only; a duplicate never beats its representative
+      // (same good, later index).  First maximum in (m, g) order: lowest
+      // index on ties (C12)
+      if ((c.kind == 0 || c.kind == 1 || c.kind == 5) && c.good > bg) {
         bg = c.good;
         bi = (int64_t)i;
       }
+    }
+    if (s->bound) {
+      bool left = false;
+      for (size_t i = 0; i < run.cands.size(); ++i) {
+        Run::Cand& c = run.cands[i];
+        if (c.kind != 3) continue;
+        if (c.ub < bg || (c.ub == bg && (int64_t)i > bi)) c.kind = 4;  // cannot be the argmax
+        else left = true;
+      }
+      if (left) {  // another round of this step: the deferred candidates that may still win
+        for (Run::Cand& c : run.cands)
+          if (c.kind == 0) c.kind = 5;
+        run.round = 1;
+        pending.push_back(s->base_run[b]);
+        continue;
+      }
+    }
+    for (Run::Cand& c : run.cands) {
+      if (c.kind == 4) ++s->bounded;
+      if (c.kind != 2) continue;
+      const Run::Cand& rep = run.cands[c.ref];
+      if (rep.kind == 4) c.kind = 4;  // no value: its representative was bounded out
+      else c.good = rep.good;
     }
     if (bi < 0) return sfail(s, ASIM_ERANGE, "step results contain no feasible candidate");
     winner_run.push_back(s->base_run[b]);
@@ -988,7 +1088,7 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
     if (keep) std::swap(s->cs_prev, s->cs_cur);
     s->have_prev = keep;
     // before the bases change: the update simulates from the old ones
-    asim_status rc = update_states(s, winner_run, winner, st);
+    asim_status rc = update_states(s, winner_run, winner, st, nullptr, &pending);
     if (rc) return rc;
   }
   for (size_t i = 0; i < winner_run.size(); ++i) {
@@ -1350,6 +1450,7 @@ asim_status asim_search_result_get(const asim_search* s, asim_search_result* out
   out->evaluated = s->evaluated;
   out->request_evals = s->evaluated * s->ctx->n;
   out->memo_hits = s->memo_hits;
+  out->bounded = s->bounded;
   if (s->bucketed) {  // the concatenated placement (groups of bucket 1 first)
     int32_t bc = -1;
     int64_t bg = 0;

@@ -23,8 +23,10 @@ def _compare(sim, prob, tr, dedup_modes=(False, True)):
     ref = osearch.alg2(prob, tr)
     sim.set_problem(prob)
     sim.set_trace(tr.arrival_ns, tr.model)
-    for dedup, prune in [(d, p) for d in dedup_modes for p in (False, True)]:
-        res = sim.search(dedup=dedup, prune=prune)
+    for dedup, prune, bounding in [(d, p, p) for d in dedup_modes for p in (False, True)]:
+        res = sim.search(dedup=dedup, prune=prune, bounding=bounding)
+        if not bounding:
+            assert res.bounded == 0
         assert len(res.runs) == len(ref["runs"])
         for r_gpu, r_ref in zip(res.runs, ref["runs"]):
             if r_gpu["pruned_at"] >= 0:  # stopped early: provably never the best run
@@ -102,3 +104,22 @@ def test_pruning_stops_hopeless_runs(sim):
     for i in pruned:
         assert full.runs[i]["best_good"] < full.best_good
     assert pr.evaluated < full.evaluated
+
+
+def test_bounding_skips_candidates_exactly(sim):
+    """Exact candidate bounding (include/asim.h, spec->cand_bound): a step
+    needs only its argmax, so candidates whose component bound cannot beat
+    the best value found are never simulated; every run's selections are
+    those of the search without it."""
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "MoE-1.3B") for i in range(3)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=5.0)
+    tr = traces.maf2_shaped(8, len(names), 10.0, 300.0)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    a = sim.search(dedup=False, prune=False, bounding=False)
+    b = sim.search(dedup=False, prune=False, bounding=True)
+    assert b.bounded > 0 and b.evaluated < a.evaluated
+    assert (a.best_run, a.best_good) == (b.best_run, b.best_good)
+    for ra, rb in zip(a.runs, b.runs):
+        assert ra["best_good"] == rb["best_good"]
+        np.testing.assert_array_equal(ra["host_mask"], rb["host_mask"])

@@ -9,6 +9,9 @@ seeded input generators in ``workloads/``.
 * ``libasim_oracle.so`` (des.cpp): event-driven simulator with explicit FIFO
   queues, an event heap and dry-run dispatch prediction (§4.3, §6
   P:812-813).
+* ``simulate_batching`` / ``evaluate_batching`` (des.cpp): the dynamic
+  batching variant of §5.4: per-model request queues, batches formed
+  by a group when it becomes available, explicit batch events.
 * ``oracle.search``: Alg. 1 (k = 1), Alg. 2 single bucket
    and brute force over every placement of tiny instances.
 
@@ -77,6 +80,13 @@ def lib():
             L.asim_oracle_evaluate.argtypes = [P, T, ctypes.c_int64, ctypes.c_int32, vp, vp,
                                                ctypes.c_int32, vp, vp, vp]
             L.asim_oracle_evaluate.restype = ctypes.c_int32
+            L.asim_oracle_simulate_batching.argtypes = [P, T, ctypes.c_int32, vp, vp, vp,
+                                                        ctypes.c_int32, vp, vp, vp, vp, vp]
+            L.asim_oracle_simulate_batching.restype = ctypes.c_int32
+            L.asim_oracle_evaluate_batching.argtypes = [P, T, ctypes.c_int64, ctypes.c_int32, vp,
+                                                        vp, vp, ctypes.c_int32, ctypes.c_int32,
+                                                        vp, vp, vp]
+            L.asim_oracle_evaluate_batching.restype = ctypes.c_int32
             L.asim_oracle_error.restype = ctypes.c_char_p
             L.asim_oracle_hardware_threads.restype = ctypes.c_int32
             _lib = L
@@ -168,6 +178,51 @@ def evaluate(prob, trace, group_cfg, host_mask, threads: int = 0, per_model: boo
     pm = np.zeros((C, M), np.int64) if per_model else None
     _check(lib().asim_oracle_evaluate(ctypes.byref(op.c), ctypes.byref(ot.c), C, G, _ptr(cfg),
                                       _ptr(mask), int(threads), _ptr(good), _ptr(sl), _ptr(pm)))
+    return good, sl, pm
+
+
+def simulate_batching(prob, trace, placement, stage_inc_ns, max_batch: int,
+                      detail: bool = False) -> dict:
+    """Dynamic batching variant (§5.4) of simulate(): a batch of k
+    requests occupies stage j for stage_ns + (k-1) * stage_inc_ns[m][p][j]."""
+    op, ot = _wrap(prob, trace)
+    M, N = op.prob.num_models, len(ot.arrival)
+    cfg = np.ascontiguousarray(placement.group_cfg, dtype=np.int32)
+    mask = np.ascontiguousarray(placement.host_mask, dtype=np.uint64)
+    inc = np.ascontiguousarray(stage_inc_ns, dtype=np.int64)
+    assert inc.shape == np.shape(op.prob.stage_ns)
+    good = np.zeros(1, np.int64)
+    sl = np.zeros(1, np.int64)
+    pm = np.zeros(M, np.int64)
+    fin = np.zeros(N, np.int64) if detail else None
+    srv = np.zeros(N, np.int32) if detail else None
+    _check(lib().asim_oracle_simulate_batching(ctypes.byref(op.c), ctypes.byref(ot.c), len(cfg),
+                                               _ptr(cfg), _ptr(mask), _ptr(inc), int(max_batch),
+                                               _ptr(good), _ptr(sl), _ptr(pm), _ptr(fin),
+                                               _ptr(srv)))
+    out = dict(good=int(good[0]), sum_latency_ns=int(sl[0]), good_per_model=pm)
+    if detail:
+        out.update(finish_ns=fin, served_by=srv)
+    return out
+
+
+def evaluate_batching(prob, trace, group_cfg, host_mask, stage_inc_ns, max_batch: int,
+                      threads: int = 0, per_model: bool = False):
+    """Batch of C placements under dynamic batching; same shapes as evaluate()."""
+    op, ot = _wrap(prob, trace)
+    cfg = np.ascontiguousarray(group_cfg, dtype=np.int32)
+    mask = np.ascontiguousarray(host_mask, dtype=np.uint64)
+    inc = np.ascontiguousarray(stage_inc_ns, dtype=np.int64)
+    assert inc.shape == np.shape(op.prob.stage_ns)
+    C, G = cfg.shape
+    M = op.prob.num_models
+    assert mask.shape == (C, M)
+    good = np.zeros(C, np.int64)
+    sl = np.zeros(C, np.int64)
+    pm = np.zeros((C, M), np.int64) if per_model else None
+    _check(lib().asim_oracle_evaluate_batching(ctypes.byref(op.c), ctypes.byref(ot.c), C, G,
+                                               _ptr(cfg), _ptr(mask), _ptr(inc), int(max_batch),
+                                               int(threads), _ptr(good), _ptr(sl), _ptr(pm)))
     return good, sl, pm
 
 

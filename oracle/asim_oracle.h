@@ -70,6 +70,24 @@ int32_t asim_oracle_evaluate(const asim_oracle_problem* prob, const asim_oracle_
                              int32_t num_threads, int64_t* good, int64_t* sum_latency_ns,
                              int64_t* good_per_model);
 
+/* Dynamic batching variant (§5.4, C31-C37): same outputs as
+ * above.  stage_inc_ns [M][P][max_stages] >= 0: a batch of k requests occupies
+ * stage j for stage_ns + (k-1) * stage_inc_ns; max_batch >= 1; at most 64
+ * models; every first-stage latency >= 1 ns. */
+int32_t asim_oracle_simulate_batching(const asim_oracle_problem* prob,
+                                      const asim_oracle_trace* tr, int32_t num_groups,
+                                      const int32_t* group_cfg, const uint64_t* host_mask,
+                                      const int64_t* stage_inc_ns, int32_t max_batch,
+                                      int64_t* good, int64_t* sum_latency_ns,
+                                      int64_t* good_per_model, int64_t* finish_ns,
+                                      int32_t* served_by);
+int32_t asim_oracle_evaluate_batching(const asim_oracle_problem* prob,
+                                      const asim_oracle_trace* tr, int64_t num_candidates,
+                                      int32_t max_groups, const int32_t* group_cfg,
+                                      const uint64_t* host_mask, const int64_t* stage_inc_ns,
+                                      int32_t max_batch, int32_t num_threads, int64_t* good,
+                                      int64_t* sum_latency_ns, int64_t* good_per_model);
+
 int32_t asim_oracle_hardware_threads(void);
 const char* asim_oracle_error(void);
 

@@ -245,6 +245,267 @@ int32_t simulate(const asim_oracle_problem* prob, const asim_oracle_trace* tr, i
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Dynamic batching variant (§5.4 "Batching strategy"; §4.3).
+//
+//   "When a request arrives, it will get executed immediately if any device
+//    group is available.  Otherwise, it will be put into a per-model requests
+//    queue for batching.  When a device group becomes idle, it will choose a
+//    model which has a replica on it and batch as many requests as possible
+//    from the requests queue of the model while satisfying the SLO
+//    requirements."
+//   "the execution latency grows linearly with the batch size"
+//
+// Readings (C31-C37): a batch of k requests of model m occupies
+// stage j of a group with config p for stage_ns[m][p][j] + (k-1) *
+// stage_inc_ns[m][p][j]; tail_ns is added to the finish only (C4) and does not
+// grow with k.  A group is "available" when its first stage is idle (a
+// pipeline accepts the next batch once its first stage is free).  An arrival
+// that finds available hosting groups runs alone on the one with the earliest
+// predicted finish (lowest index on ties) or is rejected if even that misses
+// its SLO; otherwise it waits in its model's FIFO.  A group that becomes
+// available picks, among its hosted models with waiting requests, the one
+// whose head request came first in the trace; a head that misses its SLO even
+// alone is rejected (final) and the choice is repeated; otherwise the batch is
+// the longest queue prefix of size <= max_batch whose members all meet their
+// SLO.  Groups that become available at the same time choose in ascending
+// index order, after every stage completion at that time and before any
+// arrival at that time (C6).
+// ---------------------------------------------------------------------------
+
+struct BBatch {
+  int m;
+  std::vector<int64_t> reqs;
+  int64_t predicted = -1;
+};
+
+struct BStage {
+  std::deque<int64_t> queue;  // batch ids
+  int64_t busy = -1;          // batch id in service
+  int64_t busy_until = 0;
+};
+
+struct BGroup {
+  int cfg = -1;
+  std::vector<BStage> st;
+};
+
+struct BProblem {
+  Problem P;
+  const int64_t* inc;
+  int64_t service(int m, int cfg, int k, int64_t size) const {
+    return P.stage(m, cfg, k) +
+           (size - 1) * inc[((int64_t)m * P.p->num_configs + cfg) * P.p->max_stages + k];
+  }
+};
+
+// Dry run: copy group `grp`, append a batch of `size` requests of model m at
+// its first stage at time t, run the copy alone until that batch leaves its
+// last stage; return that time + tail[m][cfg].
+int64_t dry_run_batch(const BProblem& B, const BGroup& grp, const std::vector<BBatch>& batches,
+                      int m, int64_t size, int64_t t) {
+  BGroup g = grp;
+  const int s = B.P.stages(g.cfg);
+  const int64_t probe = -2;  // id of the probe batch in the copy
+  auto model_of = [&](int64_t id) { return id == probe ? m : batches[id].m; };
+  auto size_of = [&](int64_t id) { return id == probe ? size : (int64_t)batches[id].reqs.size(); };
+  g.st[0].queue.push_back(probe);
+  std::priority_queue<Done, std::vector<Done>, std::greater<Done>> ev;
+  int64_t seq = 0;
+  auto try_start = [&](int k, int64_t now) {
+    BStage& S = g.st[k];
+    if (S.busy == -1 && !S.queue.empty()) {
+      S.busy = S.queue.front();
+      S.queue.pop_front();
+      S.busy_until = now + B.service(model_of(S.busy), g.cfg, k, size_of(S.busy));
+      ev.push(Done{S.busy_until, seq++, 0, k, S.busy});
+    }
+  };
+  for (int k = 0; k < s; ++k)
+    if (g.st[k].busy != -1) ev.push(Done{g.st[k].busy_until, seq++, 0, k, g.st[k].busy});
+  try_start(0, t);
+  while (!ev.empty()) {
+    Done e = ev.top();
+    ev.pop();
+    g.st[e.k].busy = -1;
+    if (e.k + 1 < s) {
+      g.st[e.k + 1].queue.push_back(e.req);
+      try_start(e.k + 1, e.time);
+    } else if (e.req == probe) {
+      return e.time + B.P.tail(m, g.cfg);
+    }
+    try_start(e.k, e.time);
+  }
+  return std::numeric_limits<int64_t>::max();  // unreachable
+}
+
+int32_t simulate_batching(const asim_oracle_problem* prob, const asim_oracle_trace* tr, int32_t G,
+                          const int32_t* group_cfg, const uint64_t* host_mask,
+                          const int64_t* stage_inc, int32_t max_batch, int64_t* good_out,
+                          int64_t* sum_out, int64_t* per_model, int64_t* finish_ns,
+                          int32_t* served_by) {
+  BProblem B{Problem{prob}, stage_inc};
+  const int M = prob->num_models;
+  std::vector<BGroup> groups(G);
+  for (int g = 0; g < G; ++g) {
+    groups[g].cfg = group_cfg[g];
+    if (group_cfg[g] >= 0) groups[g].st.resize(B.P.stages(group_cfg[g]));
+  }
+  std::vector<std::deque<int64_t>> Q(M);  // per-model request queues
+  std::vector<BBatch> batches;
+  std::vector<int64_t> good_m(M, 0);
+  int64_t good = 0, sum_lat = 0;
+  if (finish_ns)
+    for (int64_t i = 0; i < tr->n; ++i) finish_ns[i] = -1;
+  if (served_by)
+    for (int64_t i = 0; i < tr->n; ++i) served_by[i] = -1;
+  auto hosts = [&](int m, int g) { return ((host_mask[m] >> g) & 1ULL) != 0; };
+
+  std::priority_queue<Done, std::vector<Done>, std::greater<Done>> ev;
+  int64_t seq = 0;
+  auto try_start = [&](int g, int k, int64_t now) {
+    BStage& S = groups[g].st[k];
+    if (S.busy == -1 && !S.queue.empty()) {
+      S.busy = S.queue.front();
+      S.queue.pop_front();
+      const BBatch& b = batches[S.busy];
+      S.busy_until = now + B.service(b.m, groups[g].cfg, k, (int64_t)b.reqs.size());
+      ev.push(Done{S.busy_until, seq++, g, k, S.busy});
+    }
+  };
+  auto available = [&](int g) {
+    return groups[g].cfg >= 0 && groups[g].st[0].busy == -1 && groups[g].st[0].queue.empty();
+  };
+  auto start_batch = [&](int g, int m, std::vector<int64_t> reqs, int64_t predicted, int64_t t) {
+    BBatch b;
+    b.m = m;
+    b.reqs = std::move(reqs);
+    b.predicted = predicted;
+    if (served_by)
+      for (int64_t r : b.reqs) served_by[r] = g;
+    batches.push_back(std::move(b));
+    groups[g].st[0].queue.push_back((int64_t)batches.size() - 1);
+    try_start(g, 0, t);
+  };
+  // An available group forms one batch at time t (or rejects heads and stays idle).
+  auto form_batch = [&](int g, int64_t t) {
+    for (;;) {
+      int bm = -1;
+      for (int m = 0; m < M; ++m)  // hosted model whose head came first in the trace
+        if (hosts(m, g) && !Q[m].empty() && (bm < 0 || Q[m].front() < Q[bm].front())) bm = m;
+      if (bm < 0) return;
+      const int64_t limit = std::min<int64_t>(max_batch, (int64_t)Q[bm].size());
+      int64_t K = 0, fK = 0;
+      for (int64_t k = 1; k <= limit; ++k) {  // longest prefix whose members all meet the SLO
+        const int64_t f = dry_run_batch(B, groups[g], batches, bm, k, t);
+        bool ok = true;
+        for (int64_t j = 0; j < k; ++j)
+          if (f - tr->arrival_ns[Q[bm][j]] > prob->slo_ns[bm]) ok = false;
+        if (ok) {
+          K = k;
+          fK = f;
+        }
+      }
+      if (K == 0) {  // the head misses its SLO even alone: rejected
+        Q[bm].pop_front();
+        continue;
+      }
+      std::vector<int64_t> reqs(Q[bm].begin(), Q[bm].begin() + K);
+      Q[bm].erase(Q[bm].begin(), Q[bm].begin() + K);
+      start_batch(g, bm, std::move(reqs), fK, t);
+      return;
+    }
+  };
+  auto on_done = [&](const Done& e) {
+    BGroup& grp = groups[e.g];
+    grp.st[e.k].busy = -1;
+    const int s = (int)grp.st.size();
+    if (e.k + 1 < s) {
+      grp.st[e.k + 1].queue.push_back(e.req);
+      try_start(e.g, e.k + 1, e.time);
+    } else {
+      const BBatch& b = batches[e.req];
+      const int64_t fin = e.time + B.P.tail(b.m, grp.cfg);
+      if (fin != b.predicted) {
+        g_err = "internal: batching dry-run prediction mismatch";
+        std::abort();
+      }
+      for (int64_t r : b.reqs) {
+        good += 1;
+        sum_lat += fin - tr->arrival_ns[r];
+        good_m[b.m] += 1;
+        if (finish_ns) finish_ns[r] = fin;
+      }
+    }
+    try_start(e.g, e.k, e.time);
+  };
+
+  int64_t i = 0;
+  for (;;) {
+    const int64_t next_arrival = i < tr->n ? tr->arrival_ns[i] : INT64_MAX;
+    if (!ev.empty() && ev.top().time <= next_arrival) {
+      // every completion at time T, then the groups available at T in index order (C6)
+      const int64_t T = ev.top().time;
+      while (!ev.empty() && ev.top().time == T) {
+        Done e = ev.top();
+        ev.pop();
+        on_done(e);
+      }
+      for (int g = 0; g < G; ++g)
+        if (available(g)) form_batch(g, T);
+      continue;
+    }
+    if (i >= tr->n) break;
+    const int64_t t = tr->arrival_ns[i];
+    const int m = tr->model[i];
+    int best_g = -1;
+    bool any_host = false;
+    int64_t best_f = 0;
+    for (int g = 0; g < G; ++g) {
+      if (!hosts(m, g)) continue;
+      any_host = true;
+      if (!available(g)) continue;
+      const int64_t f = dry_run_batch(B, groups[g], batches, m, 1, t);
+      if (best_g < 0 || f < best_f) {
+        best_g = g;
+        best_f = f;
+      }
+    }
+    if (!any_host) {
+      // hosted nowhere: rejected (C8)
+    } else if (best_g < 0) {
+      Q[m].push_back(i);  // every hosting group busy: wait for batching
+    } else if (best_f - t <= prob->slo_ns[m]) {
+      start_batch(best_g, m, std::vector<int64_t>{i}, best_f, t);  // executed immediately
+    }  // else: misses its SLO even if executed now: rejected at receipt (C2)
+    ++i;
+  }
+  for (int m = 0; m < M; ++m)
+    if (!Q[m].empty()) {
+      g_err = "internal: requests left waiting at the end";
+      std::abort();
+    }
+  *good_out = good;
+  if (sum_out) *sum_out = sum_lat;
+  if (per_model)
+    for (int m = 0; m < M; ++m) per_model[m] = good_m[m];
+  return 0;
+}
+
+int32_t check_batching(const asim_oracle_problem* p, const int64_t* inc, int32_t max_batch) {
+  if (!inc) return fail("null stage_inc_ns");
+  if (max_batch < 1) return fail("max_batch must be >= 1");
+  if (p->num_models > 64) return fail("batching supports at most 64 models");
+  const int64_t total = (int64_t)p->num_models * p->num_configs * p->max_stages;
+  for (int64_t x = 0; x < total; ++x)
+    if (inc[x] < 0) return fail("negative stage_inc_ns");
+  for (int m = 0; m < p->num_models; ++m)
+    for (int c = 0; c < p->num_configs; ++c)
+      if (p->stage_ns[((int64_t)m * p->num_configs + c) * p->max_stages] < 1)
+        return fail("batching needs a first-stage latency >= 1 ns");
+  return 0;
+}
+
 int32_t check_trace(const asim_oracle_problem* p, const asim_oracle_trace* tr) {
   if (!tr || tr->n < 0) return fail("bad trace");
   if (tr->n > 0 && (!tr->arrival_ns || !tr->model)) return fail("null trace array");
@@ -306,6 +567,60 @@ int32_t asim_oracle_evaluate(const asim_oracle_problem* prob, const asim_oracle_
       }
       int64_t s = 0;
       simulate(prob, tr, G, cfg + c * G, mask + c * M, &good[c], &s, pm, nullptr, nullptr);
+      if (sum_lat) sum_lat[c] = s;
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t) {
+    int64_t lo = C * t / nthreads, hi = C * (t + 1) / nthreads;
+    th.emplace_back(work, lo, hi);
+  }
+  for (auto& x : th) x.join();
+  return 0;
+}
+
+int32_t asim_oracle_simulate_batching(const asim_oracle_problem* prob,
+                                      const asim_oracle_trace* tr, int32_t G, const int32_t* cfg,
+                                      const uint64_t* mask, const int64_t* stage_inc_ns,
+                                      int32_t max_batch, int64_t* good, int64_t* sum_lat,
+                                      int64_t* per_model, int64_t* finish_ns,
+                                      int32_t* served_by) {
+  if (check_problem(prob) || check_trace(prob, tr) || check_placement(prob, G, cfg, mask) ||
+      check_batching(prob, stage_inc_ns, max_batch))
+    return -1;
+  if (!good) return fail("null good");
+  return simulate_batching(prob, tr, G, cfg, mask, stage_inc_ns, max_batch, good, sum_lat,
+                           per_model, finish_ns, served_by);
+}
+
+int32_t asim_oracle_evaluate_batching(const asim_oracle_problem* prob,
+                                      const asim_oracle_trace* tr, int64_t C, int32_t G,
+                                      const int32_t* cfg, const uint64_t* mask,
+                                      const int64_t* stage_inc_ns, int32_t max_batch,
+                                      int32_t nthreads, int64_t* good, int64_t* sum_lat,
+                                      int64_t* per_model) {
+  if (check_problem(prob) || check_trace(prob, tr) ||
+      check_batching(prob, stage_inc_ns, max_batch))
+    return -1;
+  if (C < 0 || !good) return fail("bad candidates");
+  const int M = prob->num_models;
+  for (int64_t c = 0; c < C; ++c)
+    if (check_placement(prob, G, cfg + c * G, mask + c * M)) return -1;
+  if (nthreads <= 0) nthreads = asim_oracle_hardware_threads();
+  nthreads = (int32_t)std::max<int64_t>(1, std::min<int64_t>(nthreads, C));
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int64_t c = lo; c < hi; ++c) {
+      int64_t* pm = per_model ? per_model + c * M : nullptr;
+      if (!feasible(prob, G, cfg + c * G, mask + c * M)) {
+        good[c] = -1;
+        if (sum_lat) sum_lat[c] = 0;
+        if (pm)
+          for (int m = 0; m < M; ++m) pm[m] = 0;
+        continue;
+      }
+      int64_t s = 0;
+      simulate_batching(prob, tr, G, cfg + c * G, mask + c * M, stage_inc_ns, max_batch,
+                        &good[c], &s, pm, nullptr, nullptr);
       if (sum_lat) sum_lat[c] = s;
     }
   };

@@ -131,3 +131,23 @@ def s4(seed=0, rate=8.0, cv=4.0, duration=86400.0, slo_scale=5.0):
 
 
 CONFIGS = {"S1": s1, "S2": s2, "S3": s3, "S4": s4}
+
+
+# ------------------------------------------------------------- dynamic batching (§5.4)
+def batch_increment_ns(stage_ns, delta: float) -> np.ndarray:
+    """Per-stage increment of a batched stage: a batch of k occupies stage j for
+    stage_ns + (k-1) * round(delta * stage_ns) ns, i.e. "the execution latency
+    grows linearly with the batch size" with slope delta (SPEC S:34,
+    L(1)(1 + delta (k-1))).  Input generation only (round half even, once)."""
+    return np.rint(np.asarray(stage_ns, dtype=np.float64) * delta).astype(np.int64)
+
+
+def s1_batching(seed=0, rate_per_model=4.0, cv=4.0, duration=600.0, slo_scale=5.0,
+                delta=0.9):
+    """§5.4 setup: model set S1, "synthetic Gamma Process traffic
+    with an average rate of 4 requests/s and a CV of 4 for each model".
+    Returns (problem, trace, stage_inc_ns)."""
+    prob = table1_problem("S1", 16, slo_scale)
+    M = prob.num_models
+    tr = traces.independent_gamma(seed, [rate_per_model] * M, cv, duration)
+    return prob, tr, batch_increment_ns(prob.stage_ns, delta)

@@ -217,6 +217,46 @@ asim_status asim_evaluate(asim_ctx* ctx, const asim_candidates* cands, asim_resu
 asim_status asim_evaluate_deltas(asim_ctx* ctx, const asim_deltas* cands, asim_results* out,
                                  void* cuda_stream);
 
+/* ------------------------------------------------------ dynamic batching */
+/* The batching variant of the simulator (§5.4 "Batching strategy", P:173:
+ * "When a request arrives, it will get executed immediately if any device
+ * group is available.  Otherwise, it will be put into a per-model requests
+ * queue for batching.  When a device group becomes idle, it will choose a
+ * model which has a replica on it and batch as many requests as possible from
+ * the requests queue of the model while satisfying the SLO requirements";
+ * latency "grows linearly with the batch size").  Readings C31-C37
+ * (DESIGN.md):
+ *   - a batch of k requests of model m occupies stage j of a group with
+ *     config p for stage_ns[m][p][j] + (k-1) * stage_inc_ns[m][p][j];
+ *     tail_ns is added to the finish only and does not grow with k;
+ *   - a group is available when its first stage is idle;
+ *   - an arrival that finds available hosting groups runs alone on the one
+ *     with the earliest finish (ties -> lowest index), or is rejected if even
+ *     that misses its SLO; otherwise it waits in its model's FIFO;
+ *   - a group that becomes available takes, among its hosted models with
+ *     waiting requests, the one whose head request is earliest in the trace;
+ *     a head that misses its SLO even alone is rejected and the choice
+ *     repeated; else the batch is the longest queue prefix (<= max_batch)
+ *     whose members all meet the SLO;
+ *   - groups available at the same time choose in ascending index, after
+ *     every completion and before every arrival at that time (C6).
+ * stage_inc_ns: [M][P][max_stages] int64 >= 0, HOST memory, copied.
+ * Candidates as for asim_evaluate (full placements, infeasible -> good = -1).
+ * Outputs: good, sum_latency_ns, good_per_model, argmax as for asim_evaluate;
+ * busy_ns must be NULL (ASIM_EINVAL).
+ * Errors: ASIM_ERANGE if M > 64, max_batch outside [1, 2^20], an increment
+ * < 0, a first-stage latency stage_ns[m][p][0] < 1 ns, batched stages + tail
+ * > 2^60 or max arrival + n * max batched service >= 2^62, or the placement's
+ * state does not fit shared memory; ASIM_EINVAL for null pointers. */
+typedef struct {
+  int32_t max_batch;
+  const int64_t* stage_inc_ns;
+} asim_batching;
+
+asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
+                                   const asim_batching* opt, asim_results* out,
+                                   void* cuda_stream);
+
 /* SLO attainment = good / n; n == 0 -> 1.0; good < 0 -> -1.0. */
 double asim_attainment(int64_t good, int64_t n);
 

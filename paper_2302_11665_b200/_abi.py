@@ -67,6 +67,10 @@ class asim_bucket_result(ctypes.Structure):
                 ("bucket_run", vp)]
 
 
+class asim_batching(ctypes.Structure):
+    _fields_ = [("max_batch", i32), ("stage_inc_ns", vp)]
+
+
 class asim_search_result(ctypes.Structure):
     _fields_ = [("best_run", i32), ("best_good", i64), ("num_groups", i32), ("group_cfg", vp),
                 ("host_mask", vp), ("steps", i64), ("candidates", i64), ("evaluated", i64),
@@ -104,6 +108,8 @@ asim_set_trace = _bind("asim_set_trace", i32, [vp, i64, vp, vp, i32, vp])
 asim_evaluate = _bind("asim_evaluate", i32, [vp, _P(asim_candidates), _P(asim_results), vp])
 asim_evaluate_deltas = _bind("asim_evaluate_deltas", i32,
                              [vp, _P(asim_deltas), _P(asim_results), vp])
+asim_evaluate_batching = _bind("asim_evaluate_batching", i32,
+                               [vp, _P(asim_candidates), _P(asim_batching), _P(asim_results), vp])
 asim_attainment = _bind("asim_attainment", ctypes.c_double, [i64, i64])
 asim_search_create = _bind("asim_search_create", i32, [vp, _P(asim_search_spec), _P(vp)])
 asim_search_destroy = _bind("asim_search_destroy", None, [vp])

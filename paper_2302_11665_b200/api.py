@@ -179,6 +179,27 @@ class Simulator:
         return self._run(A.asim_evaluate, cands, C, G, per_model, sum_latency, argmax, busy,
                          stream)
 
+    def evaluate_batching(self, group_cfg, host_mask, stage_inc_ns, max_batch: int,
+                          per_model=False, sum_latency=True, argmax=True, stream=None) -> dict:
+        """Dynamic batching variant (§5.4, include/asim.h): full
+        candidates as in evaluate(); stage_inc_ns [M, P, S] int64 -- a batch of
+        k occupies stage j for stage_ns + (k - 1) * stage_inc_ns."""
+        cfg = _host(group_cfg, np.int32)
+        mask = _host(host_mask, np.uint64)
+        inc = _host(stage_inc_ns, np.int64)
+        C, G = cfg.shape
+        cands = A.asim_candidates(C, G, _ptr(cfg), _ptr(mask), A.ASIM_HOST)
+        opt = A.asim_batching(int(max_batch), _ptr(inc))
+        good = np.zeros(C, np.int64)
+        sl = np.zeros(C, np.int64) if sum_latency else None
+        pm = np.zeros((C, self.M), np.int64) if per_model else None
+        am = np.zeros(1, np.int64) if argmax else None
+        res = A.asim_results(_ptr(good), _ptr(sl), _ptr(pm), _ptr(am), A.ASIM_HOST, None)
+        self._check(A.asim_evaluate_batching(self.h, ctypes.byref(cands), ctypes.byref(opt),
+                                             ctypes.byref(res), _stream_ptr(stream)))
+        return dict(good=good, sum_latency_ns=sl, good_per_model=pm,
+                    argmax=int(am[0]) if argmax else None)
+
     def evaluate_deltas(self, base_cfg, base_mask, cand_base, cand_model, cand_group,
                         per_model=False, sum_latency=True, argmax=True, busy=False,
                         stream=None) -> dict:

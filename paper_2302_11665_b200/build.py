@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libasim.so")
-SOURCES = ["ctx.cpp", "search.cpp", "chunked.cpp", "sim.cu", "chunk.cu"]
+SOURCES = ["ctx.cpp", "search.cpp", "chunked.cpp", "sim.cu", "chunk.cu", "batch.cu"]
 HEADERS = ["asim_internal.h", "ctx.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

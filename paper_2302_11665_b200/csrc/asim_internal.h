@@ -65,6 +65,19 @@ cudaError_t launch_simulate(const DevProblem& pr, const DevTrace& tr, const DevB
 cudaError_t launch_argmax(const int64_t* good, int64_t C, int64_t* argmax_out,
                           cudaStream_t stream, int64_t* launches);
 
+// Dynamic batching variant (batch.cu, §5.4): batch-size increments and
+// the trace's per-model request lists (CSR by model, ascending trace index).
+struct DevBatching {
+  int64_t max_batch;       // >= 1
+  const int64_t* inc;      // [M][P][S] stage increment per extra batch member
+  const int32_t* moff;     // [M+1]
+  const int32_t* midx;     // [n] trace indices grouped by model
+};
+size_t batching_smem_per_warp(int32_t slots, int32_t G, int32_t M);
+cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevBatch& b,
+                            const DevBatching& bp, int32_t slots, const DevOut& out,
+                            cudaStream_t stream, int64_t* launches);
+
 }  // namespace asim
 
 namespace asim {

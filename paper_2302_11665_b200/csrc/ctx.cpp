@@ -294,7 +294,8 @@ void asim_destroy(asim_ctx* ctx) {
   {
     DeviceGuard dg(ctx->device);
     DBuf* bufs[] = {&ctx->d_stage, &ctx->d_tail, &ctx->d_slo, &ctx->d_cfg_stages,
-                    &ctx->d_arrival, &ctx->d_model, &ctx->d_base_cfg, &ctx->d_base_mask,
+                    &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc,
+                    &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group,
                     &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm, &ctx->d_busy,
                     &ctx->d_argmax, &ctx->d_counter, &ctx->d_walked, &ctx->c_items, &ctx->c_begin,
@@ -488,7 +489,7 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
   if (!ctx) return ASIM_EINVAL;
   if (ctx->broken) return asim_fail(ctx, ASIM_ECUDA, "context unusable after a CUDA error");
   if (!ctx->has_problem) return asim_fail(ctx, ASIM_ESTATE, "asim_set_problem not called");
-  if (n < 0 || n > (int64_t(1) << 40)) return asim_fail(ctx, ASIM_ERANGE, "n out of range");
+  if (n < 0 || n > (int64_t(1) << 31) - 1) return asim_fail(ctx, ASIM_ERANGE, "n out of range");
   DeviceGuard dg(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   std::vector<int64_t> a;
@@ -512,8 +513,18 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
     ap[i] = a[i];
     mp[i] = (uint16_t)m[i];
   }
+  // per-model request lists (CSR, ascending trace index) for the batching kernel
+  std::vector<int32_t> moff(ctx->hp.M + 1, 0), midx(n > 0 ? n : 1, 0);
+  for (int64_t i = 0; i < n; ++i) ++moff[m[i] + 1];
+  for (int32_t k = 0; k < ctx->hp.M; ++k) moff[k + 1] += moff[k];
+  {
+    std::vector<int32_t> fill(moff.begin(), moff.end() - 1);
+    for (int64_t i = 0; i < n; ++i) midx[fill[m[i]]++] = (int32_t)i;
+  }
   cudaError_t e = upload(ctx->d_arrival, ap, st);
   if (e == cudaSuccess) e = upload(ctx->d_model, mp, st);
+  if (e == cudaSuccess) e = upload(ctx->d_moff, moff, st);
+  if (e == cudaSuccess) e = upload(ctx->d_midx, midx, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload trace");
   ctx->n = n;
@@ -608,6 +619,137 @@ asim_status asim_evaluate(asim_ctx* ctx, const asim_candidates* cands, asim_resu
     hb.cand_ok[c] = ok ? 1 : 0;
   }
   return evaluate_batch(ctx, hb, out, st);
+}
+
+asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
+                                   const asim_batching* opt, asim_results* out,
+                                   void* cuda_stream) {
+  asim_status s = asim_ready(ctx);
+  if (s) return s;
+  if (!cands || !opt) return asim_fail(ctx, ASIM_EINVAL, "null candidates / batching options");
+  if (!opt->stage_inc_ns) return asim_fail(ctx, ASIM_EINVAL, "null stage_inc_ns");
+  if (!out || !out->good) return asim_fail(ctx, ASIM_EINVAL, "null results / good");
+  if (out->busy_ns) return asim_fail(ctx, ASIM_EINVAL, "busy_ns is not produced with batching");
+  if (out->ptr_kind != ASIM_HOST && out->ptr_kind != ASIM_DEVICE)
+    return asim_fail(ctx, ASIM_EINVAL, "bad results ptr_kind");
+  const HostProblem& hp = ctx->hp;
+  const int64_t M = hp.M, P = hp.P, S = hp.S;
+  if (M > 64) return asim_fail(ctx, ASIM_ERANGE, "batching supports at most 64 models");
+  if (opt->max_batch < 1 || opt->max_batch > (1 << 20))
+    return asim_fail(ctx, ASIM_ERANGE, "max_batch must be in [1, 2^20]");
+  const int64_t C = cands->num_candidates;
+  const int32_t G = cands->max_groups;
+  if (C < 0 || C > (int64_t(1) << 31) - 64) return asim_fail(ctx, ASIM_ERANGE, "num_candidates");
+  if (G < 0 || G > ASIM_MAX_GROUPS) return asim_fail(ctx, ASIM_ERANGE, "max_groups out of range");
+  // increments, first-stage latency >= 1 ns (C33), and the time bound of
+  // reading C20 with every service at its largest batch
+  std::vector<int64_t> inc(opt->stage_inc_ns, opt->stage_inc_ns + M * P * S);
+  int64_t max_service = 0;
+  for (int64_t m = 0; m < M; ++m)
+    for (int64_t p = 0; p < P; ++p) {
+      if (hp.stage[(m * P + p) * S] < 1)
+        return asim_fail(ctx, ASIM_ERANGE, "batching needs a first-stage latency >= 1 ns");
+      __int128 tot = hp.tail[m * P + p];
+      for (int64_t k = 0; k < S; ++k) {
+        const int64_t x = inc[(m * P + p) * S + k];
+        if (x < 0) return asim_fail(ctx, ASIM_ERANGE, "stage_inc_ns must be >= 0");
+        if (k < hp.cfg_stages[p])
+          tot += (__int128)hp.stage[(m * P + p) * S + k] + (__int128)(opt->max_batch - 1) * x;
+      }
+      if (tot > kMaxService)
+        return asim_fail(ctx, ASIM_ERANGE, "batched stages + tail must be <= 2^60");
+      max_service = std::max<int64_t>(max_service, (int64_t)tot);
+    }
+  if ((__int128)ctx->max_arrival + (__int128)ctx->n * max_service >= (__int128)kMaxTime)
+    return asim_fail(ctx, ASIM_ERANGE, "max arrival + n * max batched service must stay below 2^62");
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  HostBatch hb;
+  hb.G = G;
+  s = fetch(ctx, hb.base_cfg, cands->group_cfg, C * G, cands->ptr_kind, st, "group_cfg");
+  if (s) return s;
+  s = fetch(ctx, hb.base_mask, cands->host_mask, C * M, cands->ptr_kind, st, "host_mask");
+  if (s) return s;
+  hb.cand_base.resize(C);
+  hb.cand_model.assign(C, -1);
+  hb.cand_group.assign(C, 0);
+  hb.cand_ok.resize(C);
+  std::vector<int64_t> used;
+  for (int64_t c = 0; c < C; ++c) {
+    bool ok = false;
+    s = check_base(ctx, hb.base_cfg.data() + c * G, hb.base_mask.data() + c * M, G, used, &ok,
+                   &hb.slots);
+    if (s) return s;
+    hb.cand_base[c] = (int32_t)c;
+    hb.cand_ok[c] = ok ? 1 : 0;
+  }
+  const size_t smem = 2 * asim::batching_smem_per_warp(hb.slots, G, (int32_t)M);
+  if (smem > 227 * 1024) return asim_fail(ctx, ASIM_ERANGE, "placement too large for batching");
+  const bool want_sum = out->sum_latency_ns != nullptr;
+  const bool want_pm = out->good_per_model != nullptr;
+  const bool want_arg = out->argmax != nullptr;
+  asim::DevOut dout{};
+  cudaError_t e = upload(ctx->d_inc, inc, st);
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "upload increments");
+  if (out->ptr_kind == ASIM_DEVICE) {
+    dout.good = out->good;
+    dout.sum_latency = out->sum_latency_ns;
+    dout.good_per_model = out->good_per_model;
+  } else {
+    e = ctx->d_good.ensure(C * 8 + 8);
+    if (e == cudaSuccess && want_sum) e = ctx->d_sum.ensure(C * 8 + 8);
+    if (e == cudaSuccess && want_pm) e = ctx->d_pm.ensure(C * M * 8 + 8);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "allocate results");
+    dout.good = ctx->d_good.as<int64_t>();
+    dout.sum_latency = want_sum ? ctx->d_sum.as<int64_t>() : nullptr;
+    dout.good_per_model = want_pm ? ctx->d_pm.as<int64_t>() : nullptr;
+  }
+  if (want_pm && C > 0) {
+    e = cudaMemsetAsync(dout.good_per_model, 0, C * M * 8, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "memset per-model");
+  }
+  s = asim_upload_batch(ctx, hb, st);
+  if (s) return s;
+  asim::DevBatch b;
+  b.G = G;
+  b.base_cfg = ctx->d_base_cfg.as<int32_t>();
+  b.base_mask = ctx->d_base_mask.as<uint64_t>();
+  b.cand_base = ctx->d_cand_base.as<int32_t>();
+  b.cand_model = ctx->d_cand_model.as<int32_t>();
+  b.cand_group = ctx->d_cand_group.as<int32_t>();
+  b.cand_ok = ctx->d_cand_ok.as<uint8_t>();
+  b.cand_kmask = nullptr;
+  b.cand_gmask = nullptr;
+  b.C = C;
+  asim::DevBatching bp;
+  bp.max_batch = opt->max_batch;
+  bp.inc = ctx->d_inc.as<int64_t>();
+  bp.moff = ctx->d_moff.as<int32_t>();
+  bp.midx = ctx->d_midx.as<int32_t>();
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (ctx->profiling) {
+    if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
+      return asim_cuda(ctx, cudaGetLastError(), "event create");
+    cudaEventRecord(ev0, st);
+  }
+  e = asim::launch_batching(ctx->dev_problem(), ctx->dev_trace(), b, bp, hb.slots, dout, st,
+                            &ctx->launches);
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "batching kernel");
+  if (ctx->profiling) {
+    cudaEventRecord(ev1, st);
+    ctx->events.emplace_back(ev0, ev1);
+    ++ctx->sim_launches;
+    int64_t ok = 0;
+    for (int64_t i = 0; i < C; ++i) ok += hb.cand_ok[i];
+    ctx->request_evals += ok * ctx->n;
+  }
+  if (want_arg) {
+    e = ctx->d_argmax.ensure(8);
+    int64_t* arg_dev = out->ptr_kind == ASIM_DEVICE ? out->argmax : ctx->d_argmax.as<int64_t>();
+    if (e == cudaSuccess) e = asim::launch_argmax(dout.good, C, arg_dev, st, &ctx->launches);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "argmax kernel");
+  }
+  return finish_outputs(ctx, out, C, G, want_sum, want_pm, false, want_arg, st);
 }
 
 asim_status asim_evaluate_deltas(asim_ctx* ctx, const asim_deltas* d, asim_results* out,

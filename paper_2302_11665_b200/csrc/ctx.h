@@ -62,6 +62,8 @@ struct asim_ctx {
   int64_t min_arrival = 0;
   std::vector<int64_t> model_n;  // [M] requests per model in the trace
   DBuf d_arrival, d_model;
+  DBuf d_moff, d_midx;  // per-model request lists (CSR) for the batching kernel
+  DBuf d_inc;           // batching stage increments (asim_evaluate_batching)
 
   // statistics (asim_set_profiling)
   bool profiling = false;

@@ -241,3 +241,150 @@ def test_spec_batching_sanity():
     assert abs(run(1.5, 1.0, 2) - run(1.5, 1.0, 1)) <= 0.005
     b1 = run(8.0, 0.9, 1)
     assert run(8.0, 0.9, 2) >= b1 and run(8.0, 0.9, 4) >= b1
+
+
+# ============================================================ GPU parity (-m gpu)
+def _stack(placements, M):
+    G = max([p.num_groups for p in placements] + [1])
+    cfg = np.full((len(placements), G), -1, np.int32)
+    mask = np.zeros((len(placements), M), np.uint64)
+    for i, p in enumerate(placements):
+        cfg[i, :p.num_groups] = p.group_cfg
+        mask[i] = p.host_mask
+    return cfg, mask
+
+
+@pytest.fixture(scope="module")
+def sim():
+    from paper_2302_11665_b200 import Simulator
+    s = Simulator(0)
+    yield s
+    s.close()
+
+
+def _check(sim, prob, tr, cfg, mask, inc, b):
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    got = sim.evaluate_batching(cfg, mask, inc, b, per_model=True)
+    g, s, pm = oracle.evaluate_batching(prob, tr, cfg, mask, inc, b, per_model=True)
+    np.testing.assert_array_equal(got["good"], g)
+    np.testing.assert_array_equal(got["sum_latency_ns"], s)
+    np.testing.assert_array_equal(got["good_per_model"], pm)
+    want = int(np.argmax(g)) if len(g) and g.max() >= 0 else -1
+    assert got["argmax"] == want
+    return g
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(24))
+def test_gpu_parity_random(sim, seed):
+    """Random small instances (multi-stage groups, shared hosts, zero-latency
+    later stages, duplicate timestamps, unhosted models, finite and infinite
+    SLOs), 70 candidates per call = 2 full warps + a ragged tail."""
+    rng = np.random.default_rng(5000 + seed)
+    prob, tr, _ = random_instance(rng, M=int(rng.integers(1, 5)), P=3, n_req=int(rng.integers(0, 400)),
+                                  dmax=6, tmax=200)
+    prob.stage_ns[:, :, 0] = np.maximum(prob.stage_ns[:, :, 0], 1)
+    inc = rng.integers(0, 4, size=np.shape(prob.stage_ns))
+    pls = []
+    for _ in range(70):
+        G = int(rng.integers(1, 6))
+        cfg = [int(rng.integers(0, prob.num_configs)) for _ in range(G)]
+        groups = [[m for m in range(prob.num_models) if rng.random() < 0.5] for _ in range(G)]
+        pls.append(place(cfg, groups, prob.num_models))
+    cfg, mask = _stack(pls, prob.num_models)
+    b = int(rng.choice([1, 2, 3, 5, 1000]))
+    _check(sim, prob, tr, cfg, mask, inc, b)
+
+
+@pytest.mark.gpu
+def test_gpu_hand_cases(sim):
+    """The hand-worked oracle cases, through the C ABI."""
+    prob = tiny_problem([(1, 1)], [[[10]]], slo=[16])
+    tr = trace_of([(0, 0), (0, 0), (6, 0), (7, 0)])
+    cfg, mask = _stack([place([0], [[0]], 1)], 1)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    got = sim.evaluate_batching(cfg, mask, _inc(prob, 2), 4)
+    assert got["good"][0] == 3 and got["sum_latency_ns"][0] == 10 + 16 + 15
+    prob = tiny_problem([(1, 1)], [[[100]]])
+    tr = trace_of([(0, 0)] * 10)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    got = sim.evaluate_batching(cfg, mask, _inc(prob, 40), 3)
+    assert got["sum_latency_ns"][0] == 100 + 3 * 280 + 3 * 460 + 3 * 640
+
+
+def _s1_placements(prob):
+    """Selective replication and model-parallel groups on 16 devices (§5.4:
+    AlpaServe vs SR with batching)."""
+    M = prob.num_models
+    ix = {c: i for i, c in enumerate(prob.configs)}
+    out = []
+    for size, (s, n) in [(1, (1, 1)), (2, (2, 1)), (2, (1, 2)), (4, (4, 1)), (4, (2, 2)),
+                         (8, (8, 1))]:
+        G = 16 // size
+        groups = [[m for m in range(M) if (m * G // M) % G == g or (m + M // 2) * G // M % G == g]
+                  for g in range(G)]
+        out.append(place([ix[(s, n)]] * G, groups, M))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("delta,b,scale", [(1.0, 2, 1.5), (0.9, 2, 8.0), (0.9, 4, 8.0),
+                                           (0.7, 8, 5.0), (0.9, 1, 5.0)])
+def test_gpu_parity_s1_batching(sim, delta, b, scale):
+    """§5.4 setup (S1, 4 req/s per model, CV 4; 120 s), SR and pipeline /
+    intra-op placements, bit-exact good, latency sums and per-model counts."""
+    prob, tr, inc = configs.s1_batching(seed=1, duration=120.0, slo_scale=scale, delta=delta)
+    cfg, mask = _stack(_s1_placements(prob), prob.num_models)
+    g = _check(sim, prob, tr, cfg, mask, inc, b)
+    assert (g >= 0).all()
+
+
+@pytest.mark.gpu
+def test_gpu_parity_s3_shape(sim):
+    """S3-shaped (60 models, 64 devices, MAF2-shaped bursts), 10-min prefix,
+    random placements of up to 64 groups: bit-exact."""
+    prob, tr = configs.s3(seed=0, duration=600.0)
+    inc = configs.batch_increment_ns(prob.stage_ns, 0.9)
+    rng = np.random.default_rng(7)
+    pls = []
+    for size in (1, 2, 4, 8):
+        for cfg_i, (s, n) in enumerate(prob.configs):
+            if s * n != size:
+                continue
+            G = 64 // size
+            groups = [[m for m in range(60) if rng.random() < 0.08 * size] for _ in range(G)]
+            pls.append(place([cfg_i] * G, groups, 60))
+    cfg, mask = _stack(pls, 60)
+    _check(sim, prob, tr, cfg, mask, inc, 4)
+
+
+@pytest.mark.gpu
+def test_gpu_batching_errors(sim):
+    from paper_2302_11665_b200 import AsimError
+    prob = tiny_problem([(1, 1)], [[[10]]])
+    tr = trace_of([(0, 0)])
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    cfg, mask = _stack([place([0], [[0]], 1)], 1)
+    with pytest.raises(AsimError):
+        sim.evaluate_batching(cfg, mask, _inc(prob), 0)
+    with pytest.raises(AsimError):
+        sim.evaluate_batching(cfg, mask, _inc(prob, -1), 2)
+    z = tiny_problem([(1, 1)], [[[0]]])
+    sim.set_problem(z)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    with pytest.raises(AsimError):
+        sim.evaluate_batching(cfg, mask, _inc(z), 2)
+    big = tiny_problem([(1, 1)], [[[5]]] * 65)
+    sim.set_problem(big)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    with pytest.raises(AsimError):
+        sim.evaluate_batching(np.zeros((1, 1), np.int32), np.zeros((1, 65), np.uint64),
+                              _inc(big), 2)
+    empty = Trace(np.zeros(0, np.int64), np.zeros(0, np.int32))
+    sim.set_problem(prob)
+    sim.set_trace(empty.arrival_ns, empty.model)
+    assert sim.evaluate_batching(cfg, mask, _inc(prob), 2)["good"][0] == 0

@@ -9,21 +9,23 @@
 // size: a batch of k occupies stage j for d_j + (k-1) e_j.
 // Readings C31-C37.
 //
-// One lane simulates one candidate placement over the whole trace.  The
-// per-model FIFO of a candidate is a contiguous run of that model's requests
-// (a request only skips the queue when the queue is empty), so the lane keeps
-// one head index per model into the trace's per-model request list (CSR built
-// by asim_set_trace) plus a bitmask of non-empty queues; the number of
-// requests of each model seen so far is the same for every lane and lives once
-// per warp.  A group's "becomes available" event is its first-stage free time
-// F0; before each arrival at time a, the lane replays the events with F0 <= a
-// in (F0, group) order -- completions at a precede the arrival at a (C6) --
-// and each such group forms at most one batch (first-stage latency >= 1 ns).
-// Only groups hosting a model with a waiting request have an event, so a lane
-// whose queues are empty skips the scan.  State per lane in shared memory:
-// stage free times [slot][lane], per-group hosted-model masks, group table,
-// per-model queue heads; all int64 ns, bit-exact with the oracle's explicit
-// event simulation (oracle/des.cpp simulate_batching).
+// One WARP simulates one candidate placement over the whole trace; every
+// branch is warp-uniform.  Lane l owns groups l and l + 32 (their config,
+// hosted-model mask and stage slots) and models l and l + 32 (queue head,
+// requests seen, per-model good count), all in registers; the stage free
+// times sit in per-warp shared memory.  The per-model FIFO of a candidate is
+// a contiguous run of that model's requests (a request only skips the queue
+// when the queue is empty), so a queue is one head index into the trace's
+// per-model request list (CSR built by asim_set_trace) plus one bit of the
+// warp-uniform mask of non-empty queues.  A group's "becomes available" event
+// is its first-stage free time F0: before each arrival at time a the warp
+// replays the events with F0 <= a in (F0, group) order -- completions at a
+// precede the arrival at a (C6) -- by warp-wide argmins over the lanes'
+// groups; each event forms at most one batch (first-stage latency >= 1 ns).
+// Batch formation is lane-parallel over the batch size: lane j evaluates the
+// tandem recurrence for a batch of j + 1 and a ballot gives the longest
+// feasible prefix.  All int64 ns, bit-exact with the oracle's explicit event
+// simulation (oracle/des.cpp simulate_batching).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,111 +35,170 @@ namespace asim {
 namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr int kWarps = 2;
+constexpr int kWarps = 4;
 
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ int gt_cfg(uint32_t e) { return (int)(e & 0xFFFFu); }
 __device__ __forceinline__ int gt_off(uint32_t e) { return (int)((e >> 16) & 0xFFu); }
 __device__ __forceinline__ int gt_stages(uint32_t e) { return (int)(e >> 24); }
 
-struct Lane {
-  int64_t* F;         // [slots][32] stage free times
-  uint64_t* gm;       // [G][32] models hosted by group g
-  uint32_t* gt;       // [G][32] cfg | first slot | stages
-  int32_t* head;      // [M][32] queue head (position in the model's request list)
-  const int32_t* arrived;  // [M] requests of each model seen so far (warp-shared)
-  int lane;
-};
+// (key, index) argmin over the warp; every lane gets the result.  Ties on
+// the key go to the lowest index.
+__device__ __forceinline__ void warp_argmin(int64_t& key, int& idx) {
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const int64_t k2 = __shfl_xor_sync(FULL, key, w);
+    const int i2 = __shfl_xor_sync(FULL, idx, w);
+    if (k2 < key || (k2 == key && i2 < idx)) {
+      key = k2;
+      idx = i2;
+    }
+  }
+}
 
-// Finish of a batch of k requests of model m entering group g's first stage
-// at time T (tandem recurrence, C5); commit = write the stage departures.
-template <bool kCommit>
-__device__ __forceinline__ int64_t run_batch(const DevProblem& pr, const DevBatching& bp,
-                                             const Lane& L, int g, int m, int64_t T, int64_t k) {
-  const uint32_t e = L.gt[g * 32 + L.lane];
-  const int p = gt_cfg(e), off = gt_off(e), s = gt_stages(e);
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) v += __shfl_xor_sync(FULL, v, w);
+  return v;
+}
+
+// Tandem recurrence (C5) of a batch of k requests of model m entering a group
+// with config p whose stage slots start at F[off], at time T.
+__device__ __forceinline__ int64_t batch_finish(const DevProblem& pr, const DevBatching& bp,
+                                                const int64_t* F, int p, int off, int s, int m,
+                                                int64_t T, int64_t k) {
+  const int64_t row = ((int64_t)m * pr.P + p) * pr.S;
+  const int64_t* d = pr.stage + row;
+  const int64_t* inc = bp.inc + row;
+  int64_t x = T;
+  for (int j = 0; j < s; ++j) x = imax64(x, F[off + j]) + __ldg(d + j) + (k - 1) * __ldg(inc + j);
+  return x + __ldg(pr.tail + (int64_t)m * pr.P + p);
+}
+
+__device__ __forceinline__ void batch_commit(const DevProblem& pr, const DevBatching& bp,
+                                             int64_t* F, int p, int off, int s, int m, int64_t T,
+                                             int64_t k) {
   const int64_t row = ((int64_t)m * pr.P + p) * pr.S;
   const int64_t* d = pr.stage + row;
   const int64_t* inc = bp.inc + row;
   int64_t x = T;
   for (int j = 0; j < s; ++j) {
-    x = imax64(x, L.F[(off + j) * 32 + L.lane]) + __ldg(d + j) + (k - 1) * __ldg(inc + j);
-    if (kCommit) L.F[(off + j) * 32 + L.lane] = x;
+    x = imax64(x, F[off + j]) + __ldg(d + j) + (k - 1) * __ldg(inc + j);
+    F[off + j] = x;
   }
-  return x + __ldg(pr.tail + (int64_t)m * pr.P + p);
 }
 
-struct Acc {
-  int64_t good = 0, sum = 0;
-  int64_t* pm = nullptr;
+struct Warp {
+  int lane;
+  int64_t* F;          // [slots] stage free times (per-warp shared memory)
+  const uint32_t* gt;  // [G] cfg | first slot | stages (shared)
+  const uint64_t* gm;  // [G] models hosted by group g (shared)
+  uint32_t my_gt[2];   // lane's groups lane, lane + 32 (0xFFFFFFFF = none)
+  uint64_t my_gm[2];
+  int32_t head[2];     // lane's models lane, lane + 32
+  int32_t seen[2];
+  int64_t pm[2];
+  int64_t good, sum;
+  unsigned long long upd;
 };
 
 // Group g became available at T: reject heads that miss their SLO even
 // alone, then start the longest feasible prefix of the earliest-head model.
-__device__ void form_batch(const DevProblem& pr, const DevTrace& tr, const DevBatching& bp,
-                           const Lane& L, uint64_t& qmask, Acc& acc, int g, int64_t T) {
+__device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace& tr,
+                                           const DevBatching& bp, Warp& W, uint64_t& qmask,
+                                           int g, int64_t T) {
+  const uint32_t e = W.gt[g];
+  const int p = gt_cfg(e), off = gt_off(e), s = gt_stages(e);
+  const uint64_t hosted = W.gm[g];
   for (;;) {
-    uint64_t w = L.gm[g * 32 + L.lane] & qmask;
+    const uint64_t w = hosted & qmask;
     if (!w) return;
-    int bm = -1;
-    int32_t bidx = 0x7FFFFFFF;
-    while (w) {
-      const int m = __ffsll((long long)w) - 1;
-      w &= w - 1;
-      const int32_t idx = __ldg(bp.midx + __ldg(bp.moff + m) + L.head[m * 32 + L.lane]);
-      if (idx < bidx) {
-        bidx = idx;
-        bm = m;
+    // the hosted model whose head request came first in the trace
+    int32_t idx = 0x7FFFFFFF;
+    int mm = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int m = W.lane + 32 * q;
+      if ((w >> m) & 1ull) {
+        const int32_t x = __ldg(bp.midx + __ldg(bp.moff + m) + W.head[q]);
+        if (x < idx) {
+          idx = x;
+          mm = m;
+        }
       }
     }
+    const int32_t bidx = __reduce_min_sync(FULL, idx);
+    const unsigned owner = __ballot_sync(FULL, idx == bidx);
+    const int src = __ffs(owner) - 1;
+    const int bm = __shfl_sync(FULL, mm, src);
+    const int q = bm >> 5;
+    const int32_t h = __shfl_sync(FULL, q ? W.head[1] : W.head[0], src);
+    const int32_t seen = __shfl_sync(FULL, q ? W.seen[1] : W.seen[0], src);
     const int64_t ah = __ldg(tr.arrival + bidx);
     const int64_t slo = __ldg(pr.slo + bm);
-    int32_t& h = L.head[bm * 32 + L.lane];
-    const int32_t waiting = L.arrived[bm] - h;
-    const int64_t f1 = run_batch<false>(pr, bp, L, g, bm, T, 1);
-    if (f1 - ah > slo) {  // even alone it misses: rejected (final)
-      if (++h == L.arrived[bm]) qmask &= ~(1ull << bm);
-      continue;
-    }
-    int64_t K = 1;
+    const int64_t waiting = seen - h;
     const int64_t lim = waiting < bp.max_batch ? waiting : bp.max_batch;
-    // members share the model's SLO and arrived no earlier than the head, and
-    // the finish grows with k (increments >= 0): the head decides every prefix
-    for (int64_t k = 2; k <= lim; ++k) {
-      if (run_batch<false>(pr, bp, L, g, bm, T, k) - ah > slo) break;
-      K = k;
+    // lane j tries a batch of k = j + 1 (+32 per round); the finish grows with
+    // k (increments >= 0) and the head has the tightest deadline, so the
+    // feasible sizes form a prefix 1..K
+    int64_t K = 0, fK = 0;
+    for (int64_t k0 = 1; k0 <= lim; k0 += 32) {
+      const int64_t k = k0 + W.lane;
+      int64_t f = 0;
+      bool ok = false;
+      if (k <= lim) {
+        f = batch_finish(pr, bp, W.F, p, off, s, bm, T, k);
+        ok = f - ah <= slo;
+        W.upd += (unsigned)s;
+      }
+      const unsigned bal = __ballot_sync(FULL, ok);
+      if (!bal) break;
+      const int last = 31 - __clz(bal);
+      K = k0 + last;
+      fK = __shfl_sync(FULL, f, last);
+      if (bal != FULL) break;
     }
-    const int64_t f = run_batch<true>(pr, bp, L, g, bm, T, K);
-    const int32_t* mem = bp.midx + __ldg(bp.moff + bm) + h;
-    for (int64_t j = 0; j < K; ++j) acc.sum += f - __ldg(tr.arrival + __ldg(mem + j));
-    acc.good += K;
-    if (acc.pm) acc.pm[bm] += K;
-    h += (int32_t)K;
-    if (h == L.arrived[bm]) qmask &= ~(1ull << bm);
+    const int32_t nh = h + (int32_t)(K == 0 ? 1 : K);  // K == 0: the head is rejected
+    if (W.lane == src) {
+      if (q) W.head[1] = nh;
+      else W.head[0] = nh;
+    }
+    if (nh == seen) qmask &= ~(1ull << bm);
+    if (K == 0) continue;
+    if (W.lane == 0) batch_commit(pr, bp, W.F, p, off, s, bm, T, K);
+    int64_t lat = 0;
+    for (int64_t j = W.lane; j < K; j += 32)
+      lat += fK - __ldg(tr.arrival + __ldg(bp.midx + __ldg(bp.moff + bm) + h + j));
+    W.sum += warp_sum64(lat);
+    W.good += K;
+    if (W.lane == src) {
+      if (q) W.pm[1] += K;
+      else W.pm[0] += K;
+    }
+    __syncwarp();
     return;
   }
 }
 
 // Replay every availability event at time <= limit in (time, group) order.
-__device__ void process_events(const DevProblem& pr, const DevTrace& tr, const DevBatching& bp,
-                               const Lane& L, uint64_t gexist, uint64_t& qmask, Acc& acc,
-                               int64_t limit) {
+__device__ __forceinline__ void process_events(const DevProblem& pr, const DevTrace& tr,
+                                               const DevBatching& bp, Warp& W, uint64_t& qmask,
+                                               int64_t limit) {
   while (qmask) {
-    int bg = -1;
-    int64_t bt = INT64_MAX;
-    uint64_t gs = gexist;
-    while (gs) {  // ascending g, strict '<': lowest index among equal times
-      const int g = __ffsll((long long)gs) - 1;
-      gs &= gs - 1;
-      if (!(L.gm[g * 32 + L.lane] & qmask)) continue;
-      const int64_t f0 = L.F[gt_off(L.gt[g * 32 + L.lane]) * 32 + L.lane];
-      if (f0 <= limit && f0 < bt) {
-        bt = f0;
-        bg = g;
+    int64_t key = INT64_MAX;
+    int gi = 0x7FFFFFFF;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (W.my_gt[q] == 0xFFFFFFFFu || !(W.my_gm[q] & qmask)) continue;
+      const int64_t f0 = W.F[gt_off(W.my_gt[q])];
+      if (f0 <= limit && f0 < key) {  // q ascending: lane's lower group first on ties
+        key = f0;
+        gi = W.lane + 32 * q;
       }
     }
-    if (bg < 0) return;
-    form_batch(pr, tr, bp, L, qmask, acc, bg, bt);
+    warp_argmin(key, gi);
+    if (gi == 0x7FFFFFFF) return;
+    form_batch(pr, tr, bp, W, qmask, gi, key);
   }
 }
 
@@ -147,115 +208,138 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t first = ((int64_t)blockIdx.x * kWarps + warp) * 32;
-  if (first >= bt.C) return;  // warp-uniform
+  const int64_t c = (int64_t)blockIdx.x * kWarps + warp;
+  if (c >= bt.C) return;  // warp-uniform
   const int G = bt.G, M = pr.M;
-  const size_t per_warp = (size_t)slots * 256 + (size_t)G * 256 + (size_t)G * 128 +
-                          (size_t)M * 128 + (((size_t)M * 4 + 15) & ~(size_t)15);
-  unsigned char* base = smem + per_warp * warp;
-  Lane L;
-  L.F = reinterpret_cast<int64_t*>(base);
-  L.gm = reinterpret_cast<uint64_t*>(base + (size_t)slots * 256);
-  L.gt = reinterpret_cast<uint32_t*>(base + (size_t)slots * 256 + (size_t)G * 256);
-  L.head = reinterpret_cast<int32_t*>(base + (size_t)slots * 256 + (size_t)G * 384);
-  int32_t* arrived = reinterpret_cast<int32_t*>(base + (size_t)slots * 256 + (size_t)G * 384 +
-                                                (size_t)M * 128);
-  L.arrived = arrived;
-  L.lane = lane;
-
-  const int64_t c = first + lane;
-  const bool in = c < bt.C;
-  const bool active = in && bt.cand_ok[c];
-  const int b = in ? bt.cand_base[c] : 0;
+  unsigned char* base = smem + ((((size_t)slots * 8 + (size_t)G * 12) + 15) & ~(size_t)15) * warp;
+  Warp W;
+  W.lane = lane;
+  W.F = reinterpret_cast<int64_t*>(base);
+  uint64_t* gm = reinterpret_cast<uint64_t*>(base + (size_t)slots * 8);
+  uint32_t* gt = reinterpret_cast<uint32_t*>(base + (size_t)slots * 8 + (size_t)G * 8);
+  W.gm = gm;
+  W.gt = gt;
+  const bool active = bt.cand_ok[c] != 0;
+  const int b = bt.cand_base[c];
   const uint64_t* bmask = bt.base_mask + (int64_t)b * M;
-
-  uint64_t gexist = 0;
-  int nslots = 0;
-  for (int g = 0; g < G; ++g) {
-    const int cfg = bt.base_cfg[(int64_t)b * G + g];
-    uint32_t e = 0xFFFFFFFFu;
-    if (cfg >= 0) {
-      const int s = pr.cfg_stages[cfg];
-      e = (uint32_t)cfg | ((uint32_t)nslots << 16) | ((uint32_t)s << 24);
-      nslots += s;
-      gexist |= 1ull << g;
+  if (lane == 0) {  // group table of the placement (serial prefix over the slots)
+    int nslots = 0;
+    for (int g = 0; g < G; ++g) {
+      const int cfg = bt.base_cfg[(int64_t)b * G + g];
+      uint32_t e = 0xFFFFFFFFu;
+      if (cfg >= 0) {
+        const int st = pr.cfg_stages[cfg];
+        e = (uint32_t)cfg | ((uint32_t)nslots << 16) | ((uint32_t)st << 24);
+        nslots += st;
+      }
+      gt[g] = e;
     }
-    L.gt[g * 32 + lane] = e;
-    L.gm[g * 32 + lane] = 0;
   }
-  if (!active) gexist = 0;
-  for (int m = 0; m < M; ++m) {
-    uint64_t hm = active ? bmask[m] : 0ull;
-    while (hm) {
-      const int g = __ffsll((long long)hm) - 1;
-      hm &= hm - 1;
-      L.gm[g * 32 + lane] |= 1ull << m;
-    }
-    L.head[m * 32 + lane] = 0;
+  for (int g = lane; g < G; g += 32) {
+    uint64_t h = 0;
+    for (int m = 0; m < M; ++m) h |= ((__ldg(bmask + m) >> g) & 1ull) << m;
+    gm[g] = active ? h : 0ull;
   }
-  for (int k = 0; k < slots; ++k) L.F[k * 32 + lane] = 0;
-  for (int m = lane; m < M; m += 32) arrived[m] = 0;
+  for (int k = lane; k < slots; k += 32) W.F[k] = 0;
   __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int g = lane + 32 * q;
+    W.my_gt[q] = g < G ? gt[g] : 0xFFFFFFFFu;
+    W.my_gm[q] = g < G ? gm[g] : 0ull;
+    W.head[q] = 0;
+    W.seen[q] = 0;
+    W.pm[q] = 0;
+  }
+  W.good = 0;
+  W.sum = 0;
+  W.upd = 0;
+  uint64_t qmask = 0;  // models with waiting requests (warp-uniform)
 
-  Acc acc;
-  acc.pm = (out.good_per_model && in) ? out.good_per_model + (c - out.out_offset) * M : nullptr;
-  uint64_t qmask = 0;  // models with waiting requests
-
-  for (int64_t i0 = 0; i0 < tr.n; i0 += 32) {
+  for (int64_t i0 = 0; i0 < tr.n && active; i0 += 32) {
     const int64_t ai = tr.arrival[i0 + lane];
     const int mi = tr.model[i0 + lane];
     const int nj = (int)min((int64_t)32, tr.n - i0);
     for (int j = 0; j < nj; ++j) {
       const int64_t a = __shfl_sync(FULL, ai, j);
       const int m = __shfl_sync(FULL, mi, j);
-      if (qmask) process_events(pr, tr, bp, L, gexist, qmask, acc, a);
-      const int32_t pos = arrived[m];
-      const uint64_t hosts = active ? __ldg(bmask + m) : 0ull;
+      if (qmask) process_events(pr, tr, bp, W, qmask, a);
+      const int q = m >> 5;
+      const bool own = (m & 31) == lane;
+      const uint64_t hosts = __ldg(bmask + m);
       if (hosts && !((qmask >> m) & 1ull)) {
         // empty queue: run now on the available host with the earliest finish
-        int bg = -1;
-        int64_t bf = INT64_MAX;
-        uint64_t w = hosts;
-        while (w) {
-          const int g = __ffsll((long long)w) - 1;
-          w &= w - 1;
-          if (L.F[gt_off(L.gt[g * 32 + lane]) * 32 + lane] > a) continue;  // first stage busy
-          const int64_t f = run_batch<false>(pr, bp, L, g, m, a, 1);
-          if (f < bf) {
-            bf = f;
-            bg = g;
+        int64_t key = INT64_MAX;
+        int gi = 0x7FFFFFFF;
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int g = lane + 32 * qq;
+          if (g >= 64 || !((hosts >> g) & 1ull)) continue;
+          const uint32_t e = W.my_gt[qq];
+          if (W.F[gt_off(e)] > a) continue;  // first stage busy
+          const int64_t f = batch_finish(pr, bp, W.F, gt_cfg(e), gt_off(e), gt_stages(e), m, a, 1);
+          W.upd += (unsigned)gt_stages(e);
+          if (f < key) {
+            key = f;
+            gi = g;
           }
         }
-        if (bg < 0) {  // every host busy: wait for a batch
+        warp_argmin(key, gi);
+        if (gi == 0x7FFFFFFF) {  // every host busy: wait for a batch
           qmask |= 1ull << m;
-          L.head[m * 32 + lane] = pos;
-        } else {
-          if (bf - a <= __ldg(pr.slo + m)) {  // else rejected at receipt (C2, C3)
-            run_batch<true>(pr, bp, L, bg, m, a, 1);
-            acc.good += 1;
-            acc.sum += bf - a;
-            if (acc.pm) acc.pm[m] += 1;
+          if (own) {
+            if (q) W.head[1] = W.seen[1];
+            else W.head[0] = W.seen[0];
           }
-          L.head[m * 32 + lane] = pos + 1;
+        } else {
+          if (key - a <= __ldg(pr.slo + m)) {  // else rejected at receipt (C2, C3)
+            if (lane == (gi & 31)) {
+              const uint32_t e = (gi >> 5) ? W.my_gt[1] : W.my_gt[0];
+              batch_commit(pr, bp, W.F, gt_cfg(e), gt_off(e), gt_stages(e), m, a, 1);
+            }
+            W.good += 1;
+            W.sum += key - a;
+            if (own) {
+              if (q) W.pm[1] += 1;
+              else W.pm[0] += 1;
+            }
+          }
+          if (own) {
+            if (q) W.head[1] = W.seen[1] + 1;
+            else W.head[0] = W.seen[0] + 1;
+          }
+          __syncwarp();
         }
       }
-      __syncwarp();
-      if (lane == 0) arrived[m] = pos + 1;
-      __syncwarp();
+      if (own) {
+        if (q) W.seen[1] += 1;
+        else W.seen[0] += 1;
+      }
     }
   }
-  if (qmask) process_events(pr, tr, bp, L, gexist, qmask, acc, INT64_MAX);  // drain
-  if (in) {
-    const int64_t o = c - out.out_offset;
-    out.good[o] = active ? acc.good : -1;
-    if (out.sum_latency) out.sum_latency[o] = active ? acc.sum : 0;
+  if (active && qmask) process_events(pr, tr, bp, W, qmask, INT64_MAX);  // drain
+  if (out.stage_updates) {
+    unsigned long long u = W.upd;
+    for (int w = 16; w > 0; w >>= 1) u += __shfl_down_sync(FULL, u, w);
+    if (lane == 0) atomicAdd(out.stage_updates, u);
+  }
+  const int64_t o = c - out.out_offset;
+  if (out.good_per_model && active) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (lane + 32 * q < M) out.good_per_model[o * M + lane + 32 * q] = W.pm[q];
+  }
+  if (lane == 0) {
+    out.good[o] = active ? W.good : -1;
+    if (out.sum_latency) out.sum_latency[o] = active ? W.sum : 0;
   }
 }
 
 }  // namespace
 
 size_t batching_smem_per_warp(int32_t slots, int32_t G, int32_t M) {
-  return (size_t)slots * 256 + (size_t)G * 384 + (size_t)M * 128 + (((size_t)M * 4 + 15) & ~(size_t)15);
+  (void)M;
+  return (((size_t)slots * 8 + (size_t)G * 12) + 15) & ~(size_t)15;
 }
 
 cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevBatch& b,
@@ -267,8 +351,7 @@ cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevB
   cudaError_t ea = cudaFuncSetAttribute(batching_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (ea != cudaSuccess) return ea;
-  const int64_t warps = (b.C + 31) / 32;
-  const int blocks = (int)((warps + kWarps - 1) / kWarps);
+  const int blocks = (int)((b.C + kWarps - 1) / kWarps);
   batching_kernel<<<blocks, kWarps * 32, smem, stream>>>(pr, tr, b, bp, slots, out);
   if (launches) ++*launches;
   return cudaGetLastError();

@@ -683,7 +683,7 @@ asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
     hb.cand_base[c] = (int32_t)c;
     hb.cand_ok[c] = ok ? 1 : 0;
   }
-  const size_t smem = 2 * asim::batching_smem_per_warp(hb.slots, G, (int32_t)M);
+  const size_t smem = 4 * asim::batching_smem_per_warp(hb.slots, G, (int32_t)M);
   if (smem > 227 * 1024) return asim_fail(ctx, ASIM_ERANGE, "placement too large for batching");
   const bool want_sum = out->sum_latency_ns != nullptr;
   const bool want_pm = out->good_per_model != nullptr;
@@ -728,6 +728,7 @@ asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
   bp.midx = ctx->d_midx.as<int32_t>();
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (ctx->profiling) {
+    dout.stage_updates = ctx->d_counter.as<unsigned long long>();
     if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
       return asim_cuda(ctx, cudaGetLastError(), "event create");
     cudaEventRecord(ev0, st);

@@ -180,26 +180,22 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
   }
 }
 
-// Replay every availability event at time <= limit in (time, group) order.
-__device__ __forceinline__ void process_events(const DevProblem& pr, const DevTrace& tr,
-                                               const DevBatching& bp, Warp& W, uint64_t& qmask,
-                                               int64_t limit) {
-  while (qmask) {
-    int64_t key = INT64_MAX;
-    int gi = 0x7FFFFFFF;
+// The earliest availability event: (first-stage free time, group) minimum
+// over the groups that host a model with waiting requests; INT64_MAX if none.
+__device__ __forceinline__ void earliest_event(const Warp& W, uint64_t qmask, int64_t& key,
+                                               int& gi) {
+  key = INT64_MAX;
+  gi = 0x7FFFFFFF;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (W.my_gt[q] == 0xFFFFFFFFu || !(W.my_gm[q] & qmask)) continue;
-      const int64_t f0 = W.F[gt_off(W.my_gt[q])];
-      if (f0 <= limit && f0 < key) {  // q ascending: lane's lower group first on ties
-        key = f0;
-        gi = W.lane + 32 * q;
-      }
+  for (int q = 0; q < 2; ++q) {
+    if (W.my_gt[q] == 0xFFFFFFFFu || !(W.my_gm[q] & qmask)) continue;
+    const int64_t f0 = W.F[gt_off(W.my_gt[q])];
+    if (f0 < key) {  // q ascending: the lane's lower group first on ties
+      key = f0;
+      gi = W.lane + 32 * q;
     }
-    warp_argmin(key, gi);
-    if (gi == 0x7FFFFFFF) return;
-    form_batch(pr, tr, bp, W, qmask, gi, key);
   }
+  warp_argmin(key, gi);
 }
 
 __global__ void __launch_bounds__(kWarps * 32)
@@ -255,6 +251,9 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   W.sum = 0;
   W.upd = 0;
   uint64_t qmask = 0;  // models with waiting requests (warp-uniform)
+  int64_t nev = INT64_MAX;  // cached earliest availability event (warp-uniform)
+  int nevg = 0;
+  bool nev_ok = false;
 
   for (int64_t i0 = 0; i0 < tr.n && active; i0 += 32) {
     const int64_t ai = tr.arrival[i0 + lane];
@@ -263,7 +262,20 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
     for (int j = 0; j < nj; ++j) {
       const int64_t a = __shfl_sync(FULL, ai, j);
       const int m = __shfl_sync(FULL, mi, j);
-      if (qmask) process_events(pr, tr, bp, W, qmask, a);
+      // replay the availability events at time <= a in (time, group) order;
+      // the earliest one is cached until a batch or a newly waiting request
+      // changes it (an immediate run uses an available group, which has no
+      // waiting work, so it cannot change it)
+      if (qmask) {
+        if (!nev_ok) {
+          earliest_event(W, qmask, nev, nevg);
+          nev_ok = true;
+        }
+        while (nev <= a) {
+          form_batch(pr, tr, bp, W, qmask, nevg, nev);
+          earliest_event(W, qmask, nev, nevg);
+        }
+      }
       const int q = m >> 5;
       const bool own = (m & 31) == lane;
       const uint64_t hosts = __ldg(bmask + m);
@@ -287,6 +299,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
         warp_argmin(key, gi);
         if (gi == 0x7FFFFFFF) {  // every host busy: wait for a batch
           qmask |= 1ull << m;
+          nev_ok = false;
           if (own) {
             if (q) W.head[1] = W.seen[1];
             else W.head[0] = W.seen[0];
@@ -317,7 +330,10 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
       }
     }
   }
-  if (active && qmask) process_events(pr, tr, bp, W, qmask, INT64_MAX);  // drain
+  while (active && qmask) {  // drain
+    earliest_event(W, qmask, nev, nevg);
+    form_batch(pr, tr, bp, W, qmask, nevg, nev);
+  }
   if (out.stage_updates) {
     unsigned long long u = W.upd;
     for (int w = 16; w > 0; w >>= 1) u += __shfl_down_sync(FULL, u, w);

@@ -388,3 +388,28 @@ def test_gpu_batching_errors(sim):
     sim.set_problem(prob)
     sim.set_trace(empty.arrival_ns, empty.model)
     assert sim.evaluate_batching(cfg, mask, _inc(prob), 2)["good"][0] == 0
+
+
+@pytest.mark.gpu
+def test_gpu_batching_bench_config_sampled(sim):
+    """The bench configuration (scripts/bench_batching.py: S1 §5.4 setup, 1 h
+    trace, 4,736 placements, max_batch 4, delta 0.9) in the launch
+    configuration the bench times; 6 sampled candidates re-simulated one by
+    one by the oracle must match exactly."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "scripts"))
+    from bench_batching import placements
+
+    prob, tr, inc = configs.s1_batching(seed=0, duration=3600.0, slo_scale=5.0, delta=0.9)
+    cfg, mask = placements(prob, 148 * 32, seed=1)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    got = sim.evaluate_batching(cfg, mask, inc, 4, per_model=True)
+    rng = np.random.default_rng(3)
+    pick = sorted(set(rng.integers(0, len(cfg), size=5).tolist()) | {int(got["argmax"])})
+    g, s, pm = oracle.evaluate_batching(prob, tr, cfg[pick], mask[pick], inc, 4, per_model=True)
+    np.testing.assert_array_equal(got["good"][pick], g)
+    np.testing.assert_array_equal(got["sum_latency_ns"][pick], s)
+    np.testing.assert_array_equal(got["good_per_model"][pick], pm)
+    assert (got["good"] <= len(tr)).all() and (got["good"] >= 0).all()

@@ -45,6 +45,14 @@ __device__ __forceinline__ int gt_stages(uint32_t e) { return (int)(e >> 24); }
 // (key, index) argmin over the warp; every lane gets the result.  Ties on
 // the key go to the lowest index.
 __device__ __forceinline__ void warp_argmin(int64_t& key, int& idx) {
+  const unsigned v = __ballot_sync(FULL, idx != 0x7FFFFFFF);
+  if (v == 0u) return;  // no lane has a candidate: every lane holds (MAX, none)
+  if ((v & (v - 1u)) == 0u) {  // one lane has: broadcast it
+    const int src = __ffs(v) - 1;
+    key = __shfl_sync(FULL, key, src);
+    idx = __shfl_sync(FULL, idx, src);
+    return;
+  }
 #pragma unroll
   for (int w = 16; w > 0; w >>= 1) {
     const int64_t k2 = __shfl_xor_sync(FULL, key, w);

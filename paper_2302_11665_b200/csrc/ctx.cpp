@@ -513,18 +513,8 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
     ap[i] = a[i];
     mp[i] = (uint16_t)m[i];
   }
-  // per-model request lists (CSR, ascending trace index) for the batching kernel
-  std::vector<int32_t> moff(ctx->hp.M + 1, 0), midx(n > 0 ? n : 1, 0);
-  for (int64_t i = 0; i < n; ++i) ++moff[m[i] + 1];
-  for (int32_t k = 0; k < ctx->hp.M; ++k) moff[k + 1] += moff[k];
-  {
-    std::vector<int32_t> fill(moff.begin(), moff.end() - 1);
-    for (int64_t i = 0; i < n; ++i) midx[fill[m[i]]++] = (int32_t)i;
-  }
   cudaError_t e = upload(ctx->d_arrival, ap, st);
   if (e == cudaSuccess) e = upload(ctx->d_model, mp, st);
-  if (e == cudaSuccess) e = upload(ctx->d_moff, moff, st);
-  if (e == cudaSuccess) e = upload(ctx->d_midx, midx, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload trace");
   ctx->n = n;
@@ -532,6 +522,7 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
   ctx->min_arrival = n ? a[0] : 0;
   ctx->model_n.assign(ctx->hp.M, 0);
   for (int64_t i = 0; i < n; ++i) ++ctx->model_n[m[i]];
+  ctx->has_midx = false;  // built on the first batching call
   ctx->has_trace = true;
   return ASIM_OK;
 }
@@ -691,6 +682,22 @@ asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
   asim::DevOut dout{};
   cudaError_t e = upload(ctx->d_inc, inc, st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload increments");
+  if (!ctx->has_midx) {  // per-model request lists (CSR, ascending trace index)
+    const int64_t n = ctx->n;
+    std::vector<uint16_t> mh(n > 0 ? n : 1);
+    if (n > 0) e = cudaMemcpy(mh.data(), ctx->d_model.p, n * 2, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "download trace models");
+    std::vector<int32_t> moff(M + 1, 0), midx(n > 0 ? n : 1, 0);
+    for (int64_t i = 0; i < n; ++i) ++moff[mh[i] + 1];
+    for (int64_t k = 0; k < M; ++k) moff[k + 1] += moff[k];
+    std::vector<int32_t> fill(moff.begin(), moff.end() - 1);
+    for (int64_t i = 0; i < n; ++i) midx[fill[mh[i]]++] = (int32_t)i;
+    e = upload(ctx->d_moff, moff, st);
+    if (e == cudaSuccess) e = upload(ctx->d_midx, midx, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "upload per-model request lists");
+    ctx->has_midx = true;
+  }
   if (out->ptr_kind == ASIM_DEVICE) {
     dout.good = out->good;
     dout.sum_latency = out->sum_latency_ns;

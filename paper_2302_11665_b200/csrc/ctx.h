@@ -63,6 +63,7 @@ struct asim_ctx {
   std::vector<int64_t> model_n;  // [M] requests per model in the trace
   DBuf d_arrival, d_model;
   DBuf d_moff, d_midx;  // per-model request lists (CSR) for the batching kernel
+  bool has_midx = false;  // d_moff/d_midx match the current trace
   DBuf d_inc;           // batching stage increments (asim_evaluate_batching)
 
   // statistics (asim_set_profiling)

@@ -1,0 +1,10 @@
+# f4 batching (warp-per-candidate kernel): parity tests, bench line, launch list.
+cd $GRAFT_REPO_ROOT
+T=gpurun_out/r1g
+mkdir -p $T
+timeout 600 python -m pytest tests/test_batching.py -m gpu -x -q > $T/pytest_batching.log 2>&1
+tail -3 $T/pytest_batching.log
+timeout 900 python scripts/bench_batching.py > $T/bench_batching.json 2> $T/bench_batching.err
+cat $T/bench_batching.json | head -c 600
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $T/launches_batching.csv \
+  python scripts/bench_batching.py --steps 1 --warmup 0 --no-cpu-baseline > $T/launches_batching.json 2>&1

@@ -69,3 +69,49 @@ def run_search(engine, pg=None, stream=None, device=None, on_step=None) -> int:
         steps += 1
         if on_step is not None:
             on_step(steps, C)
+
+
+def evaluate_sharded(evaluate_fn, C: int, pg=None, device=None):
+    """Evaluate C independent candidates sharded over the ranks (the same
+    contiguous split as the search; no data-path collective besides the one
+    all-gather of the int64 good counts).
+
+    evaluate_fn(begin, end) -> int64 tensor of the good counts of candidates
+    [begin, end) on `device` (e.g. a Simulator.evaluate_batching call on that
+    slice).  Returns (good[C], argmax) identical on every rank; argmax = max
+    good, ties -> lowest global index, -1 when every candidate is infeasible
+    (good < 0)."""
+    world = dist.get_world_size(pg) if (pg is not None or dist.is_initialized()) else 1
+    rank = dist.get_rank(pg) if world > 1 else 0
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
+            else torch.device("cpu")
+    if C == 0:
+        return torch.zeros(0, dtype=torch.int64, device=device), -1
+    b, e = shard(C, rank, world)
+    pad = -(-C // world)
+    local = torch.full((pad,), -1, dtype=torch.int64, device=device)
+    if e > b:
+        local[:e - b] = evaluate_fn(b, e).to(device=device, dtype=torch.int64)
+    full = local[:C] if world == 1 else gather_all(local, C, world, pg)
+    best = int(full.max().item())
+    arg = int(torch.nonzero(full == best)[0].item()) if best >= 0 else -1
+    return full, arg
+
+
+def evaluate_batching_sharded(sim, group_cfg, host_mask, stage_inc_ns, max_batch: int,
+                              pg=None):
+    """The dynamic batching evaluator (include/asim.h asim_evaluate_batching)
+    over 1-8 GPUs: each rank simulates its contiguous shard of the placements
+    on its own device; returns (good[C] on the local device, global argmax)."""
+    import numpy as np
+
+    cfg = np.ascontiguousarray(group_cfg, dtype=np.int32)
+    mask = np.ascontiguousarray(host_mask, dtype=np.uint64)
+
+    def run(b, e):
+        out = sim.evaluate_batching(cfg[b:e], mask[b:e], stage_inc_ns, max_batch,
+                                    sum_latency=False, argmax=False)
+        return torch.from_numpy(out["good"])
+
+    return evaluate_sharded(run, len(cfg), pg=pg)

@@ -413,3 +413,17 @@ def test_gpu_batching_bench_config_sampled(sim):
     np.testing.assert_array_equal(got["sum_latency_ns"][pick], s)
     np.testing.assert_array_equal(got["good_per_model"][pick], pm)
     assert (got["good"] <= len(tr)).all() and (got["good"] >= 0).all()
+
+
+@pytest.mark.gpu
+def test_gpu_batching_sharded_single_rank(sim):
+    """dist.evaluate_batching_sharded at world size 1 (the N>1 logic is
+    covered under gloo in tests/test_dist.py)."""
+    from paper_2302_11665_b200 import dist as adist
+    prob, tr, inc = configs.s1_batching(seed=1, duration=60.0, slo_scale=3.0, delta=0.9)
+    cfg, mask = _stack(_s1_placements(prob), prob.num_models)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    good, arg = adist.evaluate_batching_sharded(sim, cfg, mask, inc, 2)
+    g, _, _ = oracle.evaluate_batching(prob, tr, cfg, mask, inc, 2)
+    assert good.cpu().tolist() == g.tolist() and arg == int(np.argmax(g))

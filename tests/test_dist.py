@@ -133,3 +133,56 @@ def test_sharded_search_matches_single_process(world):
         for (bg, best), r_ref in zip(runs, ref["runs"]):
             assert bg == r_ref["good"]
             assert best == r_ref["placement"].host_mask.tolist()
+
+
+def _batching_case():
+    from tests.helpers import place
+    prob, tr, inc = configs.s1_batching(seed=2, duration=20.0, slo_scale=3.0, delta=0.9)
+    M = prob.num_models
+    rng = np.random.default_rng(0)
+    pls = []
+    for p, (s, n) in enumerate(prob.configs):
+        G = 16 // (s * n)
+        for _ in range(3):
+            groups = [[m for m in range(M) if rng.random() < 0.15] for _ in range(G)]
+            pls.append(place([p] * G, groups, M))
+    cfg = np.full((len(pls), 16), -1, np.int32)
+    mask = np.zeros((len(pls), M), np.uint64)
+    for i, pl in enumerate(pls):
+        cfg[i, :pl.num_groups] = pl.group_cfg
+        mask[i] = pl.host_mask
+    return prob, tr, inc, cfg, mask
+
+
+def _batching_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2302_11665_b200 import dist as adist
+    prob, tr, inc, cfg, mask = _batching_case()
+
+    def run(b, e):  # CPU engine behind the same sharding logic
+        g, _, _ = oracle.evaluate_batching(prob, tr, cfg[b:e], mask[b:e], inc, 3, threads=2)
+        return torch.from_numpy(g)
+
+    good, arg = adist.evaluate_sharded(run, len(cfg), device=torch.device("cpu"))
+    q.put((rank, good.tolist(), arg))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_batching_matches_single_process(world):
+    prob, tr, inc, cfg, mask = _batching_case()
+    ref, _, _ = oracle.evaluate_batching(prob, tr, cfg, mask, inc, 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batching_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = int(np.argmax(ref)) if ref.max() >= 0 else -1
+    for rank, good, arg in outs:
+        assert good == ref.tolist() and arg == want

@@ -28,6 +28,7 @@
 // simulation (oracle/des.cpp simulate_batching).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "asim_internal.h"
 
@@ -102,10 +103,9 @@ struct Warp {
   const uint32_t* gt;  // [G] cfg | first slot | stages (shared)
   const uint64_t* gm;  // [G] models hosted by group g (shared)
   uint32_t my_gt[2];   // lane's groups lane, lane + 32 (0xFFFFFFFF = none)
-  uint64_t my_gm[2];
   int32_t head[2];     // lane's models lane, lane + 32
   int32_t seen[2];
-  int64_t pm[2];
+  int32_t pm[2];       // good per model (< n <= 2^31 - 1)
   int64_t good, sum;
   unsigned long long upd;
 };
@@ -180,8 +180,8 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     W.sum += warp_sum64(lat);
     W.good += K;
     if (W.lane == src) {
-      if (q) W.pm[1] += K;
-      else W.pm[0] += K;
+      if (q) W.pm[1] += (int32_t)K;
+      else W.pm[0] += (int32_t)K;
     }
     __syncwarp();
     return;
@@ -196,7 +196,7 @@ __device__ __forceinline__ void earliest_event(const Warp& W, uint64_t qmask, in
   gi = 0x7FFFFFFF;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    if (W.my_gt[q] == 0xFFFFFFFFu || !(W.my_gm[q] & qmask)) continue;
+    if (W.my_gt[q] == 0xFFFFFFFFu || !(W.gm[W.lane + 32 * q] & qmask)) continue;
     const int64_t f0 = W.F[gt_off(W.my_gt[q])];
     if (f0 < key) {  // q ascending: the lane's lower group first on ties
       key = f0;
@@ -206,7 +206,8 @@ __device__ __forceinline__ void earliest_event(const Warp& W, uint64_t qmask, in
   warp_argmin(key, gi);
 }
 
-__global__ void __launch_bounds__(kWarps * 32)
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t slots,
                 DevOut out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -250,7 +251,6 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   for (int q = 0; q < 2; ++q) {
     const int g = lane + 32 * q;
     W.my_gt[q] = g < G ? gt[g] : 0xFFFFFFFFu;
-    W.my_gm[q] = g < G ? gm[g] : 0ull;
     W.head[q] = 0;
     W.seen[q] = 0;
     W.pm[q] = 0;
@@ -372,11 +372,19 @@ cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevB
   if (b.C <= 0) return cudaSuccess;
   if (slots < 1) slots = 1;
   const size_t smem = (size_t)kWarps * batching_smem_per_warp(slots, b.G, pr.M);
-  cudaError_t ea = cudaFuncSetAttribute(batching_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  // resident blocks per SM the register budget is sized for (ASIM_BATCH_MINB
+  // = 4 | 6 | 8; 4 = 128 registers, no spills)
+  static const int minb = [] {
+    const char* e = getenv("ASIM_BATCH_MINB");
+    const int v = e ? atoi(e) : 4;
+    return (v == 6 || v == 8) ? v : 4;
+  }();
+  auto kern = minb == 8 ? batching_kernel<8> : minb == 6 ? batching_kernel<6> : batching_kernel<4>;
+  cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024);
   if (ea != cudaSuccess) return ea;
   const int blocks = (int)((b.C + kWarps - 1) / kWarps);
-  batching_kernel<<<blocks, kWarps * 32, smem, stream>>>(pr, tr, b, bp, slots, out);
+  kern<<<blocks, kWarps * 32, smem, stream>>>(pr, tr, b, bp, slots, out);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

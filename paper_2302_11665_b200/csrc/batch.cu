@@ -106,6 +106,8 @@ struct Warp {
   int32_t head[2];     // lane's models lane, lane + 32
   int32_t seen[2];
   int32_t pm[2];       // good per model (< n <= 2^31 - 1)
+  int32_t hidx[2];     // trace index of the head request (valid while waiting)
+  int32_t mo[2];       // start of the model's request list (CSR offset)
   int64_t good, sum;
   unsigned long long upd;
 };
@@ -128,7 +130,7 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     for (int q = 0; q < 2; ++q) {
       const int m = W.lane + 32 * q;
       if ((w >> m) & 1ull) {
-        const int32_t x = __ldg(bp.midx + __ldg(bp.moff + m) + W.head[q]);
+        const int32_t x = q ? W.hidx[1] : W.hidx[0];
         if (x < idx) {
           idx = x;
           mm = m;
@@ -168,15 +170,21 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     }
     const int32_t nh = h + (int32_t)(K == 0 ? 1 : K);  // K == 0: the head is rejected
     if (W.lane == src) {
-      if (q) W.head[1] = nh;
-      else W.head[0] = nh;
+      const int32_t nx = nh < seen ? __ldg(bp.midx + (q ? W.mo[1] : W.mo[0]) + nh) : 0;
+      if (q) {
+        W.head[1] = nh;
+        W.hidx[1] = nx;
+      } else {
+        W.head[0] = nh;
+        W.hidx[0] = nx;
+      }
     }
     if (nh == seen) qmask &= ~(1ull << bm);
     if (K == 0) continue;
     if (W.lane == 0) batch_commit(pr, bp, W.F, p, off, s, bm, T, K);
     int64_t lat = 0;
-    for (int64_t j = W.lane; j < K; j += 32)
-      lat += fK - __ldg(tr.arrival + __ldg(bp.midx + __ldg(bp.moff + bm) + h + j));
+    const int32_t* members = bp.midx + __shfl_sync(FULL, q ? W.mo[1] : W.mo[0], src) + h;
+    for (int64_t j = W.lane; j < K; j += 32) lat += fK - __ldg(tr.arrival + __ldg(members + j));
     W.sum += warp_sum64(lat);
     W.good += K;
     if (W.lane == src) {
@@ -252,6 +260,8 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
     const int g = lane + 32 * q;
     W.my_gt[q] = g < G ? gt[g] : 0xFFFFFFFFu;
     W.head[q] = 0;
+    W.hidx[q] = 0;
+    W.mo[q] = lane + 32 * q < M ? __ldg(bp.moff + lane + 32 * q) : 0;
     W.seen[q] = 0;
     W.pm[q] = 0;
   }
@@ -309,8 +319,14 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
           qmask |= 1ull << m;
           nev_ok = false;
           if (own) {
-            if (q) W.head[1] = W.seen[1];
-            else W.head[0] = W.seen[0];
+            const int32_t i = (int32_t)(i0 + j);
+            if (q) {
+              W.head[1] = W.seen[1];
+              W.hidx[1] = i;
+            } else {
+              W.head[0] = W.seen[0];
+              W.hidx[0] = i;
+            }
           }
         } else {
           if (key - a <= __ldg(pr.slo + m)) {  // else rejected at receipt (C2, C3)

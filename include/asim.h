@@ -152,7 +152,8 @@ asim_status asim_set_problem(asim_ctx* ctx, const asim_problem* problem);
 /* The workload W: n requests, arrival_ns[n] non-decreasing and >= 0,
  * model[n] in [0, M).  Requires asim_set_problem first (ASIM_ESTATE).
  * Copied into device memory (ptr_kind says where the inputs live).
- * n may be 0 (attainment 1.0, reading C9).  Errors: ASIM_EUNSORTED,
+ * n in [0, 2^31 - 1] (int32 request indices); n may be 0 (attainment 1.0,
+ * reading C9).  Errors: ASIM_EUNSORTED,
  * ASIM_ERANGE (model id, arrival > 2^62, or max arrival + n * max service
  * >= 2^62), ASIM_EINVAL. */
 asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,

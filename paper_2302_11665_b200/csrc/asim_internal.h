@@ -72,6 +72,7 @@ struct DevBatching {
   const int64_t* inc;      // [M][P][S] stage increment per extra batch member
   const int32_t* moff;     // [M+1]
   const int32_t* midx;     // [n] trace indices grouped by model
+  const int32_t* order;    // [C] candidate simulated by warp w (costliest first), nullable
 };
 size_t batching_smem_per_warp(int32_t slots, int32_t G, int32_t M);
 cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevBatch& b,

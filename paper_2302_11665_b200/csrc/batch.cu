@@ -221,8 +221,9 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * kWarps + warp;
-  if (c >= bt.C) return;  // warp-uniform
+  const int64_t w = (int64_t)blockIdx.x * kWarps + warp;
+  if (w >= bt.C) return;  // warp-uniform
+  const int64_t c = bp.order ? (int64_t)bp.order[w] : w;
   const int G = bt.G, M = pr.M;
   unsigned char* base = smem + ((((size_t)slots * 8 + (size_t)G * 12) + 15) & ~(size_t)15) * warp;
   Warp W;

@@ -294,7 +294,7 @@ void asim_destroy(asim_ctx* ctx) {
   {
     DeviceGuard dg(ctx->device);
     DBuf* bufs[] = {&ctx->d_stage, &ctx->d_tail, &ctx->d_slo, &ctx->d_cfg_stages,
-                    &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc,
+                    &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc, &ctx->d_order,
                     &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group,
                     &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm, &ctx->d_busy,
@@ -728,7 +728,31 @@ asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
   b.cand_kmask = nullptr;
   b.cand_gmask = nullptr;
   b.C = C;
+  // launch order: longest-processing-time first, so the second wave of
+  // warps fills in behind the slow candidates instead of leaving a tail;
+  // estimated cost = sum over hosted models of requests x stages of the group
+  {
+    std::vector<int64_t> cost(C, 0);
+    for (int64_t c = 0; c < C; ++c) {
+      if (!hb.cand_ok[c]) continue;
+      for (int64_t m = 0; m < M; ++m) {
+        uint64_t w = hb.base_mask[c * M + m];
+        while (w) {
+          const int g = __builtin_ctzll(w);
+          w &= w - 1;
+          cost[c] += ctx->model_n[m] * hp.cfg_stages[hb.base_cfg[c * G + g]];
+        }
+      }
+    }
+    std::vector<int32_t> order(C);
+    for (int64_t c = 0; c < C; ++c) order[c] = (int32_t)c;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
+    e = upload(ctx->d_order, order, st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "upload launch order");
+  }
   asim::DevBatching bp;
+  bp.order = ctx->d_order.as<int32_t>();
   bp.max_batch = opt->max_batch;
   bp.inc = ctx->d_inc.as<int64_t>();
   bp.moff = ctx->d_moff.as<int32_t>();

@@ -65,6 +65,7 @@ struct asim_ctx {
   DBuf d_moff, d_midx;  // per-model request lists (CSR) for the batching kernel
   bool has_midx = false;  // d_moff/d_midx match the current trace
   DBuf d_inc;           // batching stage increments (asim_evaluate_batching)
+  DBuf d_order;         // batching launch order (costliest candidates first)
 
   // statistics (asim_set_profiling)
   bool profiling = false;

@@ -45,19 +45,20 @@ __device__ __forceinline__ int gt_stages(uint32_t e) { return (int)(e >> 24); }
 
 // (key, index) argmin over the warp; every lane gets the result.  Ties on
 // the key go to the lowest index.
-__device__ __forceinline__ void warp_argmin(int64_t& key, int& idx) {
-  const unsigned v = __ballot_sync(FULL, idx != 0x7FFFFFFF);
+template <int SW>
+__device__ __forceinline__ void warp_argmin(unsigned sm, int sbase, int64_t& key, int& idx) {
+  const unsigned v = __ballot_sync(sm, idx != 0x7FFFFFFF) >> sbase;
   if (v == 0u) return;  // no lane has a candidate: every lane holds (MAX, none)
   if ((v & (v - 1u)) == 0u) {  // one lane has: broadcast it
     const int src = __ffs(v) - 1;
-    key = __shfl_sync(FULL, key, src);
-    idx = __shfl_sync(FULL, idx, src);
+    key = __shfl_sync(sm, key, src, SW);
+    idx = __shfl_sync(sm, idx, src, SW);
     return;
   }
 #pragma unroll
-  for (int w = 16; w > 0; w >>= 1) {
-    const int64_t k2 = __shfl_xor_sync(FULL, key, w);
-    const int i2 = __shfl_xor_sync(FULL, idx, w);
+  for (int w = SW / 2; w > 0; w >>= 1) {
+    const int64_t k2 = __shfl_xor_sync(sm, key, w, SW);
+    const int i2 = __shfl_xor_sync(sm, idx, w, SW);
     if (k2 < key || (k2 == key && i2 < idx)) {
       key = k2;
       idx = i2;
@@ -65,9 +66,10 @@ __device__ __forceinline__ void warp_argmin(int64_t& key, int& idx) {
   }
 }
 
-__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+template <int SW>
+__device__ __forceinline__ int64_t warp_sum64(unsigned sm, int64_t v) {
 #pragma unroll
-  for (int w = 16; w > 0; w >>= 1) v += __shfl_xor_sync(FULL, v, w);
+  for (int w = SW / 2; w > 0; w >>= 1) v += __shfl_xor_sync(sm, v, w, SW);
   return v;
 }
 
@@ -98,7 +100,9 @@ __device__ __forceinline__ void batch_commit(const DevProblem& pr, const DevBatc
 }
 
 struct Warp {
-  int lane;
+  int lane;            // lane within the (sub-)warp that owns the candidate
+  unsigned sm;         // mask of that (sub-)warp
+  int sbase;           // its first lane in the hardware warp
   int64_t* F;          // [slots] stage free times (per-warp shared memory)
   const uint32_t* gt;  // [G] cfg | first slot | stages (shared)
   const uint64_t* gm;  // [G] models hosted by group g (shared)
@@ -114,6 +118,7 @@ struct Warp {
 
 // Group g became available at T: reject heads that miss their SLO even
 // alone, then start the longest feasible prefix of the earliest-head model.
+template <int SW>
 __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace& tr,
                                            const DevBatching& bp, Warp& W, uint64_t& qmask,
                                            int g, int64_t T) {
@@ -128,7 +133,7 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     int mm = 0;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int m = W.lane + 32 * q;
+      const int m = W.lane + SW * q;
       if ((w >> m) & 1ull) {
         const int32_t x = q ? W.hidx[1] : W.hidx[0];
         if (x < idx) {
@@ -137,13 +142,13 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
         }
       }
     }
-    const int32_t bidx = __reduce_min_sync(FULL, idx);
-    const unsigned owner = __ballot_sync(FULL, idx == bidx);
+    const int32_t bidx = __reduce_min_sync(W.sm, idx);
+    const unsigned owner = __ballot_sync(W.sm, idx == bidx) >> W.sbase;
     const int src = __ffs(owner) - 1;
-    const int bm = __shfl_sync(FULL, mm, src);
-    const int q = bm >> 5;
-    const int32_t h = __shfl_sync(FULL, q ? W.head[1] : W.head[0], src);
-    const int32_t seen = __shfl_sync(FULL, q ? W.seen[1] : W.seen[0], src);
+    const int bm = __shfl_sync(W.sm, mm, src, SW);
+    const int q = bm / SW;
+    const int32_t h = __shfl_sync(W.sm, q ? W.head[1] : W.head[0], src, SW);
+    const int32_t seen = __shfl_sync(W.sm, q ? W.seen[1] : W.seen[0], src, SW);
     const int64_t ah = __ldg(tr.arrival + bidx);
     const int64_t slo = __ldg(pr.slo + bm);
     const int64_t waiting = seen - h;
@@ -152,7 +157,7 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     // k (increments >= 0) and the head has the tightest deadline, so the
     // feasible sizes form a prefix 1..K
     int64_t K = 0, fK = 0;
-    for (int64_t k0 = 1; k0 <= lim; k0 += 32) {
+    for (int64_t k0 = 1; k0 <= lim; k0 += SW) {
       const int64_t k = k0 + W.lane;
       int64_t f = 0;
       bool ok = false;
@@ -161,12 +166,12 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
         ok = f - ah <= slo;
         W.upd += (unsigned)s;
       }
-      const unsigned bal = __ballot_sync(FULL, ok);
+      const unsigned bal = (__ballot_sync(W.sm, ok) >> W.sbase) & (W.sm >> W.sbase);
       if (!bal) break;
       const int last = 31 - __clz(bal);
       K = k0 + last;
-      fK = __shfl_sync(FULL, f, last);
-      if (bal != FULL) break;
+      fK = __shfl_sync(W.sm, f, last, SW);
+      if (bal != (W.sm >> W.sbase)) break;
     }
     const int32_t nh = h + (int32_t)(K == 0 ? 1 : K);  // K == 0: the head is rejected
     if (W.lane == src) {
@@ -183,51 +188,57 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     if (K == 0) continue;
     if (W.lane == 0) batch_commit(pr, bp, W.F, p, off, s, bm, T, K);
     int64_t lat = 0;
-    const int32_t* members = bp.midx + __shfl_sync(FULL, q ? W.mo[1] : W.mo[0], src) + h;
-    for (int64_t j = W.lane; j < K; j += 32) lat += fK - __ldg(tr.arrival + __ldg(members + j));
-    W.sum += warp_sum64(lat);
+    const int32_t* members = bp.midx + __shfl_sync(W.sm, q ? W.mo[1] : W.mo[0], src, SW) + h;
+    for (int64_t j = W.lane; j < K; j += SW) lat += fK - __ldg(tr.arrival + __ldg(members + j));
+    W.sum += warp_sum64<SW>(W.sm, lat);
     W.good += K;
     if (W.lane == src) {
       if (q) W.pm[1] += (int32_t)K;
       else W.pm[0] += (int32_t)K;
     }
-    __syncwarp();
+    __syncwarp(W.sm);
     return;
   }
 }
 
 // The earliest availability event: (first-stage free time, group) minimum
 // over the groups that host a model with waiting requests; INT64_MAX if none.
+template <int SW>
 __device__ __forceinline__ void earliest_event(const Warp& W, uint64_t qmask, int64_t& key,
                                                int& gi) {
   key = INT64_MAX;
   gi = 0x7FFFFFFF;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    if (W.my_gt[q] == 0xFFFFFFFFu || !(W.gm[W.lane + 32 * q] & qmask)) continue;
+    if (W.my_gt[q] == 0xFFFFFFFFu || !(W.gm[W.lane + SW * q] & qmask)) continue;
     const int64_t f0 = W.F[gt_off(W.my_gt[q])];
     if (f0 < key) {  // q ascending: the lane's lower group first on ties
       key = f0;
-      gi = W.lane + 32 * q;
+      gi = W.lane + SW * q;
     }
   }
-  warp_argmin(key, gi);
+  warp_argmin<SW>(W.sm, W.sbase, key, gi);
 }
 
-template <int kMinBlocks>
+template <int kMinBlocks, int SW>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t slots,
                 DevOut out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kWarps + warp;
-  if (w >= bt.C) return;  // warp-uniform
+  // one candidate per SW-lane (sub-)warp: SW = 32, or 16 when every
+  // placement has <= 32 groups and the problem <= 32 models
+  const int sub = threadIdx.x / SW;  // sub-warp index in the block
+  const int lane = threadIdx.x % SW;
+  const int64_t w = (int64_t)blockIdx.x * (kWarps * 32 / SW) + sub;
+  if (w >= bt.C) return;  // uniform in the sub-warp; every sync below uses its mask
   const int64_t c = bp.order ? (int64_t)bp.order[w] : w;
   const int G = bt.G, M = pr.M;
-  unsigned char* base = smem + ((((size_t)slots * 8 + (size_t)G * 12) + 15) & ~(size_t)15) * warp;
+  unsigned char* base = smem + ((((size_t)slots * 8 + (size_t)G * 12) + 15) & ~(size_t)15) * sub;
   Warp W;
   W.lane = lane;
+  W.sbase = (threadIdx.x & 31) - lane;
+  W.sm = (SW == 32 ? FULL : 0xFFFFu) << W.sbase;
+  const unsigned sm = W.sm;
   W.F = reinterpret_cast<int64_t*>(base);
   uint64_t* gm = reinterpret_cast<uint64_t*>(base + (size_t)slots * 8);
   uint32_t* gt = reinterpret_cast<uint32_t*>(base + (size_t)slots * 8 + (size_t)G * 8);
@@ -249,20 +260,20 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
       gt[g] = e;
     }
   }
-  for (int g = lane; g < G; g += 32) {
+  for (int g = lane; g < G; g += SW) {
     uint64_t h = 0;
     for (int m = 0; m < M; ++m) h |= ((__ldg(bmask + m) >> g) & 1ull) << m;
     gm[g] = active ? h : 0ull;
   }
-  for (int k = lane; k < slots; k += 32) W.F[k] = 0;
-  __syncwarp();
+  for (int k = lane; k < slots; k += SW) W.F[k] = 0;
+  __syncwarp(sm);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int g = lane + 32 * q;
+    const int g = lane + SW * q;
     W.my_gt[q] = g < G ? gt[g] : 0xFFFFFFFFu;
     W.head[q] = 0;
     W.hidx[q] = 0;
-    W.mo[q] = lane + 32 * q < M ? __ldg(bp.moff + lane + 32 * q) : 0;
+    W.mo[q] = lane + SW * q < M ? __ldg(bp.moff + lane + SW * q) : 0;
     W.seen[q] = 0;
     W.pm[q] = 0;
   }
@@ -274,29 +285,29 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   int nevg = 0;
   bool nev_ok = false;
 
-  for (int64_t i0 = 0; i0 < tr.n && active; i0 += 32) {
+  for (int64_t i0 = 0; i0 < tr.n && active; i0 += SW) {
     const int64_t ai = tr.arrival[i0 + lane];
     const int mi = tr.model[i0 + lane];
-    const int nj = (int)min((int64_t)32, tr.n - i0);
+    const int nj = (int)min((int64_t)SW, tr.n - i0);
     for (int j = 0; j < nj; ++j) {
-      const int64_t a = __shfl_sync(FULL, ai, j);
-      const int m = __shfl_sync(FULL, mi, j);
+      const int64_t a = __shfl_sync(sm, ai, j, SW);
+      const int m = __shfl_sync(sm, mi, j, SW);
       // replay the availability events at time <= a in (time, group) order;
       // the earliest one is cached until a batch or a newly waiting request
       // changes it (an immediate run uses an available group, which has no
       // waiting work, so it cannot change it)
       if (qmask) {
         if (!nev_ok) {
-          earliest_event(W, qmask, nev, nevg);
+          earliest_event<SW>(W, qmask, nev, nevg);
           nev_ok = true;
         }
         while (nev <= a) {
-          form_batch(pr, tr, bp, W, qmask, nevg, nev);
-          earliest_event(W, qmask, nev, nevg);
+          form_batch<SW>(pr, tr, bp, W, qmask, nevg, nev);
+          earliest_event<SW>(W, qmask, nev, nevg);
         }
       }
-      const int q = m >> 5;
-      const bool own = (m & 31) == lane;
+      const int q = m / SW;
+      const bool own = (m % SW) == lane;
       const uint64_t hosts = __ldg(bmask + m);
       if (hosts && !((qmask >> m) & 1ull)) {
         // empty queue: run now on the available host with the earliest finish
@@ -304,7 +315,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
         int gi = 0x7FFFFFFF;
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {
-          const int g = lane + 32 * qq;
+          const int g = lane + SW * qq;
           if (g >= 64 || !((hosts >> g) & 1ull)) continue;
           const uint32_t e = W.my_gt[qq];
           if (W.F[gt_off(e)] > a) continue;  // first stage busy
@@ -315,7 +326,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
             gi = g;
           }
         }
-        warp_argmin(key, gi);
+        warp_argmin<SW>(sm, W.sbase, key, gi);
         if (gi == 0x7FFFFFFF) {  // every host busy: wait for a batch
           qmask |= 1ull << m;
           nev_ok = false;
@@ -331,8 +342,8 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
           }
         } else {
           if (key - a <= __ldg(pr.slo + m)) {  // else rejected at receipt (C2, C3)
-            if (lane == (gi & 31)) {
-              const uint32_t e = (gi >> 5) ? W.my_gt[1] : W.my_gt[0];
+            if (lane == (gi % SW)) {
+              const uint32_t e = (gi / SW) ? W.my_gt[1] : W.my_gt[0];
               batch_commit(pr, bp, W.F, gt_cfg(e), gt_off(e), gt_stages(e), m, a, 1);
             }
             W.good += 1;
@@ -346,7 +357,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
             if (q) W.head[1] = W.seen[1] + 1;
             else W.head[0] = W.seen[0] + 1;
           }
-          __syncwarp();
+          __syncwarp(sm);
         }
       }
       if (own) {
@@ -356,19 +367,19 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
     }
   }
   while (active && qmask) {  // drain
-    earliest_event(W, qmask, nev, nevg);
-    form_batch(pr, tr, bp, W, qmask, nevg, nev);
+    earliest_event<SW>(W, qmask, nev, nevg);
+    form_batch<SW>(pr, tr, bp, W, qmask, nevg, nev);
   }
   if (out.stage_updates) {
     unsigned long long u = W.upd;
-    for (int w = 16; w > 0; w >>= 1) u += __shfl_down_sync(FULL, u, w);
+    for (int x = SW / 2; x > 0; x >>= 1) u += __shfl_down_sync(sm, u, x, SW);
     if (lane == 0) atomicAdd(out.stage_updates, u);
   }
   const int64_t o = c - out.out_offset;
   if (out.good_per_model && active) {
 #pragma unroll
     for (int q = 0; q < 2; ++q)
-      if (lane + 32 * q < M) out.good_per_model[o * M + lane + 32 * q] = W.pm[q];
+      if (lane + SW * q < M) out.good_per_model[o * M + lane + SW * q] = W.pm[q];
   }
   if (lane == 0) {
     out.good[o] = active ? W.good : -1;
@@ -388,7 +399,6 @@ cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevB
                             cudaStream_t stream, int64_t* launches) {
   if (b.C <= 0) return cudaSuccess;
   if (slots < 1) slots = 1;
-  const size_t smem = (size_t)kWarps * batching_smem_per_warp(slots, b.G, pr.M);
   // resident blocks per SM the register budget is sized for (ASIM_BATCH_MINB
   // = 4 | 6 | 8; 4 = 128 registers, no spills)
   static const int minb = [] {
@@ -396,12 +406,25 @@ cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevB
     const int v = e ? atoi(e) : 4;
     return (v == 6 || v == 8) ? v : 4;
   }();
-  auto kern = minb == 8 ? batching_kernel<8> : minb == 6 ? batching_kernel<6> : batching_kernel<4>;
+  // half-warp candidates (ASIM_BATCH_SW=16; placements of <= 32 groups and
+  // <= 32 models): bit-exact, but measured 4 % slower than full warps on the
+  // §5.4 bench (the two halves' event handling diverges), so off by default
+  static const bool want16 = [] {
+    const char* e = getenv("ASIM_BATCH_SW");
+    return e && atoi(e) == 16;
+  }();
+  const bool half = want16 && b.G <= 32 && pr.M <= 32;
+  auto kern = half ? (minb == 8 ? batching_kernel<8, 16> : minb == 6 ? batching_kernel<6, 16>
+                                                                     : batching_kernel<4, 16>)
+                   : (minb == 8 ? batching_kernel<8, 32> : minb == 6 ? batching_kernel<6, 32>
+                                                                     : batching_kernel<4, 32>);
+  const int per_block = kWarps * (half ? 2 : 1);  // candidates per block
+  const size_t smem_b = (size_t)per_block * batching_smem_per_warp(slots, b.G, pr.M);
   cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024);
   if (ea != cudaSuccess) return ea;
-  const int blocks = (int)((b.C + kWarps - 1) / kWarps);
-  kern<<<blocks, kWarps * 32, smem, stream>>>(pr, tr, b, bp, slots, out);
+  const int blocks = (int)((b.C + per_block - 1) / per_block);
+  kern<<<blocks, kWarps * 32, smem_b, stream>>>(pr, tr, b, bp, slots, out);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -170,6 +170,11 @@ def main():
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     peak = sms * 64 * sm_max * 1e6 / 1e9
     achieved = st["stage_updates"] / max(st["sim_ms"], 1e-9) / 1e6
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["S1-batching"] / 1e9
+    except (OSError, KeyError, ValueError):
+        pass
     line = dict(
         metric=METRIC, value=value, unit=UNIT, n_gpus=1, steps=args.steps, warmup=args.warmup,
         ms_per_step=total_ms / args.steps, higher_is_better=True, scaling="weak",
@@ -182,7 +187,9 @@ def main():
                     l2="flushed between timed steps (256 MB write)"),
         gpu_launches=int(launches),
         roofline=dict(bound="alu", achieved=achieved, peak=peak, unit="G stage-updates/s",
-                      frac=achieved / peak, traffic=None, kernel="batching_kernel",
+                      frac=achieved / peak, traffic=traffic,
+                      traffic_unit="GB DRAM per launch (ncu --set full, profiles/traffic.json)",
+                      kernel="batching_kernel",
                       kernel_ms=st["sim_ms"], stage_updates=st["stage_updates"],
                       kernel_ms_share=st["sim_ms"] / max(total_ms, 1e-9),
                       peak_basis="148 SMs x 64 int max/clk x 1965 MHz (MEASURED_PEAKS sm_max_mhz)"),

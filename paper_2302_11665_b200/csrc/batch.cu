@@ -109,9 +109,8 @@ struct Warp {
   uint32_t my_gt[2];   // lane's groups lane, lane + 32 (0xFFFFFFFF = none)
   int32_t head[2];     // lane's models lane, lane + 32
   int32_t seen[2];
-  int32_t pm[2];       // good per model (< n <= 2^31 - 1)
+  int64_t* pm;         // this candidate's good-per-model row (nullable; one writer per entry)
   int32_t hidx[2];     // trace index of the head request (valid while waiting)
-  int32_t mo[2];       // start of the model's request list (CSR offset)
   int64_t good, sum;
   unsigned long long upd;
 };
@@ -175,7 +174,7 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     }
     const int32_t nh = h + (int32_t)(K == 0 ? 1 : K);  // K == 0: the head is rejected
     if (W.lane == src) {
-      const int32_t nx = nh < seen ? __ldg(bp.midx + (q ? W.mo[1] : W.mo[0]) + nh) : 0;
+      const int32_t nx = nh < seen ? __ldg(bp.midx + __ldg(bp.moff + bm) + nh) : 0;
       if (q) {
         W.head[1] = nh;
         W.hidx[1] = nx;
@@ -188,13 +187,12 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     if (K == 0) continue;
     if (W.lane == 0) batch_commit(pr, bp, W.F, p, off, s, bm, T, K);
     int64_t lat = 0;
-    const int32_t* members = bp.midx + __shfl_sync(W.sm, q ? W.mo[1] : W.mo[0], src, SW) + h;
+    const int32_t* members = bp.midx + __ldg(bp.moff + bm) + h;
     for (int64_t j = W.lane; j < K; j += SW) lat += fK - __ldg(tr.arrival + __ldg(members + j));
     W.sum += warp_sum64<SW>(W.sm, lat);
     W.good += K;
     if (W.lane == src) {
-      if (q) W.pm[1] += (int32_t)K;
-      else W.pm[0] += (int32_t)K;
+      if (W.pm) W.pm[bm] += K;
     }
     __syncwarp(W.sm);
     return;
@@ -273,11 +271,12 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
     W.my_gt[q] = g < G ? gt[g] : 0xFFFFFFFFu;
     W.head[q] = 0;
     W.hidx[q] = 0;
-    W.mo[q] = lane + SW * q < M ? __ldg(bp.moff + lane + SW * q) : 0;
     W.seen[q] = 0;
-    W.pm[q] = 0;
   }
   W.good = 0;
+  // per-model counts go straight to the candidate's (zeroed) output row: each
+  // entry has one writer, the lane that owns the model
+  W.pm = out.good_per_model ? out.good_per_model + (c - out.out_offset) * M : nullptr;
   W.sum = 0;
   W.upd = 0;
   uint64_t qmask = 0;  // models with waiting requests (warp-uniform)
@@ -349,8 +348,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
             W.good += 1;
             W.sum += key - a;
             if (own) {
-              if (q) W.pm[1] += 1;
-              else W.pm[0] += 1;
+              if (W.pm) W.pm[m] += 1;
             }
           }
           if (own) {
@@ -376,11 +374,6 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
     if (lane == 0) atomicAdd(out.stage_updates, u);
   }
   const int64_t o = c - out.out_offset;
-  if (out.good_per_model && active) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (lane + SW * q < M) out.good_per_model[o * M + lane + SW * q] = W.pm[q];
-  }
   if (lane == 0) {
     out.good[o] = active ? W.good : -1;
     if (out.sum_latency) out.sum_latency[o] = active ? W.sum : 0;
@@ -400,11 +393,12 @@ cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevB
   if (b.C <= 0) return cudaSuccess;
   if (slots < 1) slots = 1;
   // resident blocks per SM the register budget is sized for (ASIM_BATCH_MINB
-  // = 4 | 6 | 8; 4 = 128 registers, no spills)
+  // = 4 | 5 | 6 | 8; default 4: 128 registers; 5 = 96 registers without
+  // spills and 20 warps/SM measured 2 % slower, 6 and 8 spill)
   static const int minb = [] {
     const char* e = getenv("ASIM_BATCH_MINB");
     const int v = e ? atoi(e) : 4;
-    return (v == 6 || v == 8) ? v : 4;
+    return (v == 5 || v == 6 || v == 8) ? v : 4;
   }();
   // half-warp candidates (ASIM_BATCH_SW=16; placements of <= 32 groups and
   // <= 32 models): bit-exact, but measured 4 % slower than full warps on the
@@ -414,10 +408,13 @@ cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevB
     return e && atoi(e) == 16;
   }();
   const bool half = want16 && b.G <= 32 && pr.M <= 32;
-  auto kern = half ? (minb == 8 ? batching_kernel<8, 16> : minb == 6 ? batching_kernel<6, 16>
-                                                                     : batching_kernel<4, 16>)
-                   : (minb == 8 ? batching_kernel<8, 32> : minb == 6 ? batching_kernel<6, 32>
-                                                                     : batching_kernel<4, 32>);
+  auto pick = [&](auto k4, auto k5, auto k6, auto k8) {
+    return minb == 8 ? k8 : minb == 6 ? k6 : minb == 4 ? k4 : k5;
+  };
+  auto kern = half ? pick(batching_kernel<4, 16>, batching_kernel<5, 16>, batching_kernel<6, 16>,
+                          batching_kernel<8, 16>)
+                   : pick(batching_kernel<4, 32>, batching_kernel<5, 32>, batching_kernel<6, 32>,
+                          batching_kernel<8, 32>);
   const int per_block = kWarps * (half ? 2 : 1);  // candidates per block
   const size_t smem_b = (size_t)per_block * batching_smem_per_warp(slots, b.G, pr.M);
   cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -231,15 +231,18 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   if (w >= bt.C) return;  // uniform in the sub-warp; every sync below uses its mask
   const int64_t c = bp.order ? (int64_t)bp.order[w] : w;
   const int G = bt.G, M = pr.M;
-  unsigned char* base = smem + ((((size_t)slots * 8 + (size_t)G * 12) + 15) & ~(size_t)15) * sub;
+  unsigned char* base =
+      smem + ((((size_t)slots * 8 + (size_t)M * 8 + (size_t)G * 12) + 15) & ~(size_t)15) * sub;
   Warp W;
   W.lane = lane;
   W.sbase = (threadIdx.x & 31) - lane;
   W.sm = (SW == 32 ? FULL : 0xFFFFu) << W.sbase;
   const unsigned sm = W.sm;
   W.F = reinterpret_cast<int64_t*>(base);
-  uint64_t* gm = reinterpret_cast<uint64_t*>(base + (size_t)slots * 8);
-  uint32_t* gt = reinterpret_cast<uint32_t*>(base + (size_t)slots * 8 + (size_t)G * 8);
+  uint64_t* hm = reinterpret_cast<uint64_t*>(base + (size_t)slots * 8);  // [M] host masks
+  uint64_t* gm = reinterpret_cast<uint64_t*>(base + (size_t)slots * 8 + (size_t)M * 8);
+  uint32_t* gt = reinterpret_cast<uint32_t*>(base + (size_t)slots * 8 + (size_t)M * 8 +
+                                             (size_t)G * 8);
   W.gm = gm;
   W.gt = gt;
   const bool active = bt.cand_ok[c] != 0;
@@ -264,6 +267,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
     gm[g] = active ? h : 0ull;
   }
   for (int k = lane; k < slots; k += SW) W.F[k] = 0;
+  for (int m = lane; m < M; m += SW) hm[m] = __ldg(bmask + m);
   __syncwarp(sm);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -307,7 +311,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
       }
       const int q = m / SW;
       const bool own = (m % SW) == lane;
-      const uint64_t hosts = __ldg(bmask + m);
+      const uint64_t hosts = hm[m];
       if (hosts && !((qmask >> m) & 1ull)) {
         // empty queue: run now on the available host with the earliest finish
         int64_t key = INT64_MAX;
@@ -383,8 +387,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
 }  // namespace
 
 size_t batching_smem_per_warp(int32_t slots, int32_t G, int32_t M) {
-  (void)M;
-  return (((size_t)slots * 8 + (size_t)G * 12) + 15) & ~(size_t)15;
+  return (((size_t)slots * 8 + (size_t)M * 8 + (size_t)G * 12) + 15) & ~(size_t)15;
 }
 
 cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevBatch& b,

@@ -82,7 +82,9 @@ __device__ __forceinline__ int64_t batch_finish(const DevProblem& pr, const DevB
   const int64_t* d = pr.stage + row;
   const int64_t* inc = bp.inc + row;
   int64_t x = T;
-  for (int j = 0; j < s; ++j) x = imax64(x, F[off + j]) + __ldg(d + j) + (k - 1) * __ldg(inc + j);
+  const int64_t k1 = k - 1;
+#pragma unroll 4
+  for (int j = 0; j < s; ++j) x = imax64(x, F[off + j]) + (__ldg(d + j) + k1 * __ldg(inc + j));
   return x + __ldg(pr.tail + (int64_t)m * pr.P + p);
 }
 
@@ -93,8 +95,10 @@ __device__ __forceinline__ void batch_commit(const DevProblem& pr, const DevBatc
   const int64_t* d = pr.stage + row;
   const int64_t* inc = bp.inc + row;
   int64_t x = T;
+  const int64_t k1 = k - 1;
+#pragma unroll 4
   for (int j = 0; j < s; ++j) {
-    x = imax64(x, F[off + j]) + __ldg(d + j) + (k - 1) * __ldg(inc + j);
+    x = imax64(x, F[off + j]) + (__ldg(d + j) + k1 * __ldg(inc + j));
     F[off + j] = x;
   }
 }

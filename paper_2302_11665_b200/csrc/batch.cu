@@ -114,6 +114,7 @@ struct Warp {
   int32_t head[2];     // lane's models lane, lane + 32
   int32_t seen[2];
   int64_t* pm;         // this candidate's good-per-model row (nullable; one writer per entry)
+  const int32_t* mo;   // [M] start of each model's request list (shared)
   int32_t hidx[2];     // trace index of the head request (valid while waiting)
   int64_t good, sum;
   unsigned long long upd;
@@ -178,7 +179,7 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     }
     const int32_t nh = h + (int32_t)(K == 0 ? 1 : K);  // K == 0: the head is rejected
     if (W.lane == src) {
-      const int32_t nx = nh < seen ? __ldg(bp.midx + __ldg(bp.moff + bm) + nh) : 0;
+      const int32_t nx = nh < seen ? __ldg(bp.midx + W.mo[bm] + nh) : 0;
       if (q) {
         W.head[1] = nh;
         W.hidx[1] = nx;
@@ -191,7 +192,7 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     if (K == 0) continue;
     if (W.lane == 0) batch_commit(pr, bp, W.F, p, off, s, bm, T, K);
     int64_t lat = 0;
-    const int32_t* members = bp.midx + __ldg(bp.moff + bm) + h;
+    const int32_t* members = bp.midx + W.mo[bm] + h;
     for (int64_t j = W.lane; j < K; j += SW) lat += fK - __ldg(tr.arrival + __ldg(members + j));
     W.sum += warp_sum64<SW>(W.sm, lat);
     W.good += K;
@@ -236,7 +237,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   const int64_t c = bp.order ? (int64_t)bp.order[w] : w;
   const int G = bt.G, M = pr.M;
   unsigned char* base =
-      smem + ((((size_t)slots * 8 + (size_t)M * 8 + (size_t)G * 12) + 15) & ~(size_t)15) * sub;
+      smem + ((((size_t)slots * 8 + (size_t)M * 12 + (size_t)G * 12) + 15) & ~(size_t)15) * sub;
   Warp W;
   W.lane = lane;
   W.sbase = (threadIdx.x & 31) - lane;
@@ -247,6 +248,9 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
   uint64_t* gm = reinterpret_cast<uint64_t*>(base + (size_t)slots * 8 + (size_t)M * 8);
   uint32_t* gt = reinterpret_cast<uint32_t*>(base + (size_t)slots * 8 + (size_t)M * 8 +
                                              (size_t)G * 8);
+  int32_t* mo = reinterpret_cast<int32_t*>(base + (size_t)slots * 8 + (size_t)M * 8 +
+                                           (size_t)G * 12);  // [M] request-list offsets
+  W.mo = mo;
   W.gm = gm;
   W.gt = gt;
   const bool active = bt.cand_ok[c] != 0;
@@ -271,7 +275,10 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
     gm[g] = active ? h : 0ull;
   }
   for (int k = lane; k < slots; k += SW) W.F[k] = 0;
-  for (int m = lane; m < M; m += SW) hm[m] = __ldg(bmask + m);
+  for (int m = lane; m < M; m += SW) {
+    hm[m] = __ldg(bmask + m);
+    mo[m] = __ldg(bp.moff + m);
+  }
   __syncwarp(sm);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -391,7 +398,7 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
 }  // namespace
 
 size_t batching_smem_per_warp(int32_t slots, int32_t G, int32_t M) {
-  return (((size_t)slots * 8 + (size_t)M * 8 + (size_t)G * 12) + 15) & ~(size_t)15;
+  return (((size_t)slots * 8 + (size_t)M * 12 + (size_t)G * 12) + 15) & ~(size_t)15;
 }
 
 cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevBatch& b,

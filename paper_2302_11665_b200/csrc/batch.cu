@@ -366,17 +366,13 @@ batching_kernel(DevProblem pr, DevTrace tr, DevBatch bt, DevBatching bp, int32_t
               if (W.pm) W.pm[m] += 1;
             }
           }
-          if (own) {
-            if (q) W.head[1] = W.seen[1] + 1;
-            else W.head[0] = W.seen[0] + 1;
-          }
+          W.head[0] = (own && q == 0) ? W.seen[0] + 1 : W.head[0];
+          W.head[1] = (own && q == 1) ? W.seen[1] + 1 : W.head[1];
           __syncwarp(sm);
         }
       }
-      if (own) {
-        if (q) W.seen[1] += 1;
-        else W.seen[0] += 1;
-      }
+      W.seen[0] += (int32_t)(own && q == 0);  // branch-free: one owner lane per request
+      W.seen[1] += (int32_t)(own && q == 1);
     }
   }
   while (active && qmask) {  // drain

@@ -73,6 +73,8 @@ struct DevBatching {
   const int32_t* moff;     // [M+1]
   const int32_t* midx;     // [n] trace indices grouped by model
   const int32_t* order;    // [C] candidate simulated by warp w (costliest first), nullable
+  const uint64_t* mcum;    // [n + M] per model, running sums of its arrivals mod 2^64
+                           // (entry moff[m] + m + i = sum of its first i arrivals)
 };
 size_t batching_smem_per_warp(int32_t slots, int32_t G, int32_t M);
 cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevBatch& b,

@@ -66,13 +66,6 @@ __device__ __forceinline__ void warp_argmin(unsigned sm, int sbase, int64_t& key
   }
 }
 
-template <int SW>
-__device__ __forceinline__ int64_t warp_sum64(unsigned sm, int64_t v) {
-#pragma unroll
-  for (int w = SW / 2; w > 0; w >>= 1) v += __shfl_xor_sync(sm, v, w, SW);
-  return v;
-}
-
 // Tandem recurrence (C5) of a batch of k requests of model m entering a group
 // with config p whose stage slots start at F[off], at time T.
 __device__ __forceinline__ int64_t batch_finish(const DevProblem& pr, const DevBatching& bp,
@@ -191,10 +184,11 @@ __device__ __forceinline__ void form_batch(const DevProblem& pr, const DevTrace&
     if (nh == seen) qmask &= ~(1ull << bm);
     if (K == 0) continue;
     if (W.lane == 0) batch_commit(pr, bp, W.F, p, off, s, bm, T, K);
-    int64_t lat = 0;
-    const int32_t* members = bp.midx + W.mo[bm] + h;
-    for (int64_t j = W.lane; j < K; j += SW) lat += fK - __ldg(tr.arrival + __ldg(members + j));
-    W.sum += warp_sum64<SW>(W.sm, lat);
+    // sum over the members of (fK - a_j) = K fK - (their arrivals), the
+    // latter a difference of the model's running arrival sums; modulo 2^64
+    // the result is exact because it lies in [0, 2^63) (reading C20)
+    const uint64_t* cum = bp.mcum + W.mo[bm] + bm + h;
+    W.sum += (int64_t)((uint64_t)K * (uint64_t)fK - (__ldg(cum + K) - __ldg(cum)));
     W.good += K;
     if (W.lane == src) {
       if (W.pm) W.pm[bm] += K;

@@ -294,7 +294,7 @@ void asim_destroy(asim_ctx* ctx) {
   {
     DeviceGuard dg(ctx->device);
     DBuf* bufs[] = {&ctx->d_stage, &ctx->d_tail, &ctx->d_slo, &ctx->d_cfg_stages,
-                    &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc, &ctx->d_order,
+                    &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc, &ctx->d_order, &ctx->d_mcum,
                     &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group,
                     &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm, &ctx->d_busy,
@@ -692,8 +692,24 @@ asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
     for (int64_t k = 0; k < M; ++k) moff[k + 1] += moff[k];
     std::vector<int32_t> fill(moff.begin(), moff.end() - 1);
     for (int64_t i = 0; i < n; ++i) midx[fill[mh[i]]++] = (int32_t)i;
+    // running arrival sums per model (mod 2^64): model m's block starts at
+    // moff[m] + m and has moff[m+1] - moff[m] + 1 entries
+    std::vector<int64_t> arr(n > 0 ? n : 1);
+    if (n > 0) e = cudaMemcpy(arr.data(), ctx->d_arrival.p, n * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "download trace arrivals");
+    std::vector<uint64_t> mcum(n + M, 0);
+    for (int64_t k = 0; k < M; ++k) {
+      uint64_t acc = 0;
+      const int64_t b0 = moff[k] + k;
+      mcum[b0] = 0;
+      for (int64_t i = moff[k]; i < moff[k + 1]; ++i) {
+        acc += (uint64_t)arr[midx[i]];
+        mcum[b0 + (i - moff[k]) + 1] = acc;
+      }
+    }
     e = upload(ctx->d_moff, moff, st);
     if (e == cudaSuccess) e = upload(ctx->d_midx, midx, st);
+    if (e == cudaSuccess) e = upload(ctx->d_mcum, mcum, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "upload per-model request lists");
     ctx->has_midx = true;
@@ -753,6 +769,7 @@ asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
   }
   asim::DevBatching bp;
   bp.order = ctx->d_order.as<int32_t>();
+  bp.mcum = ctx->d_mcum.as<uint64_t>();
   bp.max_batch = opt->max_batch;
   bp.inc = ctx->d_inc.as<int64_t>();
   bp.moff = ctx->d_moff.as<int32_t>();

@@ -66,6 +66,7 @@ struct asim_ctx {
   bool has_midx = false;  // d_moff/d_midx match the current trace
   DBuf d_inc;           // batching stage increments (asim_evaluate_batching)
   DBuf d_order;         // batching launch order (costliest candidates first)
+  DBuf d_mcum;          // per-model running arrival sums (batching)
 
   // statistics (asim_set_profiling)
   bool profiling = false;

@@ -104,6 +104,11 @@ typedef struct {
                                    the sequential critical path of the walk pass */
   double spec_ms;               /* summed device time of the chunked path's pass-1 launches */
   int64_t spec_stage_updates;   /* stage updates performed by pass 1 (part of stage_updates) */
+  double pass2_ms;              /* summed device time of the chunked path's pass-2 launches */
+  double walk_ms;               /* summed device time of the walk pass (all walkers) */
+  int64_t spec_lane_slots;      /* pass 1: requests processed by its warps x 32 lanes */
+  int64_t spec_live_lanes;      /* pass 1: (request, lane) pairs whose candidate simulates the
+                                   request (live); live / slots = lane utilisation */
 } asim_stats;
 asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
 asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);
@@ -258,6 +263,15 @@ asim_status asim_evaluate_batching(asim_ctx* ctx, const asim_candidates* cands,
                                    const asim_batching* opt, asim_results* out,
                                    void* cuda_stream);
 
+/* pick_highest_SLO_attainment (Alg. 1) over any vector of good counts,
+ * e.g. the gathered shards of a multi-GPU evaluation: *out = index of the
+ * maximum (ties -> lowest index), -1 when n == 0 or every entry is < 0
+ * (infeasible).  good: n int64, host or device per ptr_kind; out: host,
+ * complete on return (the call synchronises cuda_stream).  Does not need a
+ * problem or trace.  Errors: ASIM_EINVAL (null / bad kind), ASIM_ERANGE (n < 0). */
+asim_status asim_argmax(asim_ctx* ctx, const int64_t* good, int64_t n, int32_t ptr_kind,
+                        int64_t* out, void* cuda_stream);
+
 /* SLO attainment = good / n; n == 0 -> 1.0; good < 0 -> -1.0. */
 double asim_attainment(int64_t good, int64_t n);
 
@@ -402,6 +416,14 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates);
 asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int64_t* good_dev,
                                  void* cuda_stream);
 asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void* cuda_stream);
+/* Work estimate of every candidate of the prepared step (shards
+ * "balanced by estimated cost"): the trace requests its simulation replays
+ * (those of the models of its hosting-graph component, or all n without
+ * component restriction) times the stage count of the group it adds to; >= 1.
+ * Identical on every rank (it depends only on the search state), so every rank
+ * derives the same contiguous shard bounds from it.  Fills min(cap, C) entries
+ * of the host array `cost`.  ASIM_ESTATE outside prepare ... apply. */
+asim_status asim_search_costs(const asim_search* s, int64_t cap, int64_t* cost);
 asim_status asim_search_run(asim_search* s, void* cuda_stream);
 asim_status asim_search_result_get(const asim_search* s, asim_search_result* out);
 /* Per-run outcome: best good of run r and its selection (host arrays). */
@@ -409,6 +431,25 @@ asim_status asim_search_run_info(const asim_search* s, int32_t run, int32_t* num
                                  int32_t* group_cfg, uint64_t* host_mask, int64_t* best_good,
                                  int64_t* steps);
 int32_t asim_search_num_runs(const asim_search* s);
+/* Step history of run r (Alg. 1's sel <- sel + (m*, g*) per iteration,
+ * P:720-724): for the i-th step so far, the model and group added and the
+ * good of the selection after it (the step's maximum; fast heuristic: the
+ * good of its next simulation, -1 while unknown).  Beam > 1: member 0's
+ * path.  Fills min(cap, steps) entries of the non-NULL arrays; *count =
+ * steps.  ASIM_EINVAL for a bad run, cap < 0 or NULL count. */
+asim_status asim_search_run_history(const asim_search* s, int32_t run, int64_t cap,
+                                    int32_t* model, int32_t* group, int64_t* good,
+                                    int64_t* count);
+/* The candidate list of run r's last step (Alg. 1's new_sels):
+ * every feasible addition (m, g) in (m, g) order with its good -- simulated,
+ * taken from the component memo, or from its duplicate's representative;
+ * INT64_MIN for a candidate removed by exact bounding (spec->cand_bound).
+ * Valid between asim_search_apply and the next asim_search_prepare
+ * (ASIM_ESTATE in between); empty once the run has stopped.  Beam > 1:
+ * member 0's list.  Fills min(cap, count) entries; *count = list length. */
+asim_status asim_search_run_candidates(const asim_search* s, int32_t run, int64_t cap,
+                                       int32_t* model, int32_t* group, int64_t* good,
+                                       int64_t* count);
 /* Step at which run r was pruned (spec->prune), -1 if it never was or r is
  * out of range. */
 int64_t asim_search_run_pruned(const asim_search* s, int32_t run);

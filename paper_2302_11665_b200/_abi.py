@@ -50,7 +50,9 @@ class asim_stats(ctypes.Structure):
     _fields_ = [("launches", i64), ("sim_launches", i64), ("sim_ms", ctypes.c_double),
                 ("stage_updates", i64), ("request_evals", i64), ("chunk_reruns", i64),
                 ("walk_candidates", i64), ("walk_critical_chunks", i64),
-                ("spec_ms", ctypes.c_double), ("spec_stage_updates", i64)]
+                ("spec_ms", ctypes.c_double), ("spec_stage_updates", i64),
+                ("pass2_ms", ctypes.c_double), ("walk_ms", ctypes.c_double),
+                ("spec_lane_slots", i64), ("spec_live_lanes", i64)]
 
 
 class asim_search_spec(ctypes.Structure):
@@ -110,17 +112,23 @@ asim_evaluate_deltas = _bind("asim_evaluate_deltas", i32,
                              [vp, _P(asim_deltas), _P(asim_results), vp])
 asim_evaluate_batching = _bind("asim_evaluate_batching", i32,
                                [vp, _P(asim_candidates), _P(asim_batching), _P(asim_results), vp])
+asim_argmax = _bind("asim_argmax", i32, [vp, vp, i64, i32, _P(i64), vp])
 asim_attainment = _bind("asim_attainment", ctypes.c_double, [i64, i64])
 asim_search_create = _bind("asim_search_create", i32, [vp, _P(asim_search_spec), _P(vp)])
 asim_search_destroy = _bind("asim_search_destroy", None, [vp])
 asim_search_prepare = _bind("asim_search_prepare", i32, [vp, _P(i64)])
 asim_search_evaluate = _bind("asim_search_evaluate", i32, [vp, i64, i64, vp, vp])
 asim_search_apply = _bind("asim_search_apply", i32, [vp, vp, vp])
+asim_search_costs = _bind("asim_search_costs", i32, [vp, i64, vp])
 asim_search_run = _bind("asim_search_run", i32, [vp, vp])
 asim_search_result_get = _bind("asim_search_result_get", i32, [vp, _P(asim_search_result)])
 asim_search_run_info = _bind("asim_search_run_info", i32,
                              [vp, i32, _P(i32), vp, vp, _P(i64), _P(i64)])
 asim_search_num_runs = _bind("asim_search_num_runs", i32, [vp])
+asim_search_run_history = _bind("asim_search_run_history", i32,
+                                [vp, i32, i64, vp, vp, vp, _P(i64)])
+asim_search_run_candidates = _bind("asim_search_run_candidates", i32,
+                                   [vp, i32, i64, vp, vp, vp, _P(i64)])
 asim_search_run_pruned = _bind("asim_search_run_pruned", i64, [vp, i32])
 asim_search_buckets_get = _bind("asim_search_buckets_get", i32, [vp, _P(asim_bucket_result)])
 

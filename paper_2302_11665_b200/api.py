@@ -135,7 +135,9 @@ class Simulator:
                     stage_updates=s.stage_updates, request_evals=s.request_evals,
                     chunk_reruns=s.chunk_reruns, walk_candidates=s.walk_candidates,
                     walk_critical_chunks=s.walk_critical_chunks, spec_ms=s.spec_ms,
-                    spec_stage_updates=s.spec_stage_updates)
+                    spec_stage_updates=s.spec_stage_updates, pass2_ms=s.pass2_ms,
+                    walk_ms=s.walk_ms, spec_lane_slots=s.spec_lane_slots,
+                    spec_live_lanes=s.spec_live_lanes)
 
     def set_chunk_size(self, min_requests: int) -> None:
         self._check(A.asim_set_chunk_size(self.h, int(min_requests)))
@@ -222,6 +224,19 @@ class Simulator:
         self._check(fn(self.h, ctypes.byref(cands), ctypes.byref(res), _stream_ptr(stream)))
         return dict(good=good, sum_latency_ns=sl, good_per_model=pm,
                     argmax=int(am[0]) if argmax else None, busy_ns=bz)
+
+    def argmax(self, good, stream=None) -> int:
+        """Library argmax kernel (max good, lowest index on ties, -1 if none
+        is feasible) over a host numpy array or a CUDA torch tensor."""
+        if _is_torch(good):
+            g = good.contiguous()
+            kind = A.ASIM_DEVICE if g.is_cuda else A.ASIM_HOST
+        else:
+            g, kind = _host(good, np.int64), A.ASIM_HOST
+        out = ctypes.c_int64()
+        self._check(A.asim_argmax(self.h, _ptr(g), int(g.shape[0]), kind, ctypes.byref(out),
+                                  _stream_ptr(stream)))
+        return int(out.value)
 
     # ------------------------------------------------------------- search
     def search_handle(self, runs=None, dedup=True, fast=False, buckets=None,
@@ -332,12 +347,39 @@ class SearchHandle:
         self.sim._check(A.asim_search_evaluate(self.h, int(begin), int(end), _ptr(good_dev),
                                                _stream_ptr(stream)))
 
+    def costs(self, C: int) -> np.ndarray:
+        """Per-candidate work estimate of the prepared step (C entries)."""
+        out = np.zeros(max(int(C), 0), np.int64)
+        self.sim._check(A.asim_search_costs(self.h, out.size, _ptr(out) if out.size else None))
+        return out
+
     def apply(self, good_all_dev, stream=None) -> None:
         self.sim._check(A.asim_search_apply(self.h, _ptr(good_all_dev) if good_all_dev is not None
                                             else None, _stream_ptr(stream)))
 
     def run(self, stream=None) -> None:
         self.sim._check(A.asim_search_run(self.h, _stream_ptr(stream)))
+
+    def num_runs(self) -> int:
+        return int(A.asim_search_num_runs(self.h))
+
+    def _triples(self, fn, run: int):
+        n = ctypes.c_int64()
+        self.sim._check(fn(self.h, int(run), 0, None, None, None, ctypes.byref(n)))
+        k = n.value
+        m = np.zeros(k, np.int32)
+        g = np.zeros(k, np.int32)
+        v = np.zeros(k, np.int64)
+        self.sim._check(fn(self.h, int(run), k, _ptr(m), _ptr(g), _ptr(v), ctypes.byref(n)))
+        return m, g, v
+
+    def history(self, run: int):
+        """(model[i], group[i], good[i]) of every step of `run` so far."""
+        return self._triples(A.asim_search_run_history, run)
+
+    def candidates(self, run: int):
+        """(model, group, good) of every candidate of `run`'s last step."""
+        return self._triples(A.asim_search_run_candidates, run)
 
     def result(self) -> SearchResult:
         M = self.sim.M

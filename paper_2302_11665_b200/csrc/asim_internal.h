@@ -89,7 +89,7 @@ namespace asim {
 // Work item: up to 32 consecutive candidates sharing one base placement.
 struct ItemDesc {
   int32_t base;    // base index in the batch
-  int32_t first;   // first candidate (batch index)
+  int32_t first;   // first candidate (batch index; ChunkParams.item_cand overrides)
   int32_t count;   // 1..32
   int32_t S;       // compile-time stage class: 1,2,4,8,16 (uniform config) or 0 (dynamic)
   int32_t cfg;     // the base's uniform config id, -1 if groups differ
@@ -104,6 +104,10 @@ struct ChunkParams {
   DevTrace tr;
   DevBatch bt;
   const ItemDesc* items;
+  // nullable: [num_items][32] batch index of the candidate in each lane (-1:
+  // none) when items are not runs of consecutive candidates (the host groups
+  // candidates by hosting component so a warp's lanes replay the same requests)
+  const int32_t* item_cand;
   int32_t num_items;
   int32_t J;                   // chunks
   const int64_t* chunk_begin;  // [J+1] request index boundaries
@@ -128,6 +132,8 @@ struct ChunkParams {
   int64_t* fix_epoch;
   uint32_t* fix_flag;          // [J][items] lanes whose trajectories never met in the chunk
   unsigned long long* stage_updates;  // nullable statistics counter
+  unsigned long long* lane_stats;     // nullable (pass 1): [0] lane slots = requests the warps
+                                      // processed x 32, [1] live lane-requests among them
   // Speculation source (nullable = idle): absolute int64 free times of the
   // base placement's TRUE trajectory at every chunk boundary,
   // spec_state[(spec_row[b] * J + j) * slots_max + k].  Any start state is

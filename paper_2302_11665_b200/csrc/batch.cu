@@ -31,6 +31,7 @@
 #include <stdlib.h>
 
 #include "asim_internal.h"
+#include "launch_cache.h"
 
 namespace asim {
 namespace {
@@ -421,8 +422,7 @@ cudaError_t launch_batching(const DevProblem& pr, const DevTrace& tr, const DevB
                           batching_kernel<8, 32>);
   const int per_block = kWarps * (half ? 2 : 1);  // candidates per block
   const size_t smem_b = (size_t)per_block * batching_smem_per_warp(slots, b.G, pr.M);
-  cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        227 * 1024);
+  cudaError_t ea = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (ea != cudaSuccess) return ea;
   const int blocks = (int)((b.C + per_block - 1) / per_block);
   kern<<<blocks, kWarps * 32, smem_b, stream>>>(pr, tr, b, bp, slots, out);

@@ -46,6 +46,7 @@
 #include <stdint.h>
 
 #include "asim_internal.h"
+#include "launch_cache.h"
 
 namespace asim {
 namespace {
@@ -55,6 +56,15 @@ constexpr int kWarps = 4;        // warps per block; each warp takes units indep
 constexpr int kSTab = 16;        // stage entries per model in the uniform-config table
 constexpr int kCheckEvery = 64;  // coalescence test period (requests) in the fix-up
 enum Mode { SPEC = 0, DUAL = 1, WALK = 2 };
+
+// Batch index of the candidate in lane `lane` of work item `item`: items
+// either hold consecutive candidates (it.first + lane) or an explicit list
+// (item_cand, when the host regrouped the candidates by hosting component).
+__device__ __forceinline__ int64_t cand_of(const ChunkParams& P, const ItemDesc& it, int item,
+                                           int lane) {
+  return P.item_cand ? (int64_t)P.item_cand[(int64_t)item * 32 + lane]
+                     : (int64_t)it.first + lane;
+}
 
 template <typename T>
 struct TT;
@@ -491,7 +501,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
                                              int item, int j, int lane, uint32_t srcmask) {
   const int64_t i_begin = P.chunk_begin[j], i_end = P.chunk_begin[j + 1];
   const bool in_item = lane < it.count;
-  const int64_t c = (int64_t)it.first + lane;
+  const int64_t c = in_item ? cand_of(P, it, item, lane) : 0;
   const int my_m = in_item ? P.bt.cand_model[c] : -1;
   const int my_g = in_item ? P.bt.cand_group[c] : 0;
   const bool active = in_item && P.bt.cand_ok[c];
@@ -551,6 +561,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
   __syncwarp();
 
   int64_t good0 = 0, sum0 = 0, good1 = 0, sum1 = 0;
+  uint32_t nreq = 0, nlive = 0;  // pass-1 lane statistics (profiling)
   unsigned long long upd = 0;
   uint32_t upd32 = 0;  // hosts evaluated (S > 0) / stage updates (S == 0) by this lane
   bool coalesced = false;
@@ -656,6 +667,10 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       }
       const bool live = active && ((kmask >> (cm & 63)) & 1ull);
       const bool mine = live && cm == my_m;
+      if constexpr (MODE == SPEC) {
+        ++nreq;
+        nlive += live ? 1u : 0u;
+      }
       int g0 = 0, g1 = 0;
       const int64_t l0 = step<T, S>(P, w, w.st0, lane, cm, chinfo, ch0, mine, my_g, live, car,
                                     dv, ctl, csl, upd32, g0);
@@ -687,6 +702,15 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
     upd += (unsigned long long)upd32 * (S > 0 ? S : 1);
     for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(FULL, upd, o);
     if (lane == 0) atomicAdd(P.stage_updates, upd);
+  }
+  if constexpr (MODE == SPEC) {
+    if (P.lane_stats) {
+      const unsigned live_w = __reduce_add_sync(FULL, nlive);
+      if (lane == 0) {
+        atomicAdd(P.lane_stats, 32ull * nreq);
+        atomicAdd(P.lane_stats + 1, (unsigned long long)live_w);
+      }
+    }
   }
   const int64_t cstride = (int64_t)P.num_items * 32;
   const int64_t Ec = P.tr.arrival[i_end - 1];  // the unit's canonical epoch
@@ -991,7 +1015,7 @@ __device__ __forceinline__ void coop_candidate(const ChunkParams& P, const WarpM
                                                uint32_t* end_src, unsigned long long& walked,
                                                unsigned long long& upd) {
   // Q = ceil(slots / 32) blocks of 32 slots; slot t = lane + 32 q
-  const int64_t c = (int64_t)it.first + cl;
+  const int64_t c = cand_of(P, it, item, cl);
   const int my_m = P.bt.cand_model[c], my_g = P.bt.cand_group[c];
   const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;
   const uint64_t gmask = P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull;
@@ -1112,7 +1136,7 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
                                                  uint32_t* end_src, unsigned long long& walked,
                                                  unsigned long long& upd) {
   constexpr int R = NG * S;
-  const int64_t c = (int64_t)it.first + cl;
+  const int64_t c = cand_of(P, it, item, cl);
   const int my_m = P.bt.cand_model[c], my_g = P.bt.cand_group[c];
   const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;
   const int ngroups = it.slots / S;
@@ -1462,7 +1486,7 @@ __device__ __forceinline__ bool scalar_dispatch(const ChunkParams& P, const Warp
                                                 const ItemDesc& it, int item, int cl, int lane,
                                                 uint32_t* end_src, unsigned long long& walked,
                                                 unsigned long long& upd) {
-  const int64_t c = (int64_t)it.first + cl;
+  const int64_t c = cand_of(P, it, item, cl);
   const int ngroups = it.slots / it.S;
   const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
   const uint64_t gmask = (P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all;
@@ -1519,8 +1543,8 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     if (u >= P.num_items * 32) break;
     const int item = u >> 5, cl = u & 31;
     const ItemDesc it = P.items[item];
-    if (it.S == 0 || cl >= it.count || !P.bt.cand_ok[(int64_t)it.first + cl]) continue;
-    const bool fits = P.scalar_walk && scalar_fits(P, it, (int64_t)it.first + cl);
+    if (it.S == 0 || cl >= it.count || !P.bt.cand_ok[cand_of(P, it, item, cl)]) continue;
+    const bool fits = P.scalar_walk && scalar_fits(P, it, cand_of(P, it, item, cl));
     if (fits != SCALAR) continue;  // the other walker's candidate
     // any chunk of this candidate flagged by pass 2?  (else nothing to walk)
     bool any = false;
@@ -1531,8 +1555,11 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
       load_base<T>(P, it, w, lane);
       cur_base = it.base;
     }
-    const unsigned long long w0 = walked, u0 = upd;
+    const unsigned long long w0 = walked;
+#ifdef ASIM_WALK_DIAGNOSTICS
+    const unsigned long long u0 = upd;
     const long long t0 = clock64();
+#endif
     if constexpr (SCALAR)
       scalar_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
     else
@@ -1540,14 +1567,16 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     if (P.walked && lane == 0 && walked > w0) {  // statistics: walking candidates, longest walk
       atomicAdd(P.walked + 1, 1ull);
       atomicMax(P.walked + 2, walked - w0);
+#ifdef ASIM_WALK_DIAGNOSTICS
       const long long cyc = clock64() - t0;
       if (P.walk_log > 0 && cyc > P.walk_log) {
-        const int64_t c = (int64_t)it.first + cl;
+        const int64_t c = cand_of(P, it, item, cl);
         printf("walk scalar=%d S=%d slots=%d ng=%d models=%d chunks=%llu cycles=%lld upd=%llu\n",
                (int)SCALAR, it.S, it.slots,
                __popcll(P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull),
                __popcll(P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull), walked - w0, cyc, upd - u0);
       }
+#endif
     }
   }
   if (lane == 0) {
@@ -1638,7 +1667,7 @@ __global__ void chunk_reduce_kernel(ChunkParams P, DevOut out) {
   const int item = (int)(t >> 5), lane = (int)(t & 31);
   const ItemDesc it = P.items[item];
   if (lane >= it.count) return;
-  const int64_t c = (int64_t)it.first + lane;
+  const int64_t c = cand_of(P, it, item, lane);
   const int64_t stride = (int64_t)P.num_items * 32;
   int64_t g = 0, s = 0;
   for (int j = 0; j < P.J; ++j) {
@@ -1672,7 +1701,7 @@ __global__ void publish_kernel(ChunkParams P, const uint32_t* __restrict__ end_s
   const ItemDesc it = P.items[pi.item];
   int64_t v = 0;  // j == 0: idle; slots beyond the item's: unused
   if (j > 0 && k < it.slots) {
-    const int64_t c = (int64_t)it.first + pi.lane;
+    const int64_t c = cand_of(P, it, pi.item, pi.lane);
     bool own = true;
     if (P.bt.cand_gmask) {  // group of slot k under the base's group table
       int g = 0, off = 0;
@@ -1724,13 +1753,8 @@ __global__ void mix_states_kernel(int64_t C0, int64_t C1, int32_t J, int32_t str
 template <typename K>
 cudaError_t grid_for(K kernel, size_t smem, int64_t units, int sms, int64_t* blocks) {
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  // always the maximum: concurrent contexts (threads) may launch the same
-  // kernel with different sizes, and a smaller attribute would fail theirs
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       227 * 1024);
-  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem);
+  cudaError_t e = blocks_per_sm(reinterpret_cast<const void*>(kernel), kWarps * 32, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t b = (int64_t)per_sm * sms;  // persistent: warps pull units from a counter
@@ -1888,12 +1912,10 @@ cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32,
   const unsigned blocks = (unsigned)((P.num_items + kWarps - 1) / kWarps);
   cudaError_t e;
   if (u32) {
-    e = cudaFuncSetAttribute(fast_stats_kernel<uint32_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    e = allow_max_smem(reinterpret_cast<const void*>(fast_stats_kernel<uint32_t>));
     if (e == cudaSuccess) fast_stats_kernel<uint32_t><<<blocks, kWarps * 32, smem, st>>>(P, out);
   } else {
-    e = cudaFuncSetAttribute(fast_stats_kernel<int64_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    e = allow_max_smem(reinterpret_cast<const void*>(fast_stats_kernel<int64_t>));
     if (e == cudaSuccess) fast_stats_kernel<int64_t><<<blocks, kWarps * 32, smem, st>>>(P, out);
   }
   if (e != cudaSuccess) return e;

@@ -13,6 +13,28 @@ namespace {
 
 constexpr int kSTab = 16;
 
+// Events around one phase of the chunked path on `st` (profiling only).
+struct PhaseTimer {
+  asim_ctx* ctx;
+  int ph;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  PhaseTimer(asim_ctx* c, int phase, cudaStream_t s, bool on) : ctx(c), ph(phase), st(s) {
+    if (!on || !c->profiling) return;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+      if (e0) cudaEventDestroy(e0);
+      e0 = e1 = nullptr;
+      return;
+    }
+    cudaEventRecord(e0, st);
+  }
+  ~PhaseTimer() {
+    if (!e0) return;
+    cudaEventRecord(e1, st);
+    ctx->phase_events[ph].emplace_back(e0, e1);
+  }
+};
+
 int stage_class(int s) { return (s == 1 || s == 2 || s == 4 || s == 8 || s == 16) ? s : 0; }
 
 }  // namespace
@@ -161,13 +183,26 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     base_slots[b] = slots;
   }
   int32_t slots_max = 1;
-  for (int64_t c = begin; c < end;) {
-    const int32_t b = hb.cand_base[c];
+  // Candidate order inside the range: the batch's, or grouped by hosting
+  // component (hb.cand_key, the search's): a warp replays the union of its
+  // lanes' requests, so lanes sharing their components keep every lane busy.
+  std::vector<int32_t> ord;
+  ord.reserve(end - begin);
+  for (int64_t c = begin; c < end; ++c) ord.push_back((int32_t)c);
+  const bool grouped = !hb.cand_key.empty();
+  if (grouped)
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+      if (hb.cand_base[a] != hb.cand_base[b]) return hb.cand_base[a] < hb.cand_base[b];
+      return hb.cand_key[a] < hb.cand_key[b];
+    });
+  std::vector<int32_t> item_cand;
+  for (size_t pos = 0; pos < ord.size();) {
+    const int32_t b = hb.cand_base[ord[pos]];
     int32_t cnt = 1;
-    while (c + cnt < end && cnt < 32 && hb.cand_base[c + cnt] == b) ++cnt;
+    while (pos + cnt < ord.size() && cnt < 32 && hb.cand_base[ord[pos + cnt]] == b) ++cnt;
     asim::ItemDesc it{};
     it.base = b;
-    it.first = (int32_t)c;
+    it.first = ord[pos];
     it.count = cnt;
     it.cfg = base_cfg_uniform[b];
     it.stages = it.cfg >= 0 ? hp.cfg_stages[it.cfg] : 0;
@@ -176,7 +211,9 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     it.slots = base_slots[b];
     slots_max = std::max(slots_max, it.slots);
     items.push_back(it);
-    c += cnt;
+    if (grouped)
+      for (int32_t l = 0; l < 32; ++l) item_cand.push_back(l < cnt ? ord[pos + l] : -1);
+    pos += cnt;
   }
   const int32_t I = (int32_t)items.size();
   if (I == 0) return ASIM_OK;
@@ -196,6 +233,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   // ---- device buffers (grow-only)
   const int64_t per_chunk = (int64_t)I * 32;
   cudaError_t e = upload(ctx->c_items, items, st);
+  if (e == cudaSuccess && grouped) e = upload(ctx->c_item_cand, item_cand, st);
   if (e == cudaSuccess) e = upload(ctx->c_begin, cb, st);
   if (e == cudaSuccess) e = ctx->c_spec_good.ensure(J * per_chunk * 4);
   if (e == cudaSuccess) e = ctx->c_spec_sum.ensure(J * per_chunk * 8);
@@ -223,6 +261,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.bt.cand_gmask = hb.cand_gmask.empty() ? nullptr : ctx->d_cand_gmask.as<uint64_t>();
   P.bt.C = (int64_t)hb.cand_base.size();
   P.items = ctx->c_items.as<asim::ItemDesc>();
+  P.item_cand = grouped ? ctx->c_item_cand.as<int32_t>() : nullptr;
   P.num_items = I;
   P.J = (int32_t)J;
   P.chunk_begin = ctx->c_begin.as<int64_t>();
@@ -297,19 +336,13 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     // profiling: pass 1 alone (the dominant kernel) gets its own events and
     // work counter (d_counter[1]; the total is d_counter[0] + d_counter[1])
     asim::ChunkParams P1 = P;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (ctx->profiling && P.stage_updates) {
       P1.stage_updates = ctx->d_counter.as<unsigned long long>() + 1;
-      if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
-        return asim_cuda(ctx, cudaGetLastError(), "event create");
-      cudaEventRecord(ev0, st);
+      P1.lane_stats = ctx->d_counter.as<unsigned long long>() + 2;
     }
+    PhaseTimer t(ctx, 0, st, P.stage_updates != nullptr);
     e = asim::launch_chunk_pass(P1, false, u32, st, ctx->sms, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
-    if (ev0) {
-      cudaEventRecord(ev1, st);
-      ctx->spec_events.emplace_back(ev0, ev1);
-    }
   }
 
   e = ctx->c_end_src.ensure(J * I * 4 + 8);
@@ -320,12 +353,18 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   if (J > 1) {
     // ---- pass 2: fix-up of every chunk j >= 1 from chunk j-1's speculative end
     P.num_units = (int32_t)((J - 1) * I);
-    e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
+    {
+      PhaseTimer t(ctx, 1, st, P.stage_updates != nullptr);
+      e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
+    }
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 2");
     // ---- pass 3: walk the chunks whose start state was wrong (exact chains)
     const asim::WalkStreams ws{st, {ctx->side[0], ctx->side[1]}, ctx->ev_fork,
                                {ctx->ev_join[0], ctx->ev_join[1]}};
-    e = asim::launch_chunk_walk(P, end_src, u32, any_dynamic, ws, ctx->sms, &ctx->launches);
+    {
+      PhaseTimer t(ctx, 2, st, P.stage_updates != nullptr);
+      e = asim::launch_chunk_walk(P, end_src, u32, any_dynamic, ws, ctx->sms, &ctx->launches);
+    }
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk walk");
   } else {
     e = cudaMemsetAsync(end_src, 0, J * I * 4, st);
@@ -341,6 +380,10 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   ctx->last_u32 = u32;
   ctx->last_params = P;
   ctx->last_items = std::move(items);
+  ctx->last_pos.assign(P.bt.C, -1);  // candidate -> item * 32 + lane of this run
+  for (size_t i = 0, pos = 0; i < ctx->last_items.size(); ++i)
+    for (int32_t l = 0; l < ctx->last_items[i].count; ++l, ++pos)
+      ctx->last_pos[ord[pos]] = (int32_t)(i * 32 + l);
   return ASIM_OK;
 }
 
@@ -351,19 +394,12 @@ asim_status asim_publish_candidates(asim_ctx* ctx, const std::vector<int64_t>& c
   if (!ctx->last_valid)
     return asim_fail(ctx, ASIM_ESTATE, "internal: no chunked run to publish from");
   std::vector<asim::PublishItem> pub;
-  const auto& items = ctx->last_items;
   for (size_t i = 0; i < cands.size(); ++i) {
     const int64_t c = cands[i];
-    // items are in candidate order: find the one holding c
-    size_t lo = 0, hi = items.size();
-    while (hi - lo > 1) {
-      const size_t mid = (lo + hi) / 2;
-      if (items[mid].first <= c) lo = mid;
-      else hi = mid;
-    }
-    if (items.empty() || c < items[lo].first || c >= items[lo].first + items[lo].count)
+    const int32_t pos = (c >= 0 && c < (int64_t)ctx->last_pos.size()) ? ctx->last_pos[c] : -1;
+    if (pos < 0)
       return asim_fail(ctx, ASIM_ESTATE, "internal: candidate not in the last chunked run");
-    pub.push_back(asim::PublishItem{(int32_t)lo, (int32_t)(c - items[lo].first), rows[i]});
+    pub.push_back(asim::PublishItem{pos >> 5, pos & 31, rows[i]});
   }
   cudaError_t e = upload(ctx->c_pub, pub, st);
   if (e == cudaSuccess)

@@ -155,8 +155,10 @@ asim_status asim_upload_batch(asim_ctx* ctx, const HostBatch& hb, cudaStream_t s
 }
 
 asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
-                           const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
+                           const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt,
+                           bool* took_chunked) {
   const int64_t C = (int64_t)hb.cand_base.size();
+  if (took_chunked) *took_chunked = false;
   if (end <= begin) return ASIM_OK;
   if (begin < 0 || end > C) return asim_fail(ctx, ASIM_ERANGE, "candidate range");
   asim_status us = asim_upload_batch(ctx, hb, st);
@@ -169,7 +171,10 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
   bool chunked = ctx->force_path >= 2 ||
                  (ctx->force_path == 0 && shared_bases && asim_chunked_eligible(ctx, hb, out));
   if (ctx->force_path >= 2 && !asim_chunked_eligible(ctx, hb, out)) chunked = false;
-  if (!hb.cand_kmask.empty()) {  // component-restricted batches only exist on the chunked path
+  // Component-restricted batches only exist on the chunked path, and a caller
+  // passing ChunkOptions (the search) relies on the chunked run's boundary
+  // states afterwards (candidate memory, publishing), so both force it.
+  if (!hb.cand_kmask.empty() || (opt && ctx->force_path != 1)) {
     if (!asim_chunked_eligible(ctx, hb, out))
       return asim_fail(ctx, ASIM_ESTATE, "internal: restricted batch not chunk-eligible");
     chunked = true;
@@ -184,6 +189,7 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
     asim::DevOut o2 = out;
     o2.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
     asim_status s = asim_run_chunked(ctx, hb, begin, end, o2, st, opt);
+    if (took_chunked) *took_chunked = s == ASIM_OK;
     if (ctx->profiling) {
       cudaEventRecord(ev1, st);
       ctx->events.emplace_back(ev0, ev1);
@@ -271,6 +277,7 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   ctx->sms = prop.multiProcessorCount;
   if (const char* sw = getenv("ASIM_SCALAR_WALK")) ctx->scalar_walk = sw[0] != '0';
   if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
+  if (const char* gc = getenv("ASIM_GROUP_CANDIDATES")) ctx->group_cands = gc[0] != '0';
   {
     DeviceGuard dg(cuda_device);
     e = cudaSuccess;
@@ -302,7 +309,7 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
                     &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src, &ctx->d_cand_kmask,
-                    &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_perm, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
+                    &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_perm, &ctx->c_item_cand, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
                     &ctx->c_fbusy};
     for (DBuf* b : bufs) b->release();
     for (DBuf& b : ctx->spool) b.release();
@@ -324,7 +331,8 @@ int64_t asim_launch_count(const asim_ctx* ctx) { return ctx ? ctx->launches : 0;
 asim_status asim_reset_stats(asim_ctx* ctx) {
   if (!ctx) return ASIM_EINVAL;
   DeviceGuard dg(ctx->device);
-  for (auto* evs : {&ctx->events, &ctx->spec_events}) {
+  for (auto* evs : {&ctx->events, &ctx->phase_events[0], &ctx->phase_events[1],
+                    &ctx->phase_events[2]}) {
     for (auto& ev : *evs) {
       cudaEventSynchronize(ev.second);
       cudaEventDestroy(ev.first);
@@ -334,10 +342,10 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   }
   ctx->sim_launches = 0;
   ctx->sim_ms = 0.0;
-  ctx->spec_ms = 0.0;
+  for (double& x : ctx->phase_ms) x = 0.0;
   ctx->request_evals = 0;
   if (ctx->d_counter.p) {
-    cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 16);
+    cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 32);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return asim_cuda(ctx, e, "reset stats");
@@ -363,9 +371,9 @@ asim_status asim_set_profiling(asim_ctx* ctx, int32_t on) {
   if (!ctx) return ASIM_EINVAL;
   DeviceGuard dg(ctx->device);
   if (on && !ctx->d_counter.p) {
-    cudaError_t e = ctx->d_counter.ensure(16);
+    cudaError_t e = ctx->d_counter.ensure(32);
     if (e == cudaSuccess) e = ctx->d_walked.ensure(32);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 16);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 32);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "profiling counter");
   }
@@ -386,19 +394,21 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
     cudaEventDestroy(ev.second);
   }
   ctx->events.clear();
-  for (auto& ev : ctx->spec_events) {
-    cudaError_t e = cudaEventSynchronize(ev.second);
-    float ms = 0.f;
-    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev.first, ev.second);
-    if (e != cudaSuccess) return asim_cuda(ctx, e, "stats events");
-    ctx->spec_ms += ms;
-    cudaEventDestroy(ev.first);
-    cudaEventDestroy(ev.second);
+  for (int ph = 0; ph < 3; ++ph) {
+    for (auto& ev : ctx->phase_events[ph]) {
+      cudaError_t e = cudaEventSynchronize(ev.second);
+      float ms = 0.f;
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev.first, ev.second);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "stats events");
+      ctx->phase_ms[ph] += ms;
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+    ctx->phase_events[ph].clear();
   }
-  ctx->spec_events.clear();
-  unsigned long long upd2[2] = {0, 0}, walked[4] = {0, 0, 0, 0};
+  unsigned long long upd2[4] = {0, 0, 0, 0}, walked[4] = {0, 0, 0, 0};
   if (ctx->d_counter.p) {
-    cudaError_t e = cudaMemcpy(upd2, ctx->d_counter.p, 16, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(upd2, ctx->d_counter.p, 32, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(walked, ctx->d_walked.p, 32, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "stats counter");
   }
@@ -407,7 +417,11 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->sim_ms = ctx->sim_ms;
   out->stage_updates = (int64_t)(upd2[0] + upd2[1]);
   out->spec_stage_updates = (int64_t)upd2[1];
-  out->spec_ms = ctx->spec_ms;
+  out->spec_ms = ctx->phase_ms[0];
+  out->pass2_ms = ctx->phase_ms[1];
+  out->walk_ms = ctx->phase_ms[2];
+  out->spec_lane_slots = (int64_t)upd2[2];
+  out->spec_live_lanes = (int64_t)upd2[3];
   out->request_evals = ctx->request_evals;
   out->chunk_reruns = (int64_t)walked[0];
   out->walk_candidates = (int64_t)walked[1];
@@ -419,6 +433,31 @@ double asim_attainment(int64_t good, int64_t n) {
   if (good < 0) return -1.0;
   if (n == 0) return 1.0;
   return (double)good / (double)n;
+}
+
+asim_status asim_argmax(asim_ctx* ctx, const int64_t* good, int64_t n, int32_t ptr_kind,
+                        int64_t* out, void* cuda_stream) {
+  if (!ctx) return ASIM_EINVAL;
+  if (ctx->broken) return asim_fail(ctx, ASIM_ECUDA, "context unusable after a CUDA error");
+  if (!out || (n > 0 && !good)) return asim_fail(ctx, ASIM_EINVAL, "null good / out");
+  if (n < 0) return asim_fail(ctx, ASIM_ERANGE, "n < 0");
+  if (ptr_kind != ASIM_HOST && ptr_kind != ASIM_DEVICE)
+    return asim_fail(ctx, ASIM_EINVAL, "bad ptr_kind");
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  const int64_t* g = good;
+  cudaError_t e = ctx->d_argmax.ensure(8);
+  if (e == cudaSuccess && ptr_kind == ASIM_HOST && n > 0) {
+    e = ctx->d_good.ensure((size_t)n * 8);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ctx->d_good.p, good, (size_t)n * 8, cudaMemcpyHostToDevice, st);
+    g = ctx->d_good.as<int64_t>();
+  }
+  if (e == cudaSuccess) e = asim::launch_argmax(g, n, ctx->d_argmax.as<int64_t>(), st, &ctx->launches);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, ctx->d_argmax.p, 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return asim_cuda(ctx, e, "argmax");
 }
 
 asim_status asim_set_problem(asim_ctx* ctx, const asim_problem* p) {

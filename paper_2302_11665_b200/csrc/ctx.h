@@ -71,12 +71,14 @@ struct asim_ctx {
   // statistics (asim_set_profiling)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spec_events;  // pass 1 launches only
-  double spec_ms = 0.0;
+  // chunked-path phases timed by their own events: 0 = pass 1, 1 = pass 2, 2 = walk
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_events[3];
+  double phase_ms[3] = {0.0, 0.0, 0.0};
   int64_t sim_launches = 0;
   double sim_ms = 0.0;
   int64_t request_evals = 0;
-  DBuf d_counter;  // unsigned long long stage-update counters [2]: other kernels, pass 1
+  DBuf d_counter;  // unsigned long long counters [4]: stage updates of other kernels, of
+                   // pass 1; pass-1 lane slots (requests x 32), pass-1 live lane-requests
   DBuf d_walked;   // unsigned long long walked-chunk counter
 
   int sms = 148;
@@ -93,10 +95,12 @@ struct asim_ctx {
   bool last_u32 = false;
   asim::ChunkParams last_params{};
   std::vector<asim::ItemDesc> last_items;
-  DBuf c_pub, c_perm;
+  std::vector<int32_t> last_pos;  // batch candidate -> item * 32 + lane (-1: not in the run)
+  DBuf c_pub, c_perm, c_item_cand;
   DBuf c_spm, c_fpm, c_sbusy, c_fbusy;  // fast-heuristic statistics rows
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
+  bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
 
   // scratch for evaluate()
@@ -146,6 +150,7 @@ struct HostBatch {
   std::vector<int32_t> cand_base, cand_model, cand_group;
   std::vector<uint8_t> cand_ok;
   std::vector<uint64_t> cand_kmask, cand_gmask;  // optional component restriction
+  std::vector<int64_t> cand_key;  // optional: chunked items group candidates by this key
   int32_t slots = 1;               // max over bases of sum of stages
 };
 // Upload a batch and launch the simulation of candidates [0, C) writing
@@ -155,7 +160,7 @@ struct ChunkOptions;
 asim_status asim_upload_batch(asim_ctx* ctx, const HostBatch& hb, cudaStream_t st);
 asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                            const asim::DevOut& out, cudaStream_t st,
-                           const ChunkOptions* opt = nullptr);
+                           const ChunkOptions* opt = nullptr, bool* took_chunked = nullptr);
 
 // Options of the chunked path used by the search (all optional).
 struct ChunkOptions {

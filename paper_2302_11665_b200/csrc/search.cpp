@@ -50,6 +50,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <functional>
 #include <map>
 #include <set>
@@ -97,6 +98,7 @@ struct Run {
   // per-root model / group masks of the base (component restriction)
   std::vector<uint64_t> rootK, rootG;
   std::vector<std::pair<int32_t, int32_t>> history;     // winners in order
+  std::vector<int64_t> history_good;                    // good of the selection after each
   // batch index of (m, g) among the candidates simulated locally in the
   // previous / current step (-1: not simulated here)
   std::vector<int32_t> prev_idx, cur_idx;
@@ -176,6 +178,7 @@ struct asim_search {
   bool prepared = false;
   HostBatch hb;
   std::vector<int32_t> base_run;  // base -> run id
+  std::vector<int64_t> cost;      // per candidate of the step: estimated simulation work
   int64_t eval_lo = 0, eval_hi = 0;  // candidates of the last local evaluate call
   DBuf d_good_all;
   std::vector<int64_t> h_good;
@@ -617,6 +620,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   hb = HostBatch();
   hb.G = G;
   s->base_run.clear();
+  s->cost.clear();
   s->eval_lo = s->eval_hi = 0;
   s->rows_uploaded = false;
   s->mixrows.clear();
@@ -640,6 +644,18 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
         hb.cand_kmask.push_back(km);
         hb.cand_gmask.push_back(gm);
       }
+      if (s->restrict_k && s->ctx->group_cands) {
+        // chunked items: the candidate's larger component first, so a warp's
+        // lanes share the bulk of the requests they replay (ties: (m, g) order)
+        const int64_t n1 = run.cn[c.r1], n2 = run.cn[c.r2];
+        const int32_t dom = n2 >= n1 ? c.r2 : c.r1, oth = n2 >= n1 ? c.r1 : c.r2;
+        hb.cand_key.push_back(((int64_t)dom << 32) | (uint32_t)oth);
+      }
+      // work estimate (sharding): requests the lane replays x stages per group
+      const int64_t nreq = s->restrict_k
+                               ? run.cn[c.r1] + (c.r2 != c.r1 ? run.cn[c.r2] : 0)
+                               : s->ctx->n;
+      s->cost.push_back(std::max<int64_t>(1, nreq) * hp.cfg_stages[run.cfg[c.g]]);
       s->mixrows.push_back(asim::MixRow{r, prev});
     };
     if (run.round == 1) {  // the same step, second round: deferred candidates
@@ -741,6 +757,14 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   return ASIM_OK;
 }
 
+asim_status asim_search_costs(const asim_search* s, int64_t cap, int64_t* cost) {
+  if (!s || cap < 0 || (cap > 0 && !cost)) return ASIM_EINVAL;
+  if (!s->prepared) return asim_fail(s->ctx, ASIM_ESTATE, "costs before prepare");
+  const int64_t C = (int64_t)s->cost.size();
+  for (int64_t i = 0; i < C && i < cap; ++i) cost[i] = s->cost[i];
+  return ASIM_OK;
+}
+
 asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int64_t* good_dev,
                                  void* cuda_stream) {
   if (!s) return ASIM_EINVAL;
@@ -790,8 +814,9 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
   asim::DevOut out{};
   out.good = good_dev;
   out.out_offset = begin;
-  st = asim_run_batch(s->ctx, s->hb, begin, end, out, strm, popt);
-  if (!st) {
+  bool chunked = false;
+  st = asim_run_batch(s->ctx, s->hb, begin, end, out, strm, popt, &chunked);
+  if (!st && chunked) {
     s->eval_lo = begin;  // the chunk buffers now hold these candidates' trajectories
     s->eval_hi = end;
   }
@@ -903,6 +928,7 @@ static void apply_winner(Run& run, const Run::Cand w, const HostProblem& hp) {
   run.used[w.g] += hp.mem_at(w.m, run.cfg[w.g]);
   run.base_good = w.good;
   run.history.emplace_back(w.m, w.g);
+  run.history_good.push_back(w.good);
   ++run.steps;
 }
 
@@ -1246,6 +1272,7 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
       int64_t g_total = 0;
       for (int32_t m = 0; m < M; ++m) g_total += run.fpm[m];
       run.base_good = g_total;
+      if (!run.history_good.empty() && run.history_good.back() < 0) run.history_good.back() = g_total;
       if (g_total > run.best_good) {  // best selection so far, strict '>' (C24)
         run.best_good = g_total;
         run.best = run.sel;
@@ -1280,6 +1307,7 @@ static asim_status run_fast(asim_search* s, cudaStream_t st) {
       run.sel[bm] |= 1ULL << bgp;
       run.used[bgp] += hp.mem_at(bm, run.cfg[bgp]);
       run.history.emplace_back(bm, bgp);
+      run.history_good.push_back(-1);  // known after the next simulation
       ++run.steps;
       const int32_t a = run.find(bgp), c = run.find(run.G + bm);
       if (a != c) run.parent[a] = c;  // unite comp(g*) and comp(m*)
@@ -1533,6 +1561,39 @@ asim_status asim_search_buckets_get(const asim_search* s, asim_bucket_result* ou
       for (int32_t m : s->jobs[j].models) out->bucket_of_model[m] = i;
     if (out->bucket_devices) out->bucket_devices[i] = s->combos[bc].H[i];
     if (out->bucket_run) out->bucket_run[i] = job_run[j];
+  }
+  return ASIM_OK;
+}
+
+asim_status asim_search_run_history(const asim_search* s, int32_t run, int64_t cap,
+                                    int32_t* model, int32_t* group, int64_t* good,
+                                    int64_t* count) {
+  if (!s || !count || run < 0 || run >= s->ngroups || cap < 0) return ASIM_EINVAL;
+  const Run& r = group_run(s, run);
+  const int64_t n = (int64_t)r.history.size();
+  *count = n;
+  for (int64_t i = 0; i < n && i < cap; ++i) {
+    if (model) model[i] = r.history[i].first;
+    if (group) group[i] = r.history[i].second;
+    if (good) good[i] = r.history_good[i];
+  }
+  return ASIM_OK;
+}
+
+asim_status asim_search_run_candidates(const asim_search* s, int32_t run, int64_t cap,
+                                       int32_t* model, int32_t* group, int64_t* good,
+                                       int64_t* count) {
+  if (!s || !count || run < 0 || run >= s->ngroups || cap < 0) return ASIM_EINVAL;
+  if (s->prepared) return asim_fail(s->ctx, ASIM_ESTATE, "candidates are read between steps");
+  const Run& r = group_run(s, run);
+  const int64_t n = (int64_t)r.cands.size();
+  *count = n;
+  for (int64_t i = 0; i < n && i < cap; ++i) {
+    const Run::Cand& c = r.cands[i];
+    if (model) model[i] = c.m;
+    if (group) group[i] = c.g;
+    // bounded out (spec->cand_bound): no value, provably not the argmax
+    if (good) good[i] = c.kind == 4 ? INT64_MIN : c.good;
   }
   return ASIM_OK;
 }

@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include "asim_internal.h"
+#include "launch_cache.h"
 
 namespace asim {
 namespace {
@@ -174,8 +175,7 @@ cudaError_t launch_simulate(const DevProblem& pr, const DevTrace& tr, const DevB
   if (num_items <= 0) return cudaSuccess;
   if (slots < 1) slots = 1;
   const size_t smem = (size_t)kWarpsPerBlock * ((size_t)slots * 32 * 8 + (size_t)b.G * 32 * 4);
-  cudaError_t ea = cudaFuncSetAttribute(simulate_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaError_t ea = allow_max_smem(reinterpret_cast<const void*>(simulate_kernel));
   if (ea != cudaSuccess) return ea;
   const int blocks = (num_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   simulate_kernel<<<blocks, kWarpsPerBlock * 32, smem, stream>>>(pr, tr, b, items, num_items,

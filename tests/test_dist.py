@@ -113,6 +113,46 @@ def test_shard_covers_exactly():
             assert max(e - b for b, e in parts) <= -(-C // W) if C else True
 
 
+def test_shard_bounds_balance_cost():
+    from paper_2302_11665_b200.dist import shard_bounds
+    rng = np.random.default_rng(0)
+    for C in (0, 1, 2, 7, 100, 1000):
+        for W in (1, 2, 3, 8):
+            cost = rng.integers(1, 1000, size=C)
+            if C > 3:
+                cost[C // 3] = 10**6  # one heavy candidate
+            b = shard_bounds(cost, W)
+            assert len(b) == W + 1 and b[0] == 0 and b[-1] == C
+            assert all(x <= y for x, y in zip(b, b[1:]))
+            if C == 0:
+                continue
+            total = int(cost.sum())
+            pref = np.concatenate([[0], np.cumsum(cost)])
+            for r in range(W):
+                # shard r holds the candidates whose cost prefix ends in
+                # (r T / W, (r+1) T / W] (the last shard: up to T)
+                for i in range(b[r], b[r + 1]):
+                    assert pref[i + 1] * W > r * total
+                    if r < W - 1:
+                        assert pref[i] * W < (r + 1) * total or i == b[r]
+            # equal costs: the count split differs by at most one per shard
+            eq = shard_bounds(np.ones(C, np.int64), W)
+            sizes = np.diff(eq)
+            assert sizes.max() - sizes.min() <= 1
+
+
+def test_concat_shards_orders_globally():
+    from paper_2302_11665_b200.dist import concat_shards, shard_bounds
+    for C, W in ((10, 3), (5, 8), (1, 2), (64, 4)):
+        bounds = shard_bounds(np.arange(1, C + 1), W)
+        pad = max(1, max(np.diff(bounds)))
+        buf = torch.full((W * pad,), -7, dtype=torch.int64)
+        for r in range(W):
+            n = bounds[r + 1] - bounds[r]
+            buf[r * pad:r * pad + n] = torch.arange(bounds[r], bounds[r + 1])
+        assert concat_shards(buf, pad, bounds).tolist() == list(range(C))
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_search_matches_single_process(world):
     prob, tr = _problem()
@@ -164,7 +204,11 @@ def _batching_worker(rank, world, port, q):
         g, _, _ = oracle.evaluate_batching(prob, tr, cfg[b:e], mask[b:e], inc, 3, threads=2)
         return torch.from_numpy(g)
 
-    good, arg = adist.evaluate_sharded(run, len(cfg), device=torch.device("cpu"))
+    def first_max(good):  # test-side argmax (the GPU path uses the library kernel)
+        g = good.numpy()
+        return int(np.argmax(g)) if g.size and g.max() >= 0 else -1
+
+    good, arg = adist.evaluate_sharded(run, first_max, len(cfg), device=torch.device("cpu"))
     q.put((rank, good.tolist(), arg))
     dist.destroy_process_group()
 

@@ -123,3 +123,76 @@ def test_bounding_skips_candidates_exactly(sim):
     for ra, rb in zip(a.runs, b.runs):
         assert ra["best_good"] == rb["best_good"]
         np.testing.assert_array_equal(ra["host_mask"], rb["host_mask"])
+
+
+# ------------------------------------------------------------------ per step
+from tests.search_driver import stepwise  # noqa: E402
+
+
+def _compare_steps(gpu_steps, ref_runs, prune):
+    for r, (gs, rr) in enumerate(zip(gpu_steps, ref_runs)):
+        ref_steps = rr["steps"]
+        if prune:
+            assert len(gs) <= len(ref_steps)
+        else:
+            assert len(gs) == len(ref_steps), f"run {r}"
+        for i, ((m, g, v, chosen), (cands, goods, ci)) in enumerate(zip(gs, ref_steps)):
+            np.testing.assert_array_equal(m, [c[0] for c in cands], err_msg=f"run {r} step {i}")
+            np.testing.assert_array_equal(g, [c[1] for c in cands], err_msg=f"run {r} step {i}")
+            np.testing.assert_array_equal(v, goods, err_msg=f"run {r} step {i} goods")
+            assert chosen == (cands[ci][0], cands[ci][1], int(goods[ci])), (r, i)
+
+
+@pytest.mark.parametrize("dedup,prune", [(False, False), (True, True)])
+def test_search_every_step_s3_shaped(sim, dedup, prune):
+    """Every greedy step of every Alg. 2 run: the same candidate list
+    (m-major, g-minor, memory-feasible), the same good for every
+    candidate -- simulated, from the component memo or a duplicate's
+    representative -- and the same pick (lowest index on ties)."""
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "BERT-6.7B", "MoE-1.3B",
+                                  "MoE-2.4B", "MoE-5.3B") for i in range(2)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=5.0)
+    tr = traces.maf2_shaped(4, len(names), 20.0, 300.0)
+    ref = osearch.alg2(prob, tr, record=True)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    gs, res = stepwise(sim, dedup=dedup, prune=prune)
+    _compare_steps(gs, ref["runs"], prune)
+    assert res.best_good == ref["good"] and res.best_run == ref["run"]
+
+
+@pytest.mark.parametrize("chunk", [37, 300])
+def test_search_every_step_small_chunks(sim, chunk):
+    """As above with many time chunks per step (speculation from the base's
+    boundary states, candidate memory mixes, walks): per-step exact."""
+    names = [f"{b}#{i}" for b in ("BERT-1.3B", "BERT-2.7B", "MoE-5.3B") for i in range(2)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=3.0)
+    tr = traces.maf2_shaped(11, len(names), 12.0, 900.0)
+    ref = osearch.alg2(prob, tr, record=True)
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    sim.set_chunk_size(chunk)
+    try:
+        gs, _ = stepwise(sim, dedup=False, prune=False)
+    finally:
+        sim.set_chunk_size(4096)
+    _compare_steps(gs, ref["runs"], False)
+
+
+def test_search_more_than_64_models(sim):
+    """M > 64: no component restriction (model masks are 64-bit), and late
+    steps simulate fewer candidates than there are active runs -- the search
+    must still take the chunked path whose boundary states it publishes
+    (a general-kernel step left stale chunk buffers)."""
+    names = [f"BERT-1.3B#{i}" for i in range(70)]
+    prob = configs.build_problem(names, 8, 13 * 10**9, slo_scale=5.0)
+    w = np.linspace(1.0, 0.2, 70)
+    tr = traces.independent_gamma(5, list(0.05 * w), 2.0, 400.0)
+    for chunk in (4096, 23):
+        sim.set_problem(prob)
+        sim.set_trace(tr.arrival_ns, tr.model)
+        sim.set_chunk_size(chunk)
+        try:
+            _compare(sim, prob, tr, dedup_modes=(False,))
+        finally:
+            sim.set_chunk_size(4096)

@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="asim", choices=["asim", "reference"])
     ap.add_argument("--config", default="S3", choices=["S1", "S2", "S3", "S4", "motivating"])
-    ap.add_argument("--hours", type=float, default=1.0, help="trace length (S1-S4)")
+    ap.add_argument("--hours", type=float, default=24.0,
+                    help="trace length (S1-S4); the north-star target is the day-long S3 trace")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dedup", action="store_true",
                     help="exact de-duplication of identical candidates (fewer simulations)")
@@ -55,6 +56,8 @@ def parse():
                     help="exact candidate bounding (include/asim.h; off by default: on S3 the "
                          "component bound rarely excludes a candidate the memo would not)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--e2e-steps", type=int, default=3,
+                    help="searches timed end to end (bounded: a day-long search takes seconds)")
     return ap.parse_args()
 
 
@@ -124,67 +127,59 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def cpu_sample(prob, tr, seconds: float, seed: int = 0):
-    """Time the CPU oracle (as it stands) on a bounded sample of the same
-    workload: mid-search placements of every Alg. 2 run (each group filled
-    to ~half its memory with seeded random models) plus all their feasible
-    additions, on a prefix of the trace sized to ~`seconds` of work."""
-    import oracle
+def step0_batch(prob):
+    """The first greedy step of every Alg. 2 run (reading C13): every
+    memory-feasible addition (m, g) to the empty placement, m-major, g-minor
+     -- exactly the candidates the GPU evaluates at step 0."""
     from oracle import search as osearch
-    from workloads import Placement
 
-    rng = np.random.default_rng(seed)
     M = prob.num_models
-    cands_cfg, cands_mask = [], []
+    cfgs, masks = [], []
     for size, p, cfg in osearch.alg2_runs(prob):
-        G = len(cfg)
-        used = np.zeros(G, np.int64)
-        mask = np.zeros(M, np.uint64)
-        for g in range(G):
-            for m in rng.permutation(M):
-                mb = int(prob.mem_bytes[m, p])
-                if mb >= 0 and used[g] + mb <= prob.budget_bytes // 2:
-                    mask[m] |= np.uint64(1) << np.uint64(g)
-                    used[g] += mb
+        mb = [int(prob.mem_bytes[m, p]) for m in range(M)]
         for m in range(M):
-            for g in range(G):
-                mb = int(prob.mem_bytes[m, p])
-                if (int(mask[m]) >> g) & 1 or mb < 0 or used[g] + mb > prob.budget_bytes:
-                    continue
-                mm = mask.copy()
-                mm[m] |= np.uint64(1) << np.uint64(g)
+            if mb[m] < 0 or mb[m] > prob.budget_bytes:
+                continue
+            for g in range(len(cfg)):
                 c = np.full(64, -1, np.int32)
-                c[:G] = cfg
-                cands_cfg.append(c)
-                cands_mask.append(mm)
-    order = rng.permutation(len(cands_cfg))
-    cfg = np.stack(cands_cfg)[order]
-    mask = np.stack(cands_mask)[order]
+                c[:len(cfg)] = cfg
+                mask = np.zeros(M, np.uint64)
+                mask[m] = np.uint64(1) << np.uint64(g)
+                cfgs.append(c)
+                masks.append(mask)
+    return np.stack(cfgs), np.stack(masks)
+
+
+def cpu_sample(prob, tr, seconds: float, seed: int = 0):
+    """Time the CPU oracle (as it stands; built -O3 -march=native for this
+    host) on a bounded sample of the GPU's own work: a seeded
+    subset of the S3 step-0 batch (every run's additions to the empty
+    placement) on the trace's 10-min prefix, sized to ~`seconds` of work."""
+    import oracle
+
+    oracle.use_timing_build()
+    cfg, mask = step0_batch(prob)
+    order = np.random.default_rng(seed).permutation(len(cfg))
+    cfg, mask = cfg[order], mask[order]
+    sub = tr.prefix(int(np.searchsorted(tr.arrival_ns, tr.arrival_ns[0] + 600 * 10**9)))
     threads = oracle.hardware_threads()
-    # calibrate: grow (candidates, requests) until ~seconds of CPU work
-    n_req, n_c = min(len(tr), 20000), min(len(cfg), 4 * threads)
-    op, _ = oracle.OracleProblem(prob), None
-    while True:
-        sub = tr.prefix(n_req)
+    op, ot = oracle.OracleProblem(prob), oracle.OracleTrace(sub)
+    n_c = min(len(cfg), 4 * threads)
+    while True:  # calibrate the candidate count to ~seconds of work
         t0 = time.perf_counter()
-        oracle.evaluate(op, sub, cfg[:n_c], mask[:n_c], threads)
+        oracle.evaluate(op, ot, cfg[:n_c], mask[:n_c], threads)
         dt = time.perf_counter() - t0
-        if dt >= 0.25 * seconds or (n_c >= len(cfg) and n_req >= len(tr)):
+        if dt >= 0.2 * seconds or n_c >= len(cfg):
             break
-        grow = min(4.0, 0.5 * seconds / max(dt, 1e-3))
-        if n_c < len(cfg):
-            n_c = min(len(cfg), int(n_c * grow) + 1)
-        else:
-            n_req = min(len(tr), int(n_req * grow) + 1)
-    scale = max(1.0, seconds / max(dt, 1e-3))
-    n_c = min(len(cfg), int(n_c * scale))
-    sub = tr.prefix(n_req)
+        n_c = min(len(cfg), int(n_c * min(8.0, 0.5 * seconds / max(dt, 1e-3))) + 1)
+    n_c = min(len(cfg), max(n_c, int(n_c * seconds / max(dt, 1e-3))))
     t0 = time.perf_counter()
-    oracle.evaluate(op, sub, cfg[:n_c], mask[:n_c], threads)
+    oracle.evaluate(op, ot, cfg[:n_c], mask[:n_c], threads)
     dt = time.perf_counter() - t0
-    return dict(value=n_c * n_req / dt, unit=UNIT, cores=threads, kind="oracle",
-                sample=f"{n_c} mid-search candidates (of {len(cfg)}, all Alg. 2 runs) x "
-                       f"{n_req}-request trace prefix, {dt:.1f} s wall on {threads} threads",
+    return dict(value=n_c * len(sub) / dt, unit=UNIT, cores=threads, kind="oracle",
+                sample=f"{n_c} of the {len(cfg)} step-0 candidates (every Alg. 2 run's additions "
+                       f"to the empty placement) x the {len(sub)}-request 10-min trace prefix, "
+                       f"{dt:.1f} s wall on {threads} threads (oracle built -O3 -march=native)",
                 seconds=dt)
 
 
@@ -284,38 +279,42 @@ def main():
     total_ms = float(t.item())
     value = evals / (total_ms / 1e3)
 
-    # ---- end to end through the public API from pinned host buffers
+    # ---- end to end through the public API: every step uploads the problem
+    # tables and the trace from host memory (numpy arrays, as a caller holds
+    # them; asim_set_trace validates them on the host and copies them to the
+    # device), runs the search and reads the placement back.  One long-lived
+    # context, warmed up once outside the timed region (a serving process keeps
+    # its context).
     e2e = None
     if not args.no_e2e:
-        a_pin = torch.from_numpy(tr.arrival_ns).pin_memory()
-        m_pin = torch.from_numpy(tr.model).pin_memory()
-        h2d = a_pin.numel() * 8 + m_pin.numel() * 4 + sum(
+        h2d = tr.arrival_ns.nbytes + tr.model.astype(np.int32).nbytes + sum(
             np.asarray(x).nbytes for x in (prob.slo_ns, prob.stage_ns, prob.tail_ns,
                                            prob.mem_bytes, prob.cfg_stages, prob.cfg_devices))
-        d2h = 0
+        d2h = 8 * (prob.num_models + 64 + 4)
         tot = 0.0
         e_evals = 0
-        # one context per process (created outside the timed region, as a
-        # serving process keeps it); every step uploads the problem and the
-        # trace from pinned host memory, searches, and reads the result back
+        ke = max(1, min(args.steps, args.e2e_steps))
         s2 = Simulator(local)
-        for k in range(args.steps):
+        s2.set_problem(prob)
+        s2.set_trace(tr.arrival_ns, tr.model)
+        one_search(s2)  # warm-up: first-use allocations
+        for k in range(ke):
             flush.fill_(k & 0xFF)
             barrier()
             t0 = time.perf_counter()
             s2.set_problem(prob)
-            s2.set_trace(a_pin.numpy(), m_pin.numpy())
+            s2.set_trace(tr.arrival_ns, tr.model)
             r2 = one_search(s2)
             barrier()
             tot += time.perf_counter() - t0
             e_evals += r2.evaluated * N
-            d2h = 8 * (prob.num_models + 64 + 4)
         s2.close()
         tt = torch.tensor([tot], dtype=torch.float64, device="cuda")
         if pg is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = dict(value=e_evals / float(tt.item()), unit=UNIT, h2d_bytes_per_step=int(h2d),
-                   d2h_bytes_per_step=int(d2h), ms_per_step=float(tt.item()) / args.steps * 1e3)
+                   d2h_bytes_per_step=int(d2h), ms_per_step=float(tt.item()) / ke * 1e3,
+                   steps=ke, host_buffers="pageable numpy (validated and padded on the host)")
 
     if rank == 0:
         peaks = {}
@@ -357,6 +356,12 @@ def main():
                         pruned_runs=sum(1 for r in res.runs if r["pruned_at"] >= 0),
                         bounding=bool(args.bound), bounded_candidates=res.bounded,
                         l2="flushed between timed steps (256 MB write)",
+                        performed_value=st["spec_live_lanes"] / max(args.steps, 1)
+                        / (total_ms / args.steps / 1e3),
+                        performed_unit="(request, candidate) pairs replayed per s: each "
+                                       "simulated candidate replays only the requests of its "
+                                       "own hosting-graph component (component restriction); "
+                                       "`value` counts the whole trace per simulated candidate",
                         parallelism=f"candidate-sharded x{world}"),
             gpu_launches=int(launches),
             roofline=dict(bound="alu", achieved=achieved, peak=peak,
@@ -368,6 +373,11 @@ def main():
                           kernel_ms_share=k_ms / max(total_ms, 1e-9),
                           kernel_ms=k_ms, kernel_stage_updates=k_upd,
                           all_sim_ms_share=st["sim_ms"] / max(total_ms, 1e-9),
+                          pass2_ms=st["pass2_ms"], walk_ms=st["walk_ms"],
+                          walk_critical_chunks=st["walk_critical_chunks"],
+                          walk_candidates=st["walk_candidates"],
+                          walked_chunks=st["chunk_reruns"],
+                          lane_utilization=st["spec_live_lanes"] / max(1, st["spec_lane_slots"]),
                           stage_updates=st["stage_updates"], sim_launches=st["sim_launches"],
                           peak_basis=f"{sms} SMs x 64 int max/clk x {sm_max:.0f} MHz "
                                      "(MEASURED_PEAKS sm_max_mhz)"),

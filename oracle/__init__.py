@@ -35,6 +35,7 @@ _HDR = os.path.join(_HERE, "asim_oracle.h")
 _LIB = os.path.join(_HERE, "libasim_oracle.so")
 _lock = threading.Lock()
 _lib = None
+_active = _LIB  # the library lib() loads (the portable build unless use_timing_build())
 
 
 def build(force: bool = False) -> str:
@@ -64,12 +65,33 @@ class _Trace(ctypes.Structure):
                 ("model", ctypes.c_void_p)]
 
 
+def use_timing_build() -> str:
+    """For the CPU-baseline timings only (bench.py's cpu_baseline / reference
+    legs, scripts/cpu_baseline.py): the same des.cpp built -O3 -march=native
+    for THIS host, into a temporary directory on it.  The tests
+    keep the portable -O2 build.  Switches every later oracle call."""
+    import hashlib
+    import tempfile
+
+    global _lib, _active
+    tag = hashlib.sha1(open(_SRC, "rb").read() + open(_HDR, "rb").read()).hexdigest()[:12]
+    path = os.path.join(tempfile.gettempdir(), f"asim_oracle_native_{tag}_{os.getpid()}.so")
+    if not os.path.exists(path):
+        subprocess.check_call(["g++", "-O3", "-march=native", "-std=c++17", "-shared", "-fPIC",
+                               "-pthread", "-o", path, _SRC])
+    with _lock:
+        _active = path
+        _lib = None
+    return path
+
+
 def lib():
     global _lib
     with _lock:
         if _lib is None:
-            build()
-            L = ctypes.CDLL(_LIB)
+            if _active == _LIB:
+                build()
+            L = ctypes.CDLL(_active)
             P = ctypes.POINTER(_Problem)
             T = ctypes.POINTER(_Trace)
             vp = ctypes.c_void_p

@@ -46,51 +46,17 @@
 #include <stdint.h>
 
 #include "asim_internal.h"
+#include "chunk_common.cuh"
 #include "launch_cache.h"
 
 namespace asim {
 namespace {
 
-constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int kWarps = 4;        // warps per block; each warp takes units independently
 constexpr int kSTab = 16;        // stage entries per model in the uniform-config table
 constexpr int kCheckEvery = 64;  // coalescence test period (requests) in the fix-up
 enum Mode { SPEC = 0, DUAL = 1, WALK = 2 };
 
-// Batch index of the candidate in lane `lane` of work item `item`: items
-// either hold consecutive candidates (it.first + lane) or an explicit list
-// (item_cand, when the host regrouped the candidates by hosting component).
-__device__ __forceinline__ int64_t cand_of(const ChunkParams& P, const ItemDesc& it, int item,
-                                           int lane) {
-  return P.item_cand ? (int64_t)P.item_cand[(int64_t)item * 32 + lane]
-                     : (int64_t)it.first + lane;
-}
-
-template <typename T>
-struct TT;
-template <>
-struct TT<uint32_t> {
-  static constexpr bool kRel = true;
-  static __device__ __forceinline__ uint32_t maxv() { return 0xFFFFFFFFu; }
-  static __device__ __forceinline__ uint32_t clip(int64_t v) {
-    return v >= 0xFFFFFFFFll ? 0xFFFFFFFFu : (uint32_t)(v < 0 ? 0 : v);
-  }
-};
-template <>
-struct TT<int64_t> {
-  static constexpr bool kRel = false;
-  static __device__ __forceinline__ int64_t maxv() { return INT64_MAX; }
-  static __device__ __forceinline__ int64_t clip(int64_t v) { return v; }
-};
-
-template <typename T>
-__device__ __forceinline__ T tmax(T a, T b) {
-  return a > b ? a : b;
-}
-template <typename T>
-__device__ __forceinline__ T tmin(T a, T b) {
-  return a < b ? a : b;
-}
 
 // Per-warp shared-memory region.
 template <typename T>
@@ -123,6 +89,7 @@ struct alignas(16) TileReq {
   int32_t m;     // model
 };
 constexpr size_t kTileBytes = 32 * sizeof(TileReq<int64_t>);
+
 
 // hid_cap: bytes of the hosting-list region = max(hostings of any base in the
 // launch, 4 M) -- the scalar walker reuses it as M uint32 compact masks.
@@ -561,7 +528,6 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
   __syncwarp();
 
   int64_t good0 = 0, sum0 = 0, good1 = 0, sum1 = 0;
-  uint32_t nreq = 0, nlive = 0;  // pass-1 lane statistics (profiling)
   unsigned long long upd = 0;
   uint32_t upd32 = 0;  // hosts evaluated (S > 0) / stage updates (S == 0) by this lane
   bool coalesced = false;
@@ -627,7 +593,9 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
     T tl_l = 0, d0_l = 0;
     if constexpr (S > 0) tl_l = w.tail[mi];
     if constexpr (S == 1) d0_l = w.d[mi * kSTab];
-    // software pipeline: the next request's shuffles issue before this one runs
+    // software pipeline: the next request's shuffles issue before this one
+    // runs (staging the fields in shared memory instead costs a block of
+    // occupancy: measured slower, profiles/r2b)
     int jj = __ffs(todo) - 1;
     todo &= todo - 1;
     int m = __shfl_sync(FULL, mi, jj);
@@ -667,10 +635,6 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       }
       const bool live = active && ((kmask >> (cm & 63)) & 1ull);
       const bool mine = live && cm == my_m;
-      if constexpr (MODE == SPEC) {
-        ++nreq;
-        nlive += live ? 1u : 0u;
-      }
       int g0 = 0, g1 = 0;
       const int64_t l0 = step<T, S>(P, w, w.st0, lane, cm, chinfo, ch0, mine, my_g, live, car,
                                     dv, ctl, csl, upd32, g0);
@@ -698,18 +662,13 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
     }
   }
 
-  if (P.stage_updates) {
-    upd += (unsigned long long)upd32 * (S > 0 ? S : 1);
-    for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(FULL, upd, o);
-    if (lane == 0) atomicAdd(P.stage_updates, upd);
-  }
-  if constexpr (MODE == SPEC) {
-    if (P.lane_stats) {
-      const unsigned live_w = __reduce_add_sync(FULL, nlive);
-      if (lane == 0) {
-        atomicAdd(P.lane_stats, 32ull * nreq);
-        atomicAdd(P.lane_stats + 1, (unsigned long long)live_w);
-      }
+  // pass 1's work is counted on the host (chunked.cpp: it is fixed by the
+  // candidates' components); passes 2-3 count what they re-simulate
+  if constexpr (MODE != SPEC) {
+    if (P.stage_updates) {
+      upd += (unsigned long long)upd32 * (S > 0 ? S : 1);
+      for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(FULL, upd, o);
+      if (lane == 0) atomicAdd(P.stage_updates, upd);
     }
   }
   const int64_t cstride = (int64_t)P.num_items * 32;
@@ -1544,6 +1503,7 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     const int item = u >> 5, cl = u & 31;
     const ItemDesc it = P.items[item];
     if (it.S == 0 || cl >= it.count || !P.bt.cand_ok[cand_of(P, it, item, cl)]) continue;
+    if (lane_class(P, it, cand_of(P, it, item, cl)) >= 0) continue;  // the lane walker's
     const bool fits = P.scalar_walk && scalar_fits(P, it, cand_of(P, it, item, cl));
     if (fits != SCALAR) continue;  // the other walker's candidate
     // any chunk of this candidate flagged by pass 2?  (else nothing to walk)
@@ -1785,7 +1745,7 @@ cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, const WalkStr
   int64_t blocks = 1;
   cudaError_t e = cudaMemsetAsync(P.counter, 0, 3 * sizeof(uint32_t), ws.main);
   if (e != cudaSuccess) return e;
-  const bool fork = P.scalar_walk || any_dynamic;
+  const bool fork = P.scalar_walk || any_dynamic || (P.lane_walk && ws.lane_list && ws.lane);
   if (fork && (e = cudaEventRecord(ws.fork, ws.main)) != cudaSuccess) return e;
   e = grid_for(coop_walk_kernel<T, false>, smem, (int64_t)P.num_items * 32, sms, &blocks);
   if (e != cudaSuccess) return e;
@@ -1801,6 +1761,13 @@ cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, const WalkStr
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaEventRecord(ws.join[0], ws.side[0])) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(ws.main, ws.join[0], 0)) != cudaSuccess) return e;
+  }
+  if (P.lane_walk && ws.lane_list && ws.lane) {
+    int64_t dummy = 0;
+    e = launch_lane_walk(P, end_src, ws.lane_list, ws.lane_counts, *ws.lane, sms, &dummy);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(ws.join[2], ws.side[2])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ws.main, ws.join[2], 0)) != cudaSuccess) return e;
   }
   if (any_dynamic) {
     ChunkParams Q = P;
@@ -1837,7 +1804,8 @@ cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32,
   if (e != cudaSuccess) return e;
   e = u32 ? launch_walk_t<uint32_t>(P, end_src, ws, sms, any_dynamic)
           : launch_walk_t<int64_t>(P, end_src, ws, sms, any_dynamic);
-  if (launches) *launches += 1 + (any_dynamic ? 1 : 0) + (P.scalar_walk ? 1 : 0);
+  if (launches)
+    *launches += 1 + (any_dynamic ? 1 : 0) + (P.scalar_walk ? 1 : 0) + (P.lane_walk ? 1 + kLaneClasses : 0);
   return e;
 }
 

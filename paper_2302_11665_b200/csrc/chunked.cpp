@@ -156,6 +156,64 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   return ASIM_OK;
 }
 
+// Pass 1's algorithmic work, fixed by the candidates alone (profiling): every
+// (item, chunk) unit replays the chunk's requests of the models some active
+// lane simulates (the union of the lanes' components), and a live lane
+// performs, for each request of a model m of its component, one max-plus
+// update per stage of every group hosting m.  Summed over
+// the J chunks that is the whole trace's per-model counts n(m):
+//   stage updates  = sum_lanes sum_{m in K_c} n(m) * sum_{g hosts m} s_g
+//   live lane-reqs = sum_lanes sum_{m in K_c} n(m)
+//   lane slots     = 32 * sum_items sum_{m in union of the lanes' K_c} n(m)
+static void pass1_work(asim_ctx* ctx, const HostBatch& hb,
+                       const std::vector<asim::ItemDesc>& items,
+                       const std::vector<int32_t>& item_cand, bool grouped) {
+  const HostProblem& hp = ctx->hp;
+  const int32_t M = hp.M;
+  const bool restricted = !hb.cand_kmask.empty();
+  unsigned long long upd = 0, live = 0, slots = 0;
+  std::vector<int64_t> hs(M);  // sum of host stage counts of m in the base
+  std::vector<uint8_t> rel(M);
+  for (size_t i = 0; i < items.size(); ++i) {
+    const asim::ItemDesc& it = items[i];
+    const int32_t b = it.base;
+    for (int32_t m = 0; m < M; ++m) {
+      const uint64_t mk = hb.base_mask[(size_t)b * M + m];
+      int64_t x = 0;
+      for (uint64_t r = mk; r; r &= r - 1) {
+        const int g = __builtin_ctzll(r);
+        x += hp.cfg_stages[hb.base_cfg[(size_t)b * hb.G + g]];
+      }
+      hs[m] = x;
+      rel[m] = 0;
+    }
+    for (int32_t l = 0; l < it.count; ++l) {
+      const int32_t c = grouped ? item_cand[i * 32 + l] : it.first + l;
+      if (!hb.cand_ok[c]) continue;
+      const int32_t mm = hb.cand_model[c], gg = hb.cand_group[c];
+      const uint64_t km = restricted ? hb.cand_kmask[c] : ~0ull;
+      for (int32_t m = 0; m < M; ++m) {
+        const bool in = restricted ? (m < 64 && ((km >> m) & 1ull))
+                                   : (hs[m] > 0 || m == mm);
+        if (!in) continue;
+        rel[m] = 1;
+        const int64_t n = ctx->model_n[m];
+        live += (unsigned long long)n;
+        int64_t h = hs[m];
+        if (m == mm) h += hp.cfg_stages[hb.base_cfg[(size_t)b * hb.G + gg]];
+        upd += (unsigned long long)(n * h);
+      }
+    }
+    int64_t u = 0;
+    for (int32_t m = 0; m < M; ++m)
+      if (rel[m]) u += ctx->model_n[m];
+    slots += 32ull * (unsigned long long)u;
+  }
+  ctx->p1_updates += (int64_t)upd;
+  ctx->p1_live += (int64_t)live;
+  ctx->p1_slots += (int64_t)slots;
+}
+
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                              const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
   const int64_t N = ctx->n;
@@ -281,6 +339,11 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.stage_updates = out.stage_updates;
   P.walked = ctx->profiling ? ctx->d_walked.as<unsigned long long>() : nullptr;
   P.scalar_walk = ctx->scalar_walk ? 1 : 0;
+  // the lane walker: uint32 times, component-restricted batches (M <= 64), no
+  // fast-heuristic statistics rows (set below)
+  P.lane_walk = (ctx->lane_walk && u32 && !hb.cand_kmask.empty() && !hb.cand_gmask.empty() &&
+                 out.good_per_model == nullptr && out.busy == nullptr) ? 1 : 0;
+  P.tile_mask = ctx->has_tmask ? ctx->d_tmask.as<uint64_t>() : nullptr;
   P.walk_log = ctx->walk_log;
   P.spec_state = opt ? opt->spec_state : nullptr;
   P.spec_row = opt ? opt->spec_row : nullptr;
@@ -336,10 +399,7 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     // profiling: pass 1 alone (the dominant kernel) gets its own events and
     // work counter (d_counter[1]; the total is d_counter[0] + d_counter[1])
     asim::ChunkParams P1 = P;
-    if (ctx->profiling && P.stage_updates) {
-      P1.stage_updates = ctx->d_counter.as<unsigned long long>() + 1;
-      P1.lane_stats = ctx->d_counter.as<unsigned long long>() + 2;
-    }
+    if (ctx->profiling && P.stage_updates) pass1_work(ctx, hb, items, item_cand, grouped);
     PhaseTimer t(ctx, 0, st, P.stage_updates != nullptr);
     e = asim::launch_chunk_pass(P1, false, u32, st, ctx->sms, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
@@ -359,8 +419,17 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     }
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 2");
     // ---- pass 3: walk the chunks whose start state was wrong (exact chains)
-    const asim::WalkStreams ws{st, {ctx->side[0], ctx->side[1]}, ctx->ev_fork,
-                               {ctx->ev_join[0], ctx->ev_join[1]}};
+    asim::WalkStreams ws{st, {ctx->side[0], ctx->side[1], ctx->side[2]}, ctx->ev_fork,
+                         {ctx->ev_join[0], ctx->ev_join[1], ctx->ev_join[2]}, nullptr, nullptr,
+                         nullptr};
+    if (P.lane_walk) {
+      e = ctx->c_lane_list.ensure((size_t)asim::kLaneClassCount * I * 2 * 4 + 8);
+      if (e == cudaSuccess) e = ctx->c_lane_counts.ensure(64 * 4);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "lane walker buffers");
+      ws.lane_list = ctx->c_lane_list.as<int32_t>();
+      ws.lane_counts = ctx->c_lane_counts.as<uint32_t>();
+      ws.lane = &ctx->lane;
+    }
     {
       PhaseTimer t(ctx, 2, st, P.stage_updates != nullptr);
       e = asim::launch_chunk_walk(P, end_src, u32, any_dynamic, ws, ctx->sms, &ctx->launches);

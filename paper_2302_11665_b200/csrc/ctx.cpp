@@ -278,14 +278,23 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   if (const char* sw = getenv("ASIM_SCALAR_WALK")) ctx->scalar_walk = sw[0] != '0';
   if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
   if (const char* gc = getenv("ASIM_GROUP_CANDIDATES")) ctx->group_cands = gc[0] != '0';
+  if (const char* lw = getenv("ASIM_LANE_WALK")) ctx->lane_walk = lw[0] != '0';
   {
     DeviceGuard dg(cuda_device);
     e = cudaSuccess;
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
       e = cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+    for (int k = 0; k < asim::kLaneClassCount && e == cudaSuccess; ++k) {
+      e = cudaStreamCreateWithFlags(&ctx->lane.streams[k], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->lane.done[k], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->lane.listed, cudaEventDisableTiming);
+    ctx->lane.fork = ctx->ev_fork;
+    ctx->lane.list_stream = ctx->side[2];
+    ctx->lane.join_stream = ctx->side[2];
     if (e != cudaSuccess) {
       asim_destroy(ctx);
       return asim_fail(nullptr, ASIM_ECUDA, std::string("side streams: ") + cudaGetErrorString(e));
@@ -309,15 +318,20 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
                     &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
                     &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src, &ctx->d_cand_kmask,
-                    &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_perm, &ctx->c_item_cand, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
+                    &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_perm, &ctx->c_item_cand, &ctx->c_lane_list, &ctx->c_lane_counts, &ctx->d_tmask, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
                     &ctx->c_fbusy};
     for (DBuf* b : bufs) b->release();
     for (DBuf& b : ctx->spool) b.release();
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
       if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
       if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);
     }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    for (int k = 0; k < asim::kLaneClassCount; ++k) {
+      if (ctx->lane.streams[k]) cudaStreamDestroy(ctx->lane.streams[k]);
+      if (ctx->lane.done[k]) cudaEventDestroy(ctx->lane.done[k]);
+    }
+    if (ctx->lane.listed) cudaEventDestroy(ctx->lane.listed);
   }
   delete ctx;
 }
@@ -343,6 +357,7 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   ctx->sim_launches = 0;
   ctx->sim_ms = 0.0;
   for (double& x : ctx->phase_ms) x = 0.0;
+  ctx->p1_updates = ctx->p1_live = ctx->p1_slots = 0;
   ctx->request_evals = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 32);
@@ -415,13 +430,13 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->launches = ctx->launches;
   out->sim_launches = ctx->sim_launches;
   out->sim_ms = ctx->sim_ms;
-  out->stage_updates = (int64_t)(upd2[0] + upd2[1]);
-  out->spec_stage_updates = (int64_t)upd2[1];
+  out->stage_updates = (int64_t)upd2[0] + ctx->p1_updates;
+  out->spec_stage_updates = ctx->p1_updates;
   out->spec_ms = ctx->phase_ms[0];
   out->pass2_ms = ctx->phase_ms[1];
   out->walk_ms = ctx->phase_ms[2];
-  out->spec_lane_slots = (int64_t)upd2[2];
-  out->spec_live_lanes = (int64_t)upd2[3];
+  out->spec_lane_slots = ctx->p1_slots;
+  out->spec_live_lanes = ctx->p1_live;
   out->request_evals = ctx->request_evals;
   out->chunk_reruns = (int64_t)walked[0];
   out->walk_candidates = (int64_t)walked[1];
@@ -556,6 +571,17 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
   if (e == cudaSuccess) e = upload(ctx->d_model, mp, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload trace");
+  // per 32-request tile, the models occurring in it (lane walker tile skips;
+  // model ids fit a 64-bit mask only when M <= 64)
+  ctx->has_tmask = false;
+  if (ctx->hp.M <= 64) {
+    std::vector<uint64_t> tm(npad / 32, 0);
+    for (int64_t i = 0; i < n; ++i) tm[i >> 5] |= 1ull << m[i];
+    e = upload(ctx->d_tmask, tm, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "upload tile masks");
+    ctx->has_tmask = true;
+  }
   ctx->n = n;
   ctx->max_arrival = n ? a[n - 1] : 0;
   ctx->min_arrival = n ? a[0] : 0;

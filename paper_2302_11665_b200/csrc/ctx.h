@@ -67,6 +67,8 @@ struct asim_ctx {
   DBuf d_inc;           // batching stage increments (asim_evaluate_batching)
   DBuf d_order;         // batching launch order (costliest candidates first)
   DBuf d_mcum;          // per-model running arrival sums (batching)
+  DBuf d_tmask;         // per 32-request tile: models present (M <= 64)
+  bool has_tmask = false;
 
   // statistics (asim_set_profiling)
   bool profiling = false;
@@ -74,18 +76,21 @@ struct asim_ctx {
   // chunked-path phases timed by their own events: 0 = pass 1, 1 = pass 2, 2 = walk
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_events[3];
   double phase_ms[3] = {0.0, 0.0, 0.0};
+  int64_t p1_updates = 0, p1_live = 0, p1_slots = 0;  // pass-1 work (host-counted, profiling)
   int64_t sim_launches = 0;
   double sim_ms = 0.0;
   int64_t request_evals = 0;
-  DBuf d_counter;  // unsigned long long counters [4]: stage updates of other kernels, of
-                   // pass 1; pass-1 lane slots (requests x 32), pass-1 live lane-requests
+  DBuf d_counter;  // unsigned long long stage-update counter of the kernels that count on
+                   // the device (everything but pass 1; slots [1..3] unused)
   DBuf d_walked;   // unsigned long long walked-chunk counter
 
   int sms = 148;
   DBuf spool[kSearchPool];  // search scratch kept across searches (search.cpp)
   // side streams / events of the concurrent walk pass (created by asim_create)
-  cudaStream_t side[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  DBuf c_lane_list, c_lane_counts;  // lane walker scratch (walk.cu)
+  asim::LaneStreams lane{};         // lane walker streams / events (one stream per class)
   // chunked path buffers (chunked.cpp)
   DBuf c_items, c_begin, c_spec_good, c_spec_sum, c_fix_good, c_fix_sum, c_spec_end, c_fix_end,
       c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_end_src;
@@ -101,6 +106,7 @@ struct asim_ctx {
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
+  bool lane_walk = false;    // item walker for small uniform components (walk.cu; ASIM_LANE_WALK=1: on)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
 
   // scratch for evaluate()

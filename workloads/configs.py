@@ -116,9 +116,12 @@ def s2(seed=0, rate=80.0, duration=3600.0, slo_scale=5.0):
     return prob, tr
 
 
-def s3(seed=0, rate=100.0, duration=3600.0, slo_scale=5.0, cv=4.0):
+def s3(seed=0, rate=100.0, duration=86400.0, slo_scale=5.0, cv=4.0):
+    """The target config; shorter traces are the opening stretch of the day
+    (the day's per-model MAF2 window factors, normalised over the day)."""
     prob = table1_problem("S3", 64, slo_scale)
-    tr = traces.maf2_shaped(seed, prob.num_models, rate, duration, cv=cv)
+    tr = traces.maf2_shaped(seed, prob.num_models, rate, duration, cv=cv,
+                            horizon=max(duration, 86400.0))
     return prob, tr
 
 

@@ -135,19 +135,25 @@ def maf1_shaped(seed: int, num_models: int, total_rate: float, duration: float,
 
 def maf2_shaped(seed: int, num_models: int, total_rate: float, duration: float,
                 exponent: float = 1.0, window: float = 5400.0, cv: float = 4.0,
-                sigma: float = 1.0) -> Trace:
+                sigma: float = 1.0, horizon: float | None = None) -> Trace:
     """MAF2-shaped: "very bursty ... distributed across functions in a highly
     skewed way".  Power-law exponent 1 over a seeded ranking, 5.4 ks
     windows (P:105 footnote) with lognormal(sigma) factors normalised to mean 1
-    per model, CV 4 within windows."""
+    per model over `horizon` (default: the trace itself), CV 4 within windows.
+    A trace shorter than the horizon is its opening stretch: with horizon = one
+    day a 1-h trace keeps the day's per-model window factors (a 1-h horizon
+    has a single window, whose normalised factor is exactly 1 -- no
+    modulation at all)."""
     rng = np.random.default_rng(seed)
     w = power_law_weights(num_models, exponent, rng)
+    horizon = duration if horizon is None else max(horizon, duration)
+    nwin_h = int(np.ceil(horizon / window))
     nwin = int(np.ceil(duration / window))
     times = []
     for m in range(num_models):
-        f = rng.lognormal(0.0, sigma, size=nwin)
-        f = f / f.mean()
+        f = rng.lognormal(0.0, sigma, size=nwin_h)
+        f = (f / f.mean())[:nwin]
         times.append(modulated_gamma_process(rng, total_rate * w[m], cv, duration, window, f))
     return merge(times, dict(kind="maf2_shaped", seed=seed, total_rate=total_rate,
                              duration=duration, exponent=exponent, window=window, cv=cv,
-                             sigma=sigma))
+                             sigma=sigma, horizon=horizon))

@@ -189,6 +189,10 @@ cudaError_t launch_chunk_pass(const ChunkParams& P, bool dual, bool u32, cudaStr
                               int64_t* launches);
 cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
                                 int64_t* launches);
+// After pass 2: out[c] = 1 if candidate c (batch index) has a chunk whose
+// trajectories never met, i.e. it walks (the search's walk prediction).
+cudaError_t launch_walk_flags(const ChunkParams& P, uint8_t* out, cudaStream_t st,
+                              int64_t* launches);
 // Fast heuristic statistics: one warp per item (one candidate each, uniform
 // config, S class != 0) over the whole trace; writes good, sum, per-model good
 // and per-group busy into `out`.  fast_stats_smem: dynamic shared memory.

@@ -1891,6 +1891,28 @@ cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32,
   return cudaGetLastError();
 }
 
+// out[c] = 1 for every candidate of the run whose trajectories pass 2 left
+// unmet in some chunk (it walks), else 0 (batch-indexed; other entries kept).
+__global__ void walk_flags_kernel(ChunkParams P, uint8_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)P.num_items * 32) return;
+  const int item = (int)(t >> 5), lane = (int)(t & 31);
+  const ItemDesc it = P.items[item];
+  if (lane >= it.count) return;
+  uint32_t f = 0;
+  for (int j = 1; j + 1 < P.J && !f; ++j) f = (P.fix_flag[(int64_t)j * P.num_items + item] >> lane) & 1u;
+  out[cand_of(P, it, item, lane)] = (uint8_t)f;
+}
+
+cudaError_t launch_walk_flags(const ChunkParams& P, uint8_t* out, cudaStream_t st,
+                              int64_t* launches) {
+  const int64_t n = (int64_t)P.num_items * 32;
+  if (n == 0 || P.J < 3) return cudaSuccess;  // no chunk after a flagged one
+  walk_flags_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_chunk_reduce(const ChunkParams& P, const DevOut& out, cudaStream_t st,
                                 int64_t* launches) {
   const int64_t n = (int64_t)P.num_items * 32;

@@ -113,9 +113,11 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   const bool u32 = theta > 0;
   const int32_t hid_cap = hid_cap_for(ctx, hb);
   if (asim::fast_stats_smem(slots_max, hp.M, hid_cap, u32) > 227 * 1024) return ASIM_OK;
-  cudaError_t e = upload(ctx->c_items, items, st);
-  if (e == cudaSuccess) e = ctx->c_spm.ensure((size_t)C * hp.M * 4 + 8);  // int32 count rows
-  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_spm.p, 0, (size_t)C * hp.M * 4, st);
+  ChunkSlot& cs = ctx->slot[0];
+  cs.last_valid = false;  // its chunk buffers are reused below
+  cudaError_t e = upload(cs.items, items, st);
+  if (e == cudaSuccess) e = cs.spm.ensure((size_t)C * hp.M * 4 + 8);  // int32 count rows
+  if (e == cudaSuccess) e = cudaMemsetAsync(cs.spm.p, 0, (size_t)C * hp.M * 4, st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload fast items");
   asim::ChunkParams P{};
   P.pr = ctx->dev_problem();
@@ -129,13 +131,13 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
   P.bt.cand_ok = ctx->d_cand_ok.as<uint8_t>();
   P.bt.cand_kmask = hb.cand_kmask.empty() ? nullptr : ctx->d_cand_kmask.as<uint64_t>();
   P.bt.C = C;
-  P.items = ctx->c_items.as<asim::ItemDesc>();
+  P.items = cs.items.as<asim::ItemDesc>();
   P.num_items = (int32_t)items.size();
   P.J = 1;
   P.theta = theta;
   P.slots_max = slots_max;
   P.hid_cap = hid_cap;
-  P.spec_pm = ctx->c_spm.as<int32_t>();
+  P.spec_pm = cs.spm.as<int32_t>();
   P.stat_C = C;
   P.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -214,8 +216,11 @@ static void pass1_work(asim_ctx* ctx, const HostBatch& hb,
   ctx->p1_slots += (int64_t)slots;
 }
 
-asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
-                             const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
+// One chunked run of the candidates `cand` (batch indices) on slot `cs`,
+// stream-ordered on `st`.
+static asim_status run_slot(asim_ctx* ctx, ChunkSlot& cs, const HostBatch& hb,
+                            std::vector<int32_t> ord, const asim::DevOut& out, cudaStream_t st,
+                            const ChunkOptions* opt) {
   const int64_t N = ctx->n;
   const HostProblem& hp = ctx->hp;
   // ---- work items: <= 32 consecutive candidates of one base
@@ -244,9 +249,6 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   // Candidate order inside the range: the batch's, or grouped by hosting
   // component (hb.cand_key, the search's): a warp replays the union of its
   // lanes' requests, so lanes sharing their components keep every lane busy.
-  std::vector<int32_t> ord;
-  ord.reserve(end - begin);
-  for (int64_t c = begin; c < end; ++c) ord.push_back((int32_t)c);
   const bool grouped = !hb.cand_key.empty();
   if (grouped)
     std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
@@ -290,19 +292,19 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
 
   // ---- device buffers (grow-only)
   const int64_t per_chunk = (int64_t)I * 32;
-  cudaError_t e = upload(ctx->c_items, items, st);
-  if (e == cudaSuccess && grouped) e = upload(ctx->c_item_cand, item_cand, st);
-  if (e == cudaSuccess) e = upload(ctx->c_begin, cb, st);
-  if (e == cudaSuccess) e = ctx->c_spec_good.ensure(J * per_chunk * 4);
-  if (e == cudaSuccess) e = ctx->c_spec_sum.ensure(J * per_chunk * 8);
-  if (e == cudaSuccess) e = ctx->c_fix_good.ensure(J * per_chunk * 4);
-  if (e == cudaSuccess) e = ctx->c_fix_sum.ensure(J * per_chunk * 8);
-  if (e == cudaSuccess) e = ctx->c_spec_end.ensure(J * I * (int64_t)slots_max * 32 * tsz);
-  if (e == cudaSuccess) e = ctx->c_fix_end.ensure(J * I * (int64_t)slots_max * 32 * tsz);
-  if (e == cudaSuccess) e = ctx->c_spec_epoch.ensure(J * I * 8);
-  if (e == cudaSuccess) e = ctx->c_fix_epoch.ensure(J * I * 8);
-  if (e == cudaSuccess) e = ctx->c_flag.ensure(J * I * 4 + 8);
-  if (e == cudaSuccess) e = ctx->c_counter.ensure(16);
+  cudaError_t e = upload(cs.items, items, st);
+  if (e == cudaSuccess && grouped) e = upload(cs.item_cand, item_cand, st);
+  if (e == cudaSuccess) e = upload(cs.begin, cb, st);
+  if (e == cudaSuccess) e = cs.spec_good.ensure(J * per_chunk * 4);
+  if (e == cudaSuccess) e = cs.spec_sum.ensure(J * per_chunk * 8);
+  if (e == cudaSuccess) e = cs.fix_good.ensure(J * per_chunk * 4);
+  if (e == cudaSuccess) e = cs.fix_sum.ensure(J * per_chunk * 8);
+  if (e == cudaSuccess) e = cs.spec_end.ensure(J * I * (int64_t)slots_max * 32 * tsz);
+  if (e == cudaSuccess) e = cs.fix_end.ensure(J * I * (int64_t)slots_max * 32 * tsz);
+  if (e == cudaSuccess) e = cs.spec_epoch.ensure(J * I * 8);
+  if (e == cudaSuccess) e = cs.fix_epoch.ensure(J * I * 8);
+  if (e == cudaSuccess) e = cs.flag.ensure(J * I * 4 + 8);
+  if (e == cudaSuccess) e = cs.counter.ensure(16);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk buffers");
 
   asim::ChunkParams P{};
@@ -318,26 +320,26 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   P.bt.cand_kmask = hb.cand_kmask.empty() ? nullptr : ctx->d_cand_kmask.as<uint64_t>();
   P.bt.cand_gmask = hb.cand_gmask.empty() ? nullptr : ctx->d_cand_gmask.as<uint64_t>();
   P.bt.C = (int64_t)hb.cand_base.size();
-  P.items = ctx->c_items.as<asim::ItemDesc>();
-  P.item_cand = grouped ? ctx->c_item_cand.as<int32_t>() : nullptr;
+  P.items = cs.items.as<asim::ItemDesc>();
+  P.item_cand = grouped ? cs.item_cand.as<int32_t>() : nullptr;
   P.num_items = I;
   P.J = (int32_t)J;
-  P.chunk_begin = ctx->c_begin.as<int64_t>();
+  P.chunk_begin = cs.begin.as<int64_t>();
   P.theta = theta;
   P.slots_max = slots_max;
   P.hid_cap = hid_cap_for(ctx, hb);
-  P.counter = ctx->c_counter.as<uint32_t>();
-  P.spec_good = ctx->c_spec_good.as<int32_t>();
-  P.spec_sum = ctx->c_spec_sum.as<int64_t>();
-  P.spec_end = ctx->c_spec_end.p;
-  P.spec_epoch = ctx->c_spec_epoch.as<int64_t>();
-  P.fix_good = ctx->c_fix_good.as<int32_t>();
-  P.fix_sum = ctx->c_fix_sum.as<int64_t>();
-  P.fix_end = ctx->c_fix_end.p;
-  P.fix_epoch = ctx->c_fix_epoch.as<int64_t>();
-  P.fix_flag = ctx->c_flag.as<uint32_t>();
+  P.counter = cs.counter.as<uint32_t>();
+  P.spec_good = cs.spec_good.as<int32_t>();
+  P.spec_sum = cs.spec_sum.as<int64_t>();
+  P.spec_end = cs.spec_end.p;
+  P.spec_epoch = cs.spec_epoch.as<int64_t>();
+  P.fix_good = cs.fix_good.as<int32_t>();
+  P.fix_sum = cs.fix_sum.as<int64_t>();
+  P.fix_end = cs.fix_end.p;
+  P.fix_epoch = cs.fix_epoch.as<int64_t>();
+  P.fix_flag = cs.flag.as<uint32_t>();
   P.stage_updates = out.stage_updates;
-  P.walked = ctx->profiling ? ctx->d_walked.as<unsigned long long>() : nullptr;
+  P.walked = ctx->profiling ? cs.walked.as<unsigned long long>() : nullptr;
   P.scalar_walk = ctx->scalar_walk ? 1 : 0;
   // the lane walker: uint32 times, component-restricted batches (M <= 64), no
   // fast-heuristic statistics rows (set below)
@@ -354,23 +356,23 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
   // fast-heuristic statistics (per-model good, per-group busy) of every candidate
   const bool stats = out.good_per_model != nullptr || out.busy != nullptr;
   if (stats) {
-    if (!out.good_per_model || !out.busy || begin != 0 || end != P.bt.C)
+    if (!out.good_per_model || !out.busy || (int64_t)ord.size() != P.bt.C)
       return asim_fail(ctx, ASIM_ESTATE, "internal: statistics need both outputs, whole batch");
     const int64_t C = P.bt.C;
     const size_t npm = (size_t)J * C * hp.M, nb = (size_t)J * C * std::max(hb.G, 1);
-    e = ctx->c_spm.ensure(npm * 4 + 8);
-    if (e == cudaSuccess) e = ctx->c_fpm.ensure(npm * 4 + 8);
-    if (e == cudaSuccess) e = ctx->c_sbusy.ensure(nb * 8 + 8);
-    if (e == cudaSuccess) e = ctx->c_fbusy.ensure(nb * 8 + 8);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_spm.p, 0, npm * 4, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_fpm.p, 0, npm * 4, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_sbusy.p, 0, nb * 8, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->c_fbusy.p, 0, nb * 8, st);
+    e = cs.spm.ensure(npm * 4 + 8);
+    if (e == cudaSuccess) e = cs.fpm.ensure(npm * 4 + 8);
+    if (e == cudaSuccess) e = cs.sbusy.ensure(nb * 8 + 8);
+    if (e == cudaSuccess) e = cs.fbusy.ensure(nb * 8 + 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cs.spm.p, 0, npm * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cs.fpm.p, 0, npm * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cs.sbusy.p, 0, nb * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cs.fbusy.p, 0, nb * 8, st);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "statistics buffers");
-    P.spec_pm = ctx->c_spm.as<int32_t>();
-    P.fix_pm = ctx->c_fpm.as<int32_t>();
-    P.spec_busy = ctx->c_sbusy.as<int64_t>();
-    P.fix_busy = ctx->c_fbusy.as<int64_t>();
+    P.spec_pm = cs.spm.as<int32_t>();
+    P.fix_pm = cs.fpm.as<int32_t>();
+    P.spec_busy = cs.sbusy.as<int64_t>();
+    P.fix_busy = cs.fbusy.as<int64_t>();
     P.stat_C = C;
   }
 
@@ -389,9 +391,9 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
         ++P.nclass;
       }
     }
-    e = upload(ctx->c_perm, perm, st);
+    e = upload(cs.perm, perm, st);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "item classes");
-    P.item_perm = ctx->c_perm.as<int32_t>();
+    P.item_perm = cs.perm.as<int32_t>();
   }
   // ---- pass 1: every (item, chunk) from the speculative start
   P.num_units = (int32_t)(J * I);
@@ -405,9 +407,9 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 1");
   }
 
-  e = ctx->c_end_src.ensure(J * I * 4 + 8);
+  e = cs.end_src.ensure(J * I * 4 + 8);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "end_src buffer");
-  uint32_t* end_src = ctx->c_end_src.as<uint32_t>();
+  uint32_t* end_src = cs.end_src.as<uint32_t>();
   bool any_dynamic = false;
   for (const auto& it : items) any_dynamic |= it.S == 0;
   if (J > 1) {
@@ -418,17 +420,21 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
       e = asim::launch_chunk_pass(P, true, u32, st, ctx->sms, &ctx->launches);
     }
     if (e != cudaSuccess) return asim_cuda(ctx, e, "chunk pass 2");
+    if (opt && opt->walk_out) {
+      e = asim::launch_walk_flags(P, opt->walk_out, st, &ctx->launches);
+      if (e != cudaSuccess) return asim_cuda(ctx, e, "walk flags");
+    }
     // ---- pass 3: walk the chunks whose start state was wrong (exact chains)
-    asim::WalkStreams ws{st, {ctx->side[0], ctx->side[1], ctx->side[2]}, ctx->ev_fork,
-                         {ctx->ev_join[0], ctx->ev_join[1], ctx->ev_join[2]}, nullptr, nullptr,
+    asim::WalkStreams ws{st, {cs.side[0], cs.side[1], cs.side[2]}, cs.ev_fork,
+                         {cs.ev_join[0], cs.ev_join[1], cs.ev_join[2]}, nullptr, nullptr,
                          nullptr};
     if (P.lane_walk) {
-      e = ctx->c_lane_list.ensure((size_t)asim::kLaneClassCount * I * 2 * 4 + 8);
-      if (e == cudaSuccess) e = ctx->c_lane_counts.ensure(64 * 4);
+      e = cs.lane_list.ensure((size_t)asim::kLaneClassCount * I * 2 * 4 + 8);
+      if (e == cudaSuccess) e = cs.lane_counts.ensure(64 * 4);
       if (e != cudaSuccess) return asim_cuda(ctx, e, "lane walker buffers");
-      ws.lane_list = ctx->c_lane_list.as<int32_t>();
-      ws.lane_counts = ctx->c_lane_counts.as<uint32_t>();
-      ws.lane = &ctx->lane;
+      ws.lane_list = cs.lane_list.as<int32_t>();
+      ws.lane_counts = cs.lane_counts.as<uint32_t>();
+      ws.lane = &cs.lane;
     }
     {
       PhaseTimer t(ctx, 2, st, P.stage_updates != nullptr);
@@ -445,14 +451,47 @@ asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, 
     e = asim::launch_chunk_stats_reduce(P, out, st, &ctx->launches);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "statistics reduce");
   }
-  ctx->last_valid = true;
-  ctx->last_u32 = u32;
-  ctx->last_params = P;
-  ctx->last_items = std::move(items);
-  ctx->last_pos.assign(P.bt.C, -1);  // candidate -> item * 32 + lane of this run
-  for (size_t i = 0, pos = 0; i < ctx->last_items.size(); ++i)
-    for (int32_t l = 0; l < ctx->last_items[i].count; ++l, ++pos)
-      ctx->last_pos[ord[pos]] = (int32_t)(i * 32 + l);
+  cs.last_valid = true;
+  cs.last_u32 = u32;
+  cs.last_gen = ctx->batch_gen;
+  cs.last_params = P;
+  cs.last_items = std::move(items);
+  cs.last_pos.assign(P.bt.C, -1);  // candidate -> item * 32 + lane of this run
+  for (size_t i = 0, pos = 0; i < cs.last_items.size(); ++i)
+    for (int32_t l = 0; l < cs.last_items[i].count; ++l, ++pos)
+      cs.last_pos[ord[pos]] = (int32_t)(i * 32 + l);
+  return ASIM_OK;
+}
+
+asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
+                             const asim::DevOut& out, cudaStream_t st, const ChunkOptions* opt) {
+  std::vector<int32_t> ord;
+  ord.reserve(end > begin ? end - begin : 0);
+  for (int64_t c = begin; c < end; ++c) ord.push_back((int32_t)c);
+  ctx->slot[1].last_valid = false;  // only slot 0 holds this batch's run
+  return run_slot(ctx, ctx->slot[0], hb, std::move(ord), out, st, opt);
+}
+
+asim_status asim_run_chunked_split(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
+                                   const std::vector<uint8_t>& group, const asim::DevOut& out,
+                                   cudaStream_t st, const ChunkOptions* opt) {
+  std::vector<int32_t> ord[kChunkSlots];
+  for (int64_t c = begin; c < end; ++c) ord[group[c] ? 1 : 0].push_back((int32_t)c);
+  if (ord[0].empty() || ord[1].empty())
+    return asim_run_chunked(ctx, hb, begin, end, out, st, opt);
+  // fork both runs from the caller's stream (after the batch upload), join back
+  cudaError_t e = cudaEventRecord(ctx->ev_split, st);
+  if (e != cudaSuccess) return asim_cuda(ctx, e, "split fork");
+  for (int k = 0; k < kChunkSlots; ++k) {
+    ChunkSlot& cs = ctx->slot[k];
+    e = cudaStreamWaitEvent(cs.main, ctx->ev_split, 0);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "split fork");
+    asim_status rc = run_slot(ctx, cs, hb, std::move(ord[k]), out, cs.main, opt);
+    if (rc) return rc;
+    e = cudaEventRecord(cs.ev_done, cs.main);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, cs.ev_done, 0);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "split join");
+  }
   return ASIM_OK;
 }
 
@@ -460,20 +499,31 @@ asim_status asim_publish_candidates(asim_ctx* ctx, const std::vector<int64_t>& c
                                     const std::vector<int32_t>& rows, int64_t* out,
                                     cudaStream_t st) {
   if (cands.empty()) return ASIM_OK;
-  if (!ctx->last_valid)
-    return asim_fail(ctx, ASIM_ESTATE, "internal: no chunked run to publish from");
-  std::vector<asim::PublishItem> pub;
+  // the runs of the current batch (one, or two for a split step)
+  std::vector<asim::PublishItem> pub[kChunkSlots];
   for (size_t i = 0; i < cands.size(); ++i) {
     const int64_t c = cands[i];
-    const int32_t pos = (c >= 0 && c < (int64_t)ctx->last_pos.size()) ? ctx->last_pos[c] : -1;
-    if (pos < 0)
+    bool found = false;
+    for (int k = 0; k < kChunkSlots && !found; ++k) {
+      const ChunkSlot& cs = ctx->slot[k];
+      if (!cs.last_valid || cs.last_gen != ctx->batch_gen) continue;
+      const int32_t pos = (c >= 0 && c < (int64_t)cs.last_pos.size()) ? cs.last_pos[c] : -1;
+      if (pos < 0) continue;
+      pub[k].push_back(asim::PublishItem{pos >> 5, pos & 31, rows[i]});
+      found = true;
+    }
+    if (!found)
       return asim_fail(ctx, ASIM_ESTATE, "internal: candidate not in the last chunked run");
-    pub.push_back(asim::PublishItem{pos >> 5, pos & 31, rows[i]});
   }
-  cudaError_t e = upload(ctx->c_pub, pub, st);
-  if (e == cudaSuccess)
-    e = asim::launch_publish_states(ctx->last_params, ctx->c_end_src.as<uint32_t>(), ctx->last_u32,
-                                    ctx->c_pub.as<asim::PublishItem>(), (int32_t)pub.size(), out,
-                                    st, &ctx->launches);
-  return asim_cuda(ctx, e, "publish states");
+  for (int k = 0; k < kChunkSlots; ++k) {
+    if (pub[k].empty()) continue;
+    ChunkSlot& cs = ctx->slot[k];
+    cudaError_t e = upload(cs.pub, pub[k], st);
+    if (e == cudaSuccess)
+      e = asim::launch_publish_states(cs.last_params, cs.end_src.as<uint32_t>(), cs.last_u32,
+                                      cs.pub.as<asim::PublishItem>(), (int32_t)pub[k].size(), out,
+                                      st, &ctx->launches);
+    if (e != cudaSuccess) return asim_cuda(ctx, e, "publish states");
+  }
+  return ASIM_OK;
 }

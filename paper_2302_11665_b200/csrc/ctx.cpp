@@ -143,6 +143,7 @@ asim_status asim_ready(asim_ctx* ctx) {
 }
 
 asim_status asim_upload_batch(asim_ctx* ctx, const HostBatch& hb, cudaStream_t st) {
+  ++ctx->batch_gen;  // chunked runs of earlier batches can no longer publish
   cudaError_t e = upload(ctx->d_base_cfg, hb.base_cfg, st);
   if (e == cudaSuccess) e = upload(ctx->d_base_mask, hb.base_mask, st);
   if (e == cudaSuccess) e = upload(ctx->d_cand_base, hb.cand_base, st);
@@ -188,7 +189,9 @@ asim_status asim_run_batch(asim_ctx* ctx, const HostBatch& hb, int64_t begin, in
     }
     asim::DevOut o2 = out;
     o2.stage_updates = ctx->profiling ? ctx->d_counter.as<unsigned long long>() : nullptr;
-    asim_status s = asim_run_chunked(ctx, hb, begin, end, o2, st, opt);
+    asim_status s = (opt && opt->split && ctx->split_steps)
+                        ? asim_run_chunked_split(ctx, hb, begin, end, *opt->split, o2, st, opt)
+                        : asim_run_chunked(ctx, hb, begin, end, o2, st, opt);
     if (took_chunked) *took_chunked = s == ASIM_OK;
     if (ctx->profiling) {
       cudaEventRecord(ev1, st);
@@ -279,22 +282,31 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
   if (const char* gc = getenv("ASIM_GROUP_CANDIDATES")) ctx->group_cands = gc[0] != '0';
   if (const char* lw = getenv("ASIM_LANE_WALK")) ctx->lane_walk = lw[0] != '0';
+  if (const char* sp = getenv("ASIM_SPLIT")) ctx->split_steps = sp[0] != '0';
   {
     DeviceGuard dg(cuda_device);
-    e = cudaSuccess;
-    for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
-      e = cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming);
+    int lo = 0, hi = 0;  // stream priorities: `hi` is the most urgent
+    e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_split, cudaEventDisableTiming);
+    for (int k = 0; k < kChunkSlots && e == cudaSuccess; ++k) {
+      ChunkSlot& cs = ctx->slot[k];
+      const int prio = k == 0 ? hi : lo;  // slot 0 carries the walk-prone candidates
+      e = cudaStreamCreateWithPriority(&cs.main, cudaStreamNonBlocking, prio);
+      for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+        e = cudaStreamCreateWithPriority(&cs.side[i], cudaStreamNonBlocking, prio);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.ev_join[i], cudaEventDisableTiming);
+      }
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.ev_fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.ev_done, cudaEventDisableTiming);
+      for (int c = 0; c < asim::kLaneClassCount && e == cudaSuccess; ++c) {
+        e = cudaStreamCreateWithPriority(&cs.lane.streams[c], cudaStreamNonBlocking, prio);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.lane.done[c], cudaEventDisableTiming);
+      }
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.lane.listed, cudaEventDisableTiming);
+      cs.lane.fork = cs.ev_fork;
+      cs.lane.list_stream = cs.side[2];
+      cs.lane.join_stream = cs.side[2];
     }
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
-    for (int k = 0; k < asim::kLaneClassCount && e == cudaSuccess; ++k) {
-      e = cudaStreamCreateWithFlags(&ctx->lane.streams[k], cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->lane.done[k], cudaEventDisableTiming);
-    }
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->lane.listed, cudaEventDisableTiming);
-    ctx->lane.fork = ctx->ev_fork;
-    ctx->lane.list_stream = ctx->side[2];
-    ctx->lane.join_stream = ctx->side[2];
     if (e != cudaSuccess) {
       asim_destroy(ctx);
       return asim_fail(nullptr, ASIM_ECUDA, std::string("side streams: ") + cudaGetErrorString(e));
@@ -310,28 +322,32 @@ void asim_destroy(asim_ctx* ctx) {
   {
     DeviceGuard dg(ctx->device);
     DBuf* bufs[] = {&ctx->d_stage, &ctx->d_tail, &ctx->d_slo, &ctx->d_cfg_stages,
-                    &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc, &ctx->d_order, &ctx->d_mcum,
-                    &ctx->d_base_cfg, &ctx->d_base_mask,
-                    &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group,
-                    &ctx->d_cand_ok, &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm, &ctx->d_busy,
-                    &ctx->d_argmax, &ctx->d_counter, &ctx->d_walked, &ctx->c_items, &ctx->c_begin,
-                    &ctx->c_spec_good, &ctx->c_spec_sum, &ctx->c_fix_good, &ctx->c_fix_sum,
-                    &ctx->c_spec_end, &ctx->c_fix_end, &ctx->c_spec_epoch, &ctx->c_fix_epoch,
-                    &ctx->c_flag, &ctx->c_counter, &ctx->c_end_src, &ctx->d_cand_kmask,
-                    &ctx->d_cand_gmask, &ctx->c_pub, &ctx->c_perm, &ctx->c_item_cand, &ctx->c_lane_list, &ctx->c_lane_counts, &ctx->d_tmask, &ctx->c_spm, &ctx->c_fpm, &ctx->c_sbusy,
-                    &ctx->c_fbusy};
+                    &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc,
+                    &ctx->d_order, &ctx->d_mcum, &ctx->d_base_cfg, &ctx->d_base_mask,
+                    &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group, &ctx->d_cand_ok,
+                    &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm, &ctx->d_busy,
+                    &ctx->d_argmax, &ctx->d_counter, &ctx->d_cand_kmask, &ctx->d_cand_gmask,
+                    &ctx->d_tmask};
     for (DBuf* b : bufs) b->release();
     for (DBuf& b : ctx->spool) b.release();
-    for (int i = 0; i < 3; ++i) {
-      if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
-      if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);
+    auto sdestroy = [](cudaStream_t& x) { if (x) cudaStreamDestroy(x); x = nullptr; };
+    auto edestroy = [](cudaEvent_t& x) { if (x) cudaEventDestroy(x); x = nullptr; };
+    for (ChunkSlot& cs : ctx->slot) {
+      for (DBuf* b : cs.bufs()) b->release();
+      sdestroy(cs.main);
+      for (int i = 0; i < 3; ++i) {
+        sdestroy(cs.side[i]);
+        edestroy(cs.ev_join[i]);
+      }
+      edestroy(cs.ev_fork);
+      edestroy(cs.ev_done);
+      for (int c = 0; c < asim::kLaneClassCount; ++c) {
+        sdestroy(cs.lane.streams[c]);
+        edestroy(cs.lane.done[c]);
+      }
+      edestroy(cs.lane.listed);
     }
-    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    for (int k = 0; k < asim::kLaneClassCount; ++k) {
-      if (ctx->lane.streams[k]) cudaStreamDestroy(ctx->lane.streams[k]);
-      if (ctx->lane.done[k]) cudaEventDestroy(ctx->lane.done[k]);
-    }
-    if (ctx->lane.listed) cudaEventDestroy(ctx->lane.listed);
+    edestroy(ctx->ev_split);
   }
   delete ctx;
 }
@@ -361,7 +377,8 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   ctx->request_evals = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 32);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
+    for (ChunkSlot& cs : ctx->slot)
+      if (e == cudaSuccess) e = cudaMemset(cs.walked.p, 0, 32);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return asim_cuda(ctx, e, "reset stats");
   }
@@ -387,9 +404,11 @@ asim_status asim_set_profiling(asim_ctx* ctx, int32_t on) {
   DeviceGuard dg(ctx->device);
   if (on && !ctx->d_counter.p) {
     cudaError_t e = ctx->d_counter.ensure(32);
-    if (e == cudaSuccess) e = ctx->d_walked.ensure(32);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 32);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_walked.p, 0, 32);
+    for (ChunkSlot& cs : ctx->slot) {
+      if (e == cudaSuccess) e = cs.walked.ensure(32);
+      if (e == cudaSuccess) e = cudaMemset(cs.walked.p, 0, 32);
+    }
     if (e != cudaSuccess) return asim_cuda(ctx, e, "profiling counter");
   }
   ctx->profiling = on != 0;
@@ -424,7 +443,11 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   unsigned long long upd2[4] = {0, 0, 0, 0}, walked[4] = {0, 0, 0, 0};
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemcpy(upd2, ctx->d_counter.p, 32, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess) e = cudaMemcpy(walked, ctx->d_walked.p, 32, cudaMemcpyDeviceToHost);
+    for (ChunkSlot& cs : ctx->slot) {
+      unsigned long long w[4] = {0, 0, 0, 0};
+      if (e == cudaSuccess && cs.walked.p) e = cudaMemcpy(w, cs.walked.p, 32, cudaMemcpyDeviceToHost);
+      for (int i = 0; i < 4; ++i) walked[i] += w[i];
+    }
     if (e != cudaSuccess) return asim_cuda(ctx, e, "stats counter");
   }
   out->launches = ctx->launches;

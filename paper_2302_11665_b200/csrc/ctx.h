@@ -9,7 +9,8 @@
 #include "../../include/asim.h"
 #include "asim_internal.h"
 
-constexpr int kSearchPool = 12;  // device scratch buffers an asim_search borrows
+constexpr int kSearchPool = 13;  // device scratch buffers an asim_search borrows
+constexpr int kChunkSlots = 2;   // concurrent chunked runs of one step (see asim_ctx::slot)
 
 // Grow-only device buffer.
 struct DBuf {
@@ -33,6 +34,29 @@ struct DBuf {
   template <class T>
   T* as() const {
     return static_cast<T*>(p);
+  }
+};
+
+// One chunked run's device buffers, streams and bookkeeping (chunked.cpp).
+struct ChunkSlot {
+  DBuf items, begin, spec_good, spec_sum, fix_good, fix_sum, spec_end, fix_end, spec_epoch,
+      fix_epoch, flag, counter, end_src, pub, perm, item_cand, spm, fpm, sbusy, fbusy, lane_list,
+      lane_counts, walked;  // walked: unsigned long long statistics [4] (profiling)
+  cudaStream_t main = nullptr;  // the run's own stream (split steps)
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // concurrent walkers
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr}, ev_done = nullptr;
+  asim::LaneStreams lane{};  // item walker streams / events (one stream per class)
+  // the last run on this slot (its per-unit buffers stay valid until the next one)
+  bool last_valid = false;
+  bool last_u32 = false;
+  uint64_t last_gen = 0;  // batch generation it ran on
+  asim::ChunkParams last_params{};
+  std::vector<asim::ItemDesc> last_items;
+  std::vector<int32_t> last_pos;  // batch candidate -> item * 32 + lane (-1: not in the run)
+  std::vector<DBuf*> bufs() {
+    return {&items, &begin, &spec_good, &spec_sum, &fix_good, &fix_sum, &spec_end, &fix_end,
+            &spec_epoch, &fix_epoch, &flag, &counter, &end_src, &pub, &perm, &item_cand,
+            &spm, &fpm, &sbusy, &fbusy, &lane_list, &lane_counts, &walked};
   }
 };
 
@@ -82,29 +106,20 @@ struct asim_ctx {
   int64_t request_evals = 0;
   DBuf d_counter;  // unsigned long long stage-update counter of the kernels that count on
                    // the device (everything but pass 1; slots [1..3] unused)
-  DBuf d_walked;   // unsigned long long walked-chunk counter
 
   int sms = 148;
   DBuf spool[kSearchPool];  // search scratch kept across searches (search.cpp)
-  // side streams / events of the concurrent walk pass (created by asim_create)
-  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
-  DBuf c_lane_list, c_lane_counts;  // lane walker scratch (walk.cu)
-  asim::LaneStreams lane{};         // lane walker streams / events (one stream per class)
-  // chunked path buffers (chunked.cpp)
-  DBuf c_items, c_begin, c_spec_good, c_spec_sum, c_fix_good, c_fix_sum, c_spec_end, c_fix_end,
-      c_spec_epoch, c_fix_epoch, c_flag, c_counter, c_end_src;
+  // Chunked runs (chunked.cpp).  A search step may split its candidates into
+  // two runs on their own streams (slot 0: the candidates predicted to walk,
+  // high priority; slot 1: the rest) so that one run's sequential walks
+  // overlap the other's pass 1; each slot owns its buffers and streams.
+  ChunkSlot slot[kChunkSlots];
+  cudaEvent_t ev_split = nullptr;  // fork point of a split step on the caller's stream
+  uint64_t batch_gen = 0;          // incremented by every asim_upload_batch
   int32_t force_path = 0;  // 0 auto, 1 general kernel, 2 chunked kernel (tests)
-  // the last chunked run (its per-unit buffers stay valid until the next one)
-  bool last_valid = false;
-  bool last_u32 = false;
-  asim::ChunkParams last_params{};
-  std::vector<asim::ItemDesc> last_items;
-  std::vector<int32_t> last_pos;  // batch candidate -> item * 32 + lane (-1: not in the run)
-  DBuf c_pub, c_perm, c_item_cand;
-  DBuf c_spm, c_fpm, c_sbusy, c_fbusy;  // fast-heuristic statistics rows
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
+  bool split_steps = true;   // search steps run walk-prone candidates concurrently (ASIM_SPLIT=0: off)
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
   bool lane_walk = false;    // item walker for small uniform components (walk.cu; ASIM_LANE_WALK=1: on)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
@@ -175,6 +190,8 @@ struct ChunkOptions {
   const int32_t* spec_row = nullptr;     // [B] device
   const int64_t* spec_cand = nullptr;    // per-candidate rows (device), see ChunkParams
   int32_t state_stride = 0;
+  const std::vector<uint8_t>* split = nullptr;  // search steps: walk-prone group per candidate
+  uint8_t* walk_out = nullptr;  // device [C]: 1 = the candidate walked (launch_walk_flags)
 };
 bool asim_chunked_eligible(const asim_ctx* ctx, const HostBatch& hb, const asim::DevOut& out);
 // Fast heuristic statistics (good, sum, per-model good, per-group busy) of
@@ -186,6 +203,12 @@ asim_status asim_run_fast_stats(asim_ctx* ctx, const HostBatch& hb, const asim::
 asim_status asim_run_chunked(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
                              const asim::DevOut& out, cudaStream_t st,
                              const ChunkOptions* opt = nullptr);
+// As asim_run_chunked over the candidates of [begin, end) split by `group`
+// (batch-indexed, 0 or 1): two concurrent runs forked from and joined back
+// into `st` (slot 0: group 0 on a high-priority stream).  A group may be empty.
+asim_status asim_run_chunked_split(asim_ctx* ctx, const HostBatch& hb, int64_t begin, int64_t end,
+                                   const std::vector<uint8_t>& group, const asim::DevOut& out,
+                                   cudaStream_t st, const ChunkOptions* opt);
 // After a chunked run: true boundary states of chosen candidates of that run
 // (batch index c -> row of `out`, see publish_kernel).  Returns ASIM_ESTATE if
 // a candidate was not part of the last run.

@@ -102,6 +102,9 @@ struct Run {
   // batch index of (m, g) among the candidates simulated locally in the
   // previous / current step (-1: not simulated here)
   std::vector<int32_t> prev_idx, cur_idx;
+  // whether (m, g) walked (pass 2 left a chunk unmet) the last time it was
+  // simulated: such candidates run first, on their own stream (split steps)
+  std::vector<uint8_t> walk_prone;
 
   int32_t find(int32_t x) {
     while (parent[x] != x) x = parent[x] = parent[parent[x]];
@@ -179,6 +182,9 @@ struct asim_search {
   HostBatch hb;
   std::vector<int32_t> base_run;  // base -> run id
   std::vector<int64_t> cost;      // per candidate of the step: estimated simulation work
+  std::vector<uint8_t> split;     // per candidate: 0 = predicted to walk, 1 = not
+  DBuf d_walk;                    // per candidate: 1 = walked in this step's run
+  std::vector<uint8_t> h_walk;
   int64_t eval_lo = 0, eval_hi = 0;  // candidates of the last local evaluate call
   DBuf d_good_all;
   std::vector<int64_t> h_good;
@@ -424,7 +430,7 @@ static asim_status bucket_plan(asim_ctx* ctx, const asim_search_spec* spec, asim
 static void search_buffers(asim_search* s, DBuf* (&bufs)[kSearchPool]) {
   DBuf* b[kSearchPool] = {&s->d_good_all, &s->st_base, &s->st_next, &s->d_rows, &s->d_rows2,
                           &s->d_scratch, &s->cs_prev, &s->cs_cur, &s->spec_mix, &s->d_mixrows,
-                          &s->d_pm, &s->d_busy};
+                          &s->d_pm, &s->d_busy, &s->d_walk};
   for (int i = 0; i < kSearchPool; ++i) bufs[i] = b[i];
 }
 
@@ -540,6 +546,7 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
     r.memo_good.assign((size_t)hp.M * r.G, 0);
     r.memo_ok.assign((size_t)hp.M * r.G, 0);
     r.prev_idx.assign((size_t)hp.M * r.G, -1);
+    r.walk_prone.assign((size_t)hp.M * r.G, 0);
     r.cur_idx.assign((size_t)hp.M * r.G, -1);
     int64_t devices = 0;
     int32_t slots = 0;
@@ -621,6 +628,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
   hb.G = G;
   s->base_run.clear();
   s->cost.clear();
+  s->split.clear();
   s->eval_lo = s->eval_hi = 0;
   s->rows_uploaded = false;
   s->mixrows.clear();
@@ -656,6 +664,7 @@ asim_status asim_search_prepare(asim_search* s, int64_t* num_candidates) {
                                ? run.cn[c.r1] + (c.r2 != c.r1 ? run.cn[c.r2] : 0)
                                : s->ctx->n;
       s->cost.push_back(std::max<int64_t>(1, nreq) * hp.cfg_stages[run.cfg[c.g]]);
+      s->split.push_back(run.walk_prone[(size_t)c.m * run.G + c.g] ? 0 : 1);
       s->mixrows.push_back(asim::MixRow{r, prev});
     };
     if (run.round == 1) {  // the same step, second round: deferred candidates
@@ -794,6 +803,16 @@ asim_status asim_search_evaluate(asim_search* s, int64_t begin, int64_t end, int
     opt.spec_state = s->st_base.as<int64_t>();
     opt.spec_row = s->d_rows.as<int32_t>();
     popt = &opt;
+    // walk prediction: the candidates that walked when last simulated run
+    // first, concurrently with the others (asim_run_chunked_split)
+    opt.split = &s->split;
+    cudaError_t ew = s->d_walk.ensure((size_t)C + 8);
+    if (ew == cudaSuccess) ew = cudaMemsetAsync(s->d_walk.p, 0, (size_t)C, strm);
+    if (ew != cudaSuccess) {
+      if (prev >= 0 && prev != s->ctx->device) cudaSetDevice(prev);
+      return asim_cuda(s->ctx, ew, "walk flags");
+    }
+    opt.walk_out = s->d_walk.as<uint8_t>();
     // mixed speculation rows for [begin, end) (candidate memory of the last step)
     const size_t per = (size_t)s->J * s->stride * 8;
     if (s->have_prev && (size_t)C * per <= kMixBytesCap) {
@@ -1015,9 +1034,14 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
   if (C > 0 && !good_all_dev) return sfail(s, ASIM_EINVAL, "null good_all_dev");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   s->h_good.resize(C);
+  const bool walks = s->use_states && s->eval_hi > s->eval_lo;
+  if (walks) s->h_walk.resize(C);
   if (C > 0) {
     cudaError_t e =
         cudaMemcpyAsync(s->h_good.data(), good_all_dev, C * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && walks)
+      e = cudaMemcpyAsync(s->h_walk.data() + s->eval_lo, s->d_walk.as<uint8_t>() + s->eval_lo,
+                          (size_t)(s->eval_hi - s->eval_lo), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return asim_cuda(s->ctx, e, "copy step results");
   }
@@ -1030,6 +1054,8 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
       Run::Cand& c = run.cands[i];
       if (c.kind == 0) {
         c.good = s->h_good[c.ref];
+        if (walks && c.ref >= s->eval_lo && c.ref < s->eval_hi)
+          run.walk_prone[(size_t)c.m * run.G + c.g] = s->h_walk[c.ref];
         if (restricted)  // good(base) - good_base(comp(g)) - good_base(comp(m)) + good_c(K_c)
           c.good += run.base_good - run.cgood[c.r1] - (c.r2 != c.r1 ? run.cgood[c.r2] : 0);
       }

@@ -156,6 +156,7 @@ struct ChunkParams {
   int64_t stat_C;
   int32_t scalar_walk;  // 1 = small components walk with the register-state scalar walker
   int32_t lane_walk;    // 1 = small uniform components walk one candidate per lane (walk.cu)
+  int32_t transient;    // 1 = passes 1-2 launch one unit per warp, blocks retire (split steps)
   // per 32-request tile of the trace: bit m set if model m (< 64) occurs in it
   // (nullable; M <= 64 only) -- the lane walker skips tiles of other models
   const uint64_t* tile_mask;

@@ -45,6 +45,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "asim_internal.h"
 #include "chunk_common.cuh"
 #include "launch_cache.h"
@@ -1730,6 +1732,10 @@ cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
   int64_t blocks = 1;
   cudaError_t e = grid_for(chunk_kernel<T, MODE>, smem, P.num_units, sms, &blocks);
   if (e != cudaSuccess) return e;
+  // a split step's runs share the GPU: one unit per warp and blocks that
+  // retire, so the block scheduler interleaves the two runs by stream priority
+  // (persistent blocks would hold their SMs until their run's last unit)
+  if (P.transient) blocks = std::max<int64_t>(1, std::min<int64_t>((P.num_units + kWarps - 1) / kWarps, 0x7FFFFFFF));
   chunk_kernel<T, MODE><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P);
   return cudaGetLastError();
 }

@@ -220,7 +220,7 @@ static void pass1_work(asim_ctx* ctx, const HostBatch& hb,
 // stream-ordered on `st`.
 static asim_status run_slot(asim_ctx* ctx, ChunkSlot& cs, const HostBatch& hb,
                             std::vector<int32_t> ord, const asim::DevOut& out, cudaStream_t st,
-                            const ChunkOptions* opt) {
+                            const ChunkOptions* opt, bool transient = false) {
   const int64_t N = ctx->n;
   const HostProblem& hp = ctx->hp;
   // ---- work items: <= 32 consecutive candidates of one base
@@ -249,8 +249,13 @@ static asim_status run_slot(asim_ctx* ctx, ChunkSlot& cs, const HostBatch& hb,
   // Candidate order inside the range: the batch's, or grouped by hosting
   // component (hb.cand_key, the search's): a warp replays the union of its
   // lanes' requests, so lanes sharing their components keep every lane busy.
-  const bool grouped = !hb.cand_key.empty();
-  if (grouped)
+  const bool by_key = !hb.cand_key.empty();
+  // items list their candidates explicitly (item_cand) unless they are runs of
+  // consecutive batch indices: when regrouped, or when the run takes a subset
+  // of the range (a split step)
+  bool grouped = by_key;
+  for (size_t i = 1; i < ord.size() && !grouped; ++i) grouped = ord[i] != ord[i - 1] + 1;
+  if (by_key)
     std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
       if (hb.cand_base[a] != hb.cand_base[b]) return hb.cand_base[a] < hb.cand_base[b];
       return hb.cand_key[a] < hb.cand_key[b];
@@ -341,6 +346,7 @@ static asim_status run_slot(asim_ctx* ctx, ChunkSlot& cs, const HostBatch& hb,
   P.stage_updates = out.stage_updates;
   P.walked = ctx->profiling ? cs.walked.as<unsigned long long>() : nullptr;
   P.scalar_walk = ctx->scalar_walk ? 1 : 0;
+  P.transient = transient ? 1 : 0;
   // the lane walker: uint32 times, component-restricted batches (M <= 64), no
   // fast-heuristic statistics rows (set below)
   P.lane_walk = (ctx->lane_walk && u32 && !hb.cand_kmask.empty() && !hb.cand_gmask.empty() &&
@@ -486,7 +492,7 @@ asim_status asim_run_chunked_split(asim_ctx* ctx, const HostBatch& hb, int64_t b
     ChunkSlot& cs = ctx->slot[k];
     e = cudaStreamWaitEvent(cs.main, ctx->ev_split, 0);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "split fork");
-    asim_status rc = run_slot(ctx, cs, hb, std::move(ord[k]), out, cs.main, opt);
+    asim_status rc = run_slot(ctx, cs, hb, std::move(ord[k]), out, cs.main, opt, true);
     if (rc) return rc;
     e = cudaEventRecord(cs.ev_done, cs.main);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, cs.ev_done, 0);

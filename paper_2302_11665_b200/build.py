@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libasim.so")
-SOURCES = ["ctx.cpp", "search.cpp", "chunked.cpp", "sim.cu", "chunk.cu", "walk.cu", "batch.cu"]
+SOURCES = ["ctx.cpp", "search.cpp", "chunked.cpp", "sim.cu", "chunk.cu", "batch.cu"]
 HEADERS = ["asim_internal.h", "ctx.h", "launch_cache.h", "chunk_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

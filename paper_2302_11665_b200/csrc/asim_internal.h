@@ -155,11 +155,7 @@ struct ChunkParams {
   int64_t* fix_busy;
   int64_t stat_C;
   int32_t scalar_walk;  // 1 = small components walk with the register-state scalar walker
-  int32_t lane_walk;    // 1 = small uniform components walk one candidate per lane (walk.cu)
   int32_t transient;    // 1 = passes 1-2 launch one unit per warp, blocks retire (split steps)
-  // per 32-request tile of the trace: bit m set if model m (< 64) occurs in it
-  // (nullable; M <= 64 only) -- the lane walker skips tiles of other models
-  const uint64_t* tile_mask;
   int64_t walk_log;     // diagnostics (ASIM_WALK_LOG=cycles): printf every walk longer than this
 };
 
@@ -209,30 +205,13 @@ cudaError_t launch_fast_stats(const ChunkParams& P, const DevOut& out, bool u32,
 // end of chunk j is in spec_end (0) or fix_end (1).
 // The three walkers run concurrently: fork from `main` onto the side
 // streams, join back before returning (stream-ordered for the caller).
-struct LaneStreams;
 struct WalkStreams {
   cudaStream_t main;
-  cudaStream_t side[3];
-  cudaEvent_t fork, join[3];
-  int32_t* lane_list;     // lane walker scratch (see launch_lane_walk); nullable = off
-  uint32_t* lane_counts;
-  const LaneStreams* lane;
+  cudaStream_t side[2];
+  cudaEvent_t fork, join[2];
 };
 cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32, bool any_dynamic,
                               const WalkStreams& ws, int sms, int64_t* launches);
-// The lane walker (walk.cu, uint32 times only): after `fork` (on `main`),
-// lists the walking candidates of every lane class into `list`
-// ([kLaneClasses][num_items * 32] int32) with per-class counts in `counts`
-// ([kLaneClasses + 1], zeroed here) on list_stream, then walks each class on
-// its own stream, 32 candidates per warp; join_stream waits for all of them.
-constexpr int kLaneClassCount = 12;  // = kLaneClasses (chunk_common.cuh)
-struct LaneStreams {
-  cudaStream_t list_stream, join_stream;
-  cudaStream_t streams[kLaneClassCount];
-  cudaEvent_t fork, listed;
-  cudaEvent_t done[kLaneClassCount];
-};
-cudaError_t launch_lane_walk(const ChunkParams& P, uint32_t* end_src, int32_t* list,
-                             uint32_t* counts, const LaneStreams& ls, int sms, int64_t* launches);
+
 
 }  // namespace asim

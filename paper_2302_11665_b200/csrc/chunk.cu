@@ -860,10 +860,18 @@ __device__ __forceinline__ void coop_range(const ChunkParams& P, const WarpMem<T
                                            const uint64_t (&lastbit)[Q], int lane, int64_t& good,
                                            int64_t& sum, unsigned long long& upd,
                                            int32_t* pm_row, int64_t* busy_row) {
+  // the next tile's records load one tile ahead (the walk is one warp on a
+  // dependent chain: an L2 round trip per tile would sit on it)
+  int64_t al_n = i_begin + lane < i_end ? P.tr.arrival[i_begin + lane] : 0;
+  int ml_n = i_begin + lane < i_end ? (int)P.tr.model[i_begin + lane] : 0;
   for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
     const bool valid = i0 + lane < i_end;
-    const int64_t al = valid ? P.tr.arrival[i0 + lane] : 0;
-    const int ml = valid ? (int)P.tr.model[i0 + lane] : 0;
+    const int64_t al = valid ? al_n : 0;
+    const int ml = valid ? ml_n : 0;
+    if (i0 + 32 + lane < i_end) {
+      al_n = P.tr.arrival[i0 + 32 + lane];
+      ml_n = (int)P.tr.model[i0 + 32 + lane];
+    }
     unsigned todo = __ballot_sync(FULL, valid && ((kmask >> (ml & 63)) & 1ull));
     if (!todo) continue;
     bool per_req = false;
@@ -895,15 +903,31 @@ __device__ __forceinline__ void coop_range(const ChunkParams& P, const WarpMem<T
       const bool rel = (todo >> lane) & 1u;
       upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popcll(hml) : 0u) * S;
     }
-    while (todo) {
-      const int jj = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int m = __shfl_sync(FULL, ml, jj);
-      T ar = __shfl_sync(FULL, arl, jj);
-      const uint64_t hm = __shfl_sync(FULL, hml, jj);
-      const T tl = __shfl_sync(FULL, tll, jj), sl = __shfl_sync(FULL, sll, jj);
-      T dk = 0;
-      if constexpr (S == 1) dk = __shfl_sync(FULL, dkl, jj);
+    // software pipeline: the next request's shuffles issue before this
+    // request's dependent chain
+    int njj = __ffs(todo) - 1;
+    todo &= todo - 1;
+    int nm = __shfl_sync(FULL, ml, njj);
+    T nar = __shfl_sync(FULL, arl, njj);
+    uint64_t nhm = __shfl_sync(FULL, hml, njj);
+    T ntl = __shfl_sync(FULL, tll, njj), nsl = __shfl_sync(FULL, sll, njj), ndk = 0;
+    if constexpr (S == 1) ndk = __shfl_sync(FULL, dkl, njj);
+    for (;;) {
+      const int jj = njj, m = nm;
+      T ar = nar;
+      const uint64_t hm = nhm;
+      const T tl = ntl, sl = nsl, dk = ndk;
+      const bool more = todo != 0;
+      if (more) {
+        njj = __ffs(todo) - 1;
+        todo &= todo - 1;
+        nm = __shfl_sync(FULL, ml, njj);
+        nar = __shfl_sync(FULL, arl, njj);
+        nhm = __shfl_sync(FULL, hml, njj);
+        ntl = __shfl_sync(FULL, tll, njj);
+        nsl = __shfl_sync(FULL, sll, njj);
+        if constexpr (S == 1) ndk = __shfl_sync(FULL, dkl, njj);
+      }
       if constexpr (TT<T>::kRel) {
         if (per_req) {
           const int64_t a = __shfl_sync(FULL, al, jj);
@@ -942,30 +966,32 @@ __device__ __forceinline__ void coop_range(const ChunkParams& P, const WarpMem<T
         fl = tmin(fl, f[q]);
       }
       const T fmin = warp_min<T>(fl);
-      if (fmin == TT<T>::maxv() || (T)(fmin - ar) > sl) continue;  // no host / misses the SLO
-      // lowest group index among the minima (slots ascend with q, then lane)
-      int wq = 0, wl = 0;
+      if (fmin != TT<T>::maxv() && (T)(fmin - ar) <= sl) {  // else no host / misses the SLO
+        // lowest group index among the minima (slots ascend with q, then lane)
+        int wq = 0, wl = 0;
 #pragma unroll
-      for (int q = Q - 1; q >= 0; --q) {
-        const unsigned b = __ballot_sync(FULL, f[q] == fmin);
-        if (b) {
-          wq = q;
-          wl = __ffs(b) - 1;
+        for (int q = Q - 1; q >= 0; --q) {
+          const unsigned b = __ballot_sync(FULL, f[q] == fmin);
+          if (b) {
+            wq = q;
+            wl = __ffs(b) - 1;
+          }
+        }
+        const int gw = (wl + 32 * wq) / S;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (q == wq && (lane + 32 * q) / S == gw) v[q] = y[q];
+        ++good;
+        sum += (int64_t)(fmin - ar);
+        if constexpr (STATS) {
+          const int64_t occ = __shfl_sync(FULL, occl, jj);
+          if (lane == 0) {
+            atomicAdd(pm_row + m, 1);
+            atomicAdd(reinterpret_cast<unsigned long long*>(busy_row + gw), (unsigned long long)occ);
+          }
         }
       }
-      const int gw = (wl + 32 * wq) / S;
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
-        if (q == wq && (lane + 32 * q) / S == gw) v[q] = y[q];
-      ++good;
-      sum += (int64_t)(fmin - ar);
-      if constexpr (STATS) {
-        const int64_t occ = __shfl_sync(FULL, occl, jj);
-        if (lane == 0) {
-          atomicAdd(pm_row + m, 1);
-          atomicAdd(reinterpret_cast<unsigned long long*>(busy_row + gw), (unsigned long long)occ);
-        }
-      }
+      if (!more) break;
     }
   }
 }
@@ -1505,7 +1531,6 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     const int item = u >> 5, cl = u & 31;
     const ItemDesc it = P.items[item];
     if (it.S == 0 || cl >= it.count || !P.bt.cand_ok[cand_of(P, it, item, cl)]) continue;
-    if (lane_class(P, it, cand_of(P, it, item, cl)) >= 0) continue;  // the lane walker's
     const bool fits = P.scalar_walk && scalar_fits(P, it, cand_of(P, it, item, cl));
     if (fits != SCALAR) continue;  // the other walker's candidate
     // any chunk of this candidate flagged by pass 2?  (else nothing to walk)
@@ -1751,7 +1776,7 @@ cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, const WalkStr
   int64_t blocks = 1;
   cudaError_t e = cudaMemsetAsync(P.counter, 0, 3 * sizeof(uint32_t), ws.main);
   if (e != cudaSuccess) return e;
-  const bool fork = P.scalar_walk || any_dynamic || (P.lane_walk && ws.lane_list && ws.lane);
+  const bool fork = P.scalar_walk || any_dynamic;
   if (fork && (e = cudaEventRecord(ws.fork, ws.main)) != cudaSuccess) return e;
   e = grid_for(coop_walk_kernel<T, false>, smem, (int64_t)P.num_items * 32, sms, &blocks);
   if (e != cudaSuccess) return e;
@@ -1767,13 +1792,6 @@ cudaError_t launch_walk_t(const ChunkParams& P, uint32_t* end_src, const WalkStr
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaEventRecord(ws.join[0], ws.side[0])) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(ws.main, ws.join[0], 0)) != cudaSuccess) return e;
-  }
-  if (P.lane_walk && ws.lane_list && ws.lane) {
-    int64_t dummy = 0;
-    e = launch_lane_walk(P, end_src, ws.lane_list, ws.lane_counts, *ws.lane, sms, &dummy);
-    if (e != cudaSuccess) return e;
-    if ((e = cudaEventRecord(ws.join[2], ws.side[2])) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(ws.main, ws.join[2], 0)) != cudaSuccess) return e;
   }
   if (any_dynamic) {
     ChunkParams Q = P;
@@ -1810,8 +1828,7 @@ cudaError_t launch_chunk_walk(const ChunkParams& P, uint32_t* end_src, bool u32,
   if (e != cudaSuccess) return e;
   e = u32 ? launch_walk_t<uint32_t>(P, end_src, ws, sms, any_dynamic)
           : launch_walk_t<int64_t>(P, end_src, ws, sms, any_dynamic);
-  if (launches)
-    *launches += 1 + (any_dynamic ? 1 : 0) + (P.scalar_walk ? 1 : 0) + (P.lane_walk ? 1 + kLaneClasses : 0);
+  if (launches) *launches += 1 + (any_dynamic ? 1 : 0) + (P.scalar_walk ? 1 : 0);
   return e;
 }
 

@@ -347,11 +347,6 @@ static asim_status run_slot(asim_ctx* ctx, ChunkSlot& cs, const HostBatch& hb,
   P.walked = ctx->profiling ? cs.walked.as<unsigned long long>() : nullptr;
   P.scalar_walk = ctx->scalar_walk ? 1 : 0;
   P.transient = transient ? 1 : 0;
-  // the lane walker: uint32 times, component-restricted batches (M <= 64), no
-  // fast-heuristic statistics rows (set below)
-  P.lane_walk = (ctx->lane_walk && u32 && !hb.cand_kmask.empty() && !hb.cand_gmask.empty() &&
-                 out.good_per_model == nullptr && out.busy == nullptr) ? 1 : 0;
-  P.tile_mask = ctx->has_tmask ? ctx->d_tmask.as<uint64_t>() : nullptr;
   P.walk_log = ctx->walk_log;
   P.spec_state = opt ? opt->spec_state : nullptr;
   P.spec_row = opt ? opt->spec_row : nullptr;
@@ -431,17 +426,8 @@ static asim_status run_slot(asim_ctx* ctx, ChunkSlot& cs, const HostBatch& hb,
       if (e != cudaSuccess) return asim_cuda(ctx, e, "walk flags");
     }
     // ---- pass 3: walk the chunks whose start state was wrong (exact chains)
-    asim::WalkStreams ws{st, {cs.side[0], cs.side[1], cs.side[2]}, cs.ev_fork,
-                         {cs.ev_join[0], cs.ev_join[1], cs.ev_join[2]}, nullptr, nullptr,
-                         nullptr};
-    if (P.lane_walk) {
-      e = cs.lane_list.ensure((size_t)asim::kLaneClassCount * I * 2 * 4 + 8);
-      if (e == cudaSuccess) e = cs.lane_counts.ensure(64 * 4);
-      if (e != cudaSuccess) return asim_cuda(ctx, e, "lane walker buffers");
-      ws.lane_list = cs.lane_list.as<int32_t>();
-      ws.lane_counts = cs.lane_counts.as<uint32_t>();
-      ws.lane = &cs.lane;
-    }
+    const asim::WalkStreams ws{st, {cs.side[0], cs.side[1]}, cs.ev_fork,
+                               {cs.ev_join[0], cs.ev_join[1]}};
     {
       PhaseTimer t(ctx, 2, st, P.stage_updates != nullptr);
       e = asim::launch_chunk_walk(P, end_src, u32, any_dynamic, ws, ctx->sms, &ctx->launches);

@@ -281,7 +281,6 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   if (const char* sw = getenv("ASIM_SCALAR_WALK")) ctx->scalar_walk = sw[0] != '0';
   if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
   if (const char* gc = getenv("ASIM_GROUP_CANDIDATES")) ctx->group_cands = gc[0] != '0';
-  if (const char* lw = getenv("ASIM_LANE_WALK")) ctx->lane_walk = lw[0] != '0';
   if (const char* sp = getenv("ASIM_SPLIT")) ctx->split_steps = sp[0] != '0';
   {
     DeviceGuard dg(cuda_device);
@@ -292,20 +291,12 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
       ChunkSlot& cs = ctx->slot[k];
       const int prio = k == 0 ? hi : lo;  // slot 0 carries the walk-prone candidates
       e = cudaStreamCreateWithPriority(&cs.main, cudaStreamNonBlocking, prio);
-      for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+      for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaStreamCreateWithPriority(&cs.side[i], cudaStreamNonBlocking, prio);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.ev_join[i], cudaEventDisableTiming);
       }
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.ev_fork, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.ev_done, cudaEventDisableTiming);
-      for (int c = 0; c < asim::kLaneClassCount && e == cudaSuccess; ++c) {
-        e = cudaStreamCreateWithPriority(&cs.lane.streams[c], cudaStreamNonBlocking, prio);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.lane.done[c], cudaEventDisableTiming);
-      }
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cs.lane.listed, cudaEventDisableTiming);
-      cs.lane.fork = cs.ev_fork;
-      cs.lane.list_stream = cs.side[2];
-      cs.lane.join_stream = cs.side[2];
     }
     if (e != cudaSuccess) {
       asim_destroy(ctx);
@@ -326,8 +317,7 @@ void asim_destroy(asim_ctx* ctx) {
                     &ctx->d_order, &ctx->d_mcum, &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group, &ctx->d_cand_ok,
                     &ctx->d_items, &ctx->d_good, &ctx->d_sum, &ctx->d_pm, &ctx->d_busy,
-                    &ctx->d_argmax, &ctx->d_counter, &ctx->d_cand_kmask, &ctx->d_cand_gmask,
-                    &ctx->d_tmask};
+                    &ctx->d_argmax, &ctx->d_counter, &ctx->d_cand_kmask, &ctx->d_cand_gmask};
     for (DBuf* b : bufs) b->release();
     for (DBuf& b : ctx->spool) b.release();
     auto sdestroy = [](cudaStream_t& x) { if (x) cudaStreamDestroy(x); x = nullptr; };
@@ -335,17 +325,12 @@ void asim_destroy(asim_ctx* ctx) {
     for (ChunkSlot& cs : ctx->slot) {
       for (DBuf* b : cs.bufs()) b->release();
       sdestroy(cs.main);
-      for (int i = 0; i < 3; ++i) {
+      for (int i = 0; i < 2; ++i) {
         sdestroy(cs.side[i]);
         edestroy(cs.ev_join[i]);
       }
       edestroy(cs.ev_fork);
       edestroy(cs.ev_done);
-      for (int c = 0; c < asim::kLaneClassCount; ++c) {
-        sdestroy(cs.lane.streams[c]);
-        edestroy(cs.lane.done[c]);
-      }
-      edestroy(cs.lane.listed);
     }
     edestroy(ctx->ev_split);
   }
@@ -594,17 +579,6 @@ asim_status asim_set_trace(asim_ctx* ctx, int64_t n, const int64_t* arrival_ns,
   if (e == cudaSuccess) e = upload(ctx->d_model, mp, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload trace");
-  // per 32-request tile, the models occurring in it (lane walker tile skips;
-  // model ids fit a 64-bit mask only when M <= 64)
-  ctx->has_tmask = false;
-  if (ctx->hp.M <= 64) {
-    std::vector<uint64_t> tm(npad / 32, 0);
-    for (int64_t i = 0; i < n; ++i) tm[i >> 5] |= 1ull << m[i];
-    e = upload(ctx->d_tmask, tm, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return asim_cuda(ctx, e, "upload tile masks");
-    ctx->has_tmask = true;
-  }
   ctx->n = n;
   ctx->max_arrival = n ? a[n - 1] : 0;
   ctx->min_arrival = n ? a[0] : 0;

@@ -40,12 +40,11 @@ struct DBuf {
 // One chunked run's device buffers, streams and bookkeeping (chunked.cpp).
 struct ChunkSlot {
   DBuf items, begin, spec_good, spec_sum, fix_good, fix_sum, spec_end, fix_end, spec_epoch,
-      fix_epoch, flag, counter, end_src, pub, perm, item_cand, spm, fpm, sbusy, fbusy, lane_list,
-      lane_counts, walked;  // walked: unsigned long long statistics [4] (profiling)
+      fix_epoch, flag, counter, end_src, pub, perm, item_cand, spm, fpm, sbusy, fbusy,
+      walked;  // walked: unsigned long long statistics [4] (profiling)
   cudaStream_t main = nullptr;  // the run's own stream (split steps)
-  cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // concurrent walkers
-  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr}, ev_done = nullptr;
-  asim::LaneStreams lane{};  // item walker streams / events (one stream per class)
+  cudaStream_t side[2] = {nullptr, nullptr};  // concurrent walkers
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr}, ev_done = nullptr;
   // the last run on this slot (its per-unit buffers stay valid until the next one)
   bool last_valid = false;
   bool last_u32 = false;
@@ -56,7 +55,7 @@ struct ChunkSlot {
   std::vector<DBuf*> bufs() {
     return {&items, &begin, &spec_good, &spec_sum, &fix_good, &fix_sum, &spec_end, &fix_end,
             &spec_epoch, &fix_epoch, &flag, &counter, &end_src, &pub, &perm, &item_cand,
-            &spm, &fpm, &sbusy, &fbusy, &lane_list, &lane_counts, &walked};
+            &spm, &fpm, &sbusy, &fbusy, &walked};
   }
 };
 
@@ -91,8 +90,6 @@ struct asim_ctx {
   DBuf d_inc;           // batching stage increments (asim_evaluate_batching)
   DBuf d_order;         // batching launch order (costliest candidates first)
   DBuf d_mcum;          // per-model running arrival sums (batching)
-  DBuf d_tmask;         // per 32-request tile: models present (M <= 64)
-  bool has_tmask = false;
 
   // statistics (asim_set_profiling)
   bool profiling = false;
@@ -119,9 +116,8 @@ struct asim_ctx {
   int32_t force_path = 0;  // 0 auto, 1 general kernel, 2 chunked kernel (tests)
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
-  bool split_steps = true;   // search steps run walk-prone candidates concurrently (ASIM_SPLIT=0: off)
+  bool split_steps = false;  // search steps run walk-prone candidates concurrently (ASIM_SPLIT=1: on)
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
-  bool lane_walk = false;    // item walker for small uniform components (walk.cu; ASIM_LANE_WALK=1: on)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
 
   // scratch for evaluate()

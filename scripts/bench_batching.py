@@ -9,9 +9,14 @@ one asim_evaluate_batching call over C seeded random feasible placements of
 every S1 parallel config (inputs resident in HBM), including the argmax.
 
 Prints one JSON line like bench.py: value = C x N / device time, roofline of
-the batching kernel (stage updates vs the ALU roof, same basis as bench.py),
-e2e through the public API from pinned host buffers, and the CPU oracle
-(oracle.evaluate_batching, as it stands) on a bounded sample.
+the batching kernel against warp-instruction ISSUE (4 per SM per clock: with
+one candidate per warp a request step is a sequence of warp-wide
+instructions, so issue is the binding roof), with the measured
+warp instructions per (request, candidate) evaluation I_eval from ncu
+(`--ieval`, or the JSON file written by the ncu launch-list pass:
+smsp__inst_executed.sum / (C x N)); e2e through the public API from host
+buffers; and the CPU oracle (oracle.evaluate_batching, as it stands) on a
+bounded sample.
 """
 
 from __future__ import annotations
@@ -65,6 +70,8 @@ def main():
     ap.add_argument("--slo-scale", type=float, default=5.0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ieval", default=os.path.join(ROOT, "profiles", "r2d", "batching_ieval.json"),
+                    help="JSON with the ncu-measured warp instructions per evaluation")
     args = ap.parse_args()
 
     import torch
@@ -168,8 +175,15 @@ def main():
         pass
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    peak = sms * 64 * sm_max * 1e6 / 1e9
-    achieved = st["stage_updates"] / max(st["sim_ms"], 1e-9) / 1e6
+    # issue roof: 4 warp instructions per SM per clock
+    peak = 4 * sms * sm_max * 1e6 / 1e9  # G warp-instructions/s
+    ieval = None
+    try:
+        ieval = float(json.load(open(args.ieval))["inst_per_eval"])
+    except (OSError, KeyError, ValueError):
+        pass
+    k_evals = feasible * N * args.steps  # (request, candidate) evaluations by the kernel
+    achieved = (k_evals * ieval / (st["sim_ms"] / 1e3) / 1e9) if ieval else None
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["S1-batching"] / 1e9
@@ -186,13 +200,16 @@ def main():
                     best_attainment=float(good.max()) / max(N, 1),
                     l2="flushed between timed steps (256 MB write)"),
         gpu_launches=int(launches),
-        roofline=dict(bound="alu", achieved=achieved, peak=peak, unit="G stage-updates/s",
-                      frac=achieved / peak, traffic=traffic,
+        roofline=dict(bound="issue", achieved=achieved, peak=peak, unit="G warp-instructions/s",
+                      frac=(achieved / peak) if achieved else None, traffic=traffic,
+                      inst_per_eval=ieval, ieval_source=os.path.relpath(args.ieval, ROOT),
                       traffic_unit="GB DRAM per launch (ncu --set full, profiles/traffic.json)",
                       kernel="batching_kernel",
                       kernel_ms=st["sim_ms"], stage_updates=st["stage_updates"],
                       kernel_ms_share=st["sim_ms"] / max(total_ms, 1e-9),
-                      peak_basis="148 SMs x 64 int max/clk x 1965 MHz (MEASURED_PEAKS sm_max_mhz)"),
+                      stage_updates_per_s=st["stage_updates"] / max(st["sim_ms"], 1e-9) * 1e3,
+                      peak_basis=f"{sms} SMs x 4 warp-instructions/clk x {sm_max:.0f} MHz "
+                                 "(MEASURED_PEAKS sm_max_mhz)"),
         clocks=clk.summary(), e2e=e2e, cpu_baseline=cpu)
     print(json.dumps(line), flush=True)
     sim.close()

@@ -282,6 +282,7 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
   if (const char* gc = getenv("ASIM_GROUP_CANDIDATES")) ctx->group_cands = gc[0] != '0';
   if (const char* sp = getenv("ASIM_SPLIT")) ctx->split_steps = sp[0] != '0';
+  if (const char* mc = getenv("ASIM_MAX_CHUNKS")) ctx->max_chunks = std::max(1ll, atoll(mc));
   {
     DeviceGuard dg(cuda_device);
     int lo = 0, hi = 0;  // stream priorities: `hi` is the most urgent

@@ -572,7 +572,8 @@ asim_status asim_search_create(asim_ctx* ctx, const asim_search_spec* spec, asim
   s->gub.assign(s->ngroups, 0);
   if (s->prune)
     for (int32_t gi = 0; gi < s->ngroups; ++gi) s->gub[gi] = run_capacity_bound(ctx, group_run(s, gi));
-  s->J = std::max<int64_t>(1, std::min<int64_t>(1024, ctx->n / std::max<int64_t>(1, ctx->min_chunk)));
+  s->J = std::max<int64_t>(
+      1, std::min<int64_t>(ctx->max_chunks, ctx->n / std::max<int64_t>(1, ctx->min_chunk)));
   {
     HostBatch probe_hb;
     probe_hb.slots = stride;

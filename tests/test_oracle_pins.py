@@ -346,3 +346,62 @@ def test_p12bc_burstiness_and_skew_direction():
     assert 1.15 < r1 < 1.45
     assert r3 > r1 + 0.3
     assert rs > 3.0
+
+
+def test_feasibility_branches_hand_cases():
+    """Feasibility (reading C11; Alg. 1 "if sel' is in memory constraint",
+    P:711), every branch worked by hand: a 2-device cluster with a 10-byte
+    budget per device; config 0 = (1,1) on 1 device, config 1 = (2,1) on 2.
+    Per-device bytes: model 0: 6 / 3, model 1: not placeable (-1) / 4,
+    model 2: 5 / 3."""
+    from oracle import feasible
+
+    prob = tiny_problem([(1, 1), (2, 1)], stage=[[[5], [2, 3]]] * 3,
+                        mem=[[6, 3], [-1, 4], [5, 3]], num_devices=2, budget=10)
+    M = prob.num_models
+    cases = [
+        ([0, 0], [[0], [0]], True),       # 2 devices, 6 <= 10 on each
+        ([0, 0], [[0, 2], []], False),    # 6 + 5 = 11 > 10: memory
+        ([0, 0], [[2], [0]], True),       # 5 and 6
+        ([0], [[1]], False),              # (model 1, (1,1)) not placeable
+        ([1], [[0, 1, 2]], True),         # 3 + 4 + 3 = 10 <= 10 on both devices
+        ([1, 1], [[0], []], False),       # 4 devices > 2 (an empty group still holds its devices)
+        ([0, 0, 0], [[0], [], []], False),  # 3 devices > 2
+        ([1], [[]], True),                # nothing placed
+    ]
+    tr = trace_of([(0, 0), (1, 1), (2, 2)])
+    for cfg, groups, want in cases:
+        pl = place(cfg, groups, M)
+        assert feasible(prob, pl) == want, (cfg, groups)
+        g, _, _ = oracle.evaluate(prob, tr, np.array([cfg], np.int32),
+                                  pl.host_mask[None, :], threads=1)
+        assert (g[0] >= 0) == want and (want or g[0] == -1)
+
+
+def test_greedy_ties_and_strict_best_hand_case():
+    """Alg. 1's ties and best updates (reading C12), worked by
+    hand.  Two (1,1) groups with memory for one model each; models A = 0 and
+    B = 1 identical (10 ns, no deadline).  Trace A@0, B@100: every hosted
+    request is good.
+      step 1: (A,g0) (A,g1) (B,g0) (B,g1) all give 1 -> the first, (A,g0);
+      step 2: g0 is full; (A,g1) gives 1 (a useless replica), (B,g1) gives 2
+              -> (B,g1); no feasible addition is left.
+    The lowest-index bijection A->g0, B->g1 with best good 2.  Without B's
+    request the step-2 tie (A,g1) = (B,g1) = 1 goes to (A,g1) (m-major
+    order), and the best stays step 1's selection: 1 is not > 1."""
+    from oracle import search as osearch
+
+    prob = tiny_problem([(1, 1)], stage=[[[10]], [[10]]], mem=[[6], [6]], num_devices=2,
+                        budget=10)
+    res = osearch.greedy(prob, trace_of([(0, 0), (100, 1)]), [0, 0], record=True)
+    steps = res["steps"]
+    assert [c for c, _, _ in steps] == [[(0, 0), (0, 1), (1, 0), (1, 1)], [(0, 1), (1, 1)]]
+    assert [list(g) for _, g, _ in steps] == [[1, 1, 1, 1], [1, 2]]
+    assert [i for _, _, i in steps] == [0, 1]
+    assert res["good"] == 2 and res["placement"].host_mask.tolist() == [1, 2]
+
+    res = osearch.greedy(prob, trace_of([(0, 0)]), [0, 0], record=True)
+    steps = res["steps"]
+    assert [list(g) for _, g, _ in steps] == [[1, 1, 0, 0], [1, 1]]
+    assert [steps[k][0][i] for k, (_, _, i) in enumerate(steps)] == [(0, 0), (0, 1)]
+    assert res["good"] == 1 and res["placement"].host_mask.tolist() == [1, 0]

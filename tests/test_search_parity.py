@@ -196,3 +196,47 @@ def test_search_more_than_64_models(sim):
             _compare(sim, prob, tr, dedup_modes=(False,))
         finally:
             sim.set_chunk_size(4096)
+
+
+def test_greedy_hand_case_ties_and_strict_best(sim):
+    """The GPU search on the hand-worked case of
+    test_oracle_pins.test_greedy_ties_and_strict_best_hand_case."""
+    from tests.helpers import tiny_problem, trace_of
+
+    prob = tiny_problem([(1, 1)], stage=[[[10]], [[10]]], mem=[[6], [6]], num_devices=2,
+                        budget=10)
+    for pairs, hist, best, mask in (([(0, 0), (100, 1)], [(0, 0, 1), (1, 1, 2)], 2, [1, 2]),
+                                    ([(0, 0)], [(0, 0, 1), (0, 1, 1)], 1, [1, 0])):
+        tr = trace_of(pairs)
+        sim.set_problem(prob)
+        sim.set_trace(tr.arrival_ns, tr.model)
+        with sim.search_handle(runs=[[0, 0]], dedup=False, prune=False) as h:
+            h.run()
+            m, g, v = h.history(0)
+            assert list(zip(m.tolist(), g.tolist(), v.tolist())) == hist
+            res = h.result()
+        assert res.best_good == best and res.host_mask.tolist() == mask
+
+
+def test_feasibility_hand_cases_gpu(sim):
+    """Infeasible placements are data (good = -1), every branch of reading C11
+    as in test_oracle_pins.test_feasibility_branches_hand_cases."""
+    from tests.helpers import place, tiny_problem, trace_of
+
+    prob = tiny_problem([(1, 1), (2, 1)], stage=[[[5], [2, 3]]] * 3,
+                        mem=[[6, 3], [-1, 4], [5, 3]], num_devices=2, budget=10)
+    cases = [([0, 0], [[0], [0]], True), ([0, 0], [[0, 2], []], False),
+             ([0, 0], [[2], [0]], True), ([0, -1], [[1], []], False),
+             ([1, -1], [[0, 1, 2], []], True), ([1, 1], [[0], []], False)]
+    tr = trace_of([(0, 0), (1, 1), (2, 2)])
+    sim.set_problem(prob)
+    sim.set_trace(tr.arrival_ns, tr.model)
+    cfg = np.full((len(cases), 3), -1, np.int32)
+    mask = np.zeros((len(cases), 3), np.uint64)
+    for i, (c, groups, _) in enumerate(cases):
+        pl = place([x for x in c if x >= 0], [gm for x, gm in zip(c, groups) if x >= 0], 3)
+        cfg[i, :pl.num_groups] = pl.group_cfg
+        mask[i] = pl.host_mask
+    got = sim.evaluate(cfg, mask)["good"]
+    assert [(x >= 0) for x in got] == [w for _, _, w in cases]
+    assert all(x == -1 for x, (_, _, w) in zip(got, cases) if not w)

@@ -120,8 +120,9 @@ asim_status asim_reset_stats(asim_ctx* ctx);
  * Results are identical for every choice. */
 asim_status asim_set_path(asim_ctx* ctx, int32_t path);
 /* Minimum time-chunk length in requests for the chunked kernel (default
- * 4096; small values exercise the fix-up in tests).  Results do not depend
- * on it. */
+ * 4096; small values exercise the fix-up in tests).  A search uses
+ * min(256, n / min_requests) chunks (environment ASIM_MAX_CHUNKS overrides the
+ * cap).  Results do not depend on either. */
 asim_status asim_set_chunk_size(asim_ctx* ctx, int64_t min_requests);
 
 /* ---------------------------------------------------------------- problem */

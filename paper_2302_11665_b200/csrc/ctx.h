@@ -115,7 +115,7 @@ struct asim_ctx {
   uint64_t batch_gen = 0;          // incremented by every asim_upload_batch
   int32_t force_path = 0;  // 0 auto, 1 general kernel, 2 chunked kernel (tests)
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
-  int64_t max_chunks = 1024; // time chunks of a search (ASIM_MAX_CHUNKS; results do not depend on it)
+  int64_t max_chunks = 256;  // time chunks of a search (ASIM_MAX_CHUNKS; results do not depend on it)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
   bool split_steps = false;  // search steps run walk-prone candidates concurrently (ASIM_SPLIT=1: on)
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)

@@ -109,6 +109,10 @@ typedef struct {
   int64_t spec_lane_slots;      /* pass 1: requests processed by its warps x 32 lanes */
   int64_t spec_live_lanes;      /* pass 1: (request, lane) pairs whose candidate simulates the
                                    request (live); live / slots = lane utilisation */
+  int64_t walk_predicted;       /* search steps: simulated candidates that walked and had walked
+                                   when last simulated (run first, split steps) */
+  int64_t walk_unpredicted;     /* ... that walked but had not */
+  int64_t walk_mispredicted;    /* ... that had walked but did not now */
 } asim_stats;
 asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
 asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);

@@ -52,7 +52,8 @@ class asim_stats(ctypes.Structure):
                 ("walk_candidates", i64), ("walk_critical_chunks", i64),
                 ("spec_ms", ctypes.c_double), ("spec_stage_updates", i64),
                 ("pass2_ms", ctypes.c_double), ("walk_ms", ctypes.c_double),
-                ("spec_lane_slots", i64), ("spec_live_lanes", i64)]
+                ("spec_lane_slots", i64), ("spec_live_lanes", i64),
+                ("walk_predicted", i64), ("walk_unpredicted", i64), ("walk_mispredicted", i64)]
 
 
 class asim_search_spec(ctypes.Structure):

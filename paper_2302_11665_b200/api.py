@@ -137,7 +137,8 @@ class Simulator:
                     walk_critical_chunks=s.walk_critical_chunks, spec_ms=s.spec_ms,
                     spec_stage_updates=s.spec_stage_updates, pass2_ms=s.pass2_ms,
                     walk_ms=s.walk_ms, spec_lane_slots=s.spec_lane_slots,
-                    spec_live_lanes=s.spec_live_lanes)
+                    spec_live_lanes=s.spec_live_lanes, walk_predicted=s.walk_predicted,
+                    walk_unpredicted=s.walk_unpredicted, walk_mispredicted=s.walk_mispredicted)
 
     def set_chunk_size(self, min_requests: int) -> None:
         self._check(A.asim_set_chunk_size(self.h, int(min_requests)))

@@ -360,6 +360,7 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   ctx->sim_ms = 0.0;
   for (double& x : ctx->phase_ms) x = 0.0;
   ctx->p1_updates = ctx->p1_live = ctx->p1_slots = 0;
+  for (int64_t& x : ctx->walk_pred) x = 0;
   ctx->request_evals = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 32);
@@ -446,6 +447,9 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->walk_ms = ctx->phase_ms[2];
   out->spec_lane_slots = ctx->p1_slots;
   out->spec_live_lanes = ctx->p1_live;
+  out->walk_predicted = ctx->walk_pred[0];
+  out->walk_unpredicted = ctx->walk_pred[1];
+  out->walk_mispredicted = ctx->walk_pred[2];
   out->request_evals = ctx->request_evals;
   out->chunk_reruns = (int64_t)walked[0];
   out->walk_candidates = (int64_t)walked[1];

@@ -98,6 +98,7 @@ struct asim_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_events[3];
   double phase_ms[3] = {0.0, 0.0, 0.0};
   int64_t p1_updates = 0, p1_live = 0, p1_slots = 0;  // pass-1 work (host-counted, profiling)
+  int64_t walk_pred[4] = {0, 0, 0, 0};  // split-step walk prediction: hit, miss, false, neither
   int64_t sim_launches = 0;
   double sim_ms = 0.0;
   int64_t request_evals = 0;
@@ -117,7 +118,7 @@ struct asim_ctx {
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
   int64_t max_chunks = 256;  // time chunks of a search (ASIM_MAX_CHUNKS; results do not depend on it)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
-  bool split_steps = false;  // search steps run walk-prone candidates concurrently (ASIM_SPLIT=1: on)
+  bool split_steps = true;   // search steps run walk-prone candidates concurrently (ASIM_SPLIT=0: off)
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
 

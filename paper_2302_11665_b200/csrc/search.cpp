@@ -1055,8 +1055,14 @@ asim_status asim_search_apply(asim_search* s, const int64_t* good_all_dev, void*
       Run::Cand& c = run.cands[i];
       if (c.kind == 0) {
         c.good = s->h_good[c.ref];
-        if (walks && c.ref >= s->eval_lo && c.ref < s->eval_hi)
-          run.walk_prone[(size_t)c.m * run.G + c.g] = s->h_walk[c.ref];
+        if (walks && c.ref >= s->eval_lo && c.ref < s->eval_hi) {
+          uint8_t& wp = run.walk_prone[(size_t)c.m * run.G + c.g];
+          const uint8_t w = s->h_walk[c.ref];
+          // statistics of the walk prediction (split steps): walked & predicted,
+          // walked & not predicted, predicted & not walked
+          s->ctx->walk_pred[w && wp ? 0 : w ? 1 : wp ? 2 : 3] += 1;
+          wp = w;
+        }
         if (restricted)  // good(base) - good_base(comp(g)) - good_base(comp(m)) + good_c(K_c)
           c.good += run.base_good - run.cgood[c.r1] - (c.r2 != c.r1 ? run.cgood[c.r2] : 0);
       }

@@ -329,9 +329,11 @@ def main():
         # min/max pipe issues 16 lanes/clk per SMSP -> 64 updates/clk/SM.
         peak = sms * 64 * sm_max * 1e6 / 1e9  # G stage-updates/s
         # dominant kernel: the chunked path's pass 1 (chunk_kernel SPEC), timed
-        # by its own CUDA events on the search stream, its own work counter
+        # by its own CUDA events on the stream it is launched on; split steps
+        # run two chunked runs concurrently, so its time is the union of its
+        # launches' [start, end] intervals (busy time), not their sum
         spec = st["spec_ms"] > 0
-        k_ms = st["spec_ms"] if spec else st["sim_ms"]
+        k_ms = st["spec_busy_ms"] if spec else st["sim_ms"]
         k_upd = st["spec_stage_updates"] if spec else st["stage_updates"]
         achieved = k_upd / max(k_ms, 1e-9) / 1e6  # G stage-updates/s
         traffic = None
@@ -373,7 +375,11 @@ def main():
                           kernel_ms_share=k_ms / max(total_ms, 1e-9),
                           kernel_ms=k_ms, kernel_stage_updates=k_upd,
                           all_sim_ms_share=st["sim_ms"] / max(total_ms, 1e-9),
-                          pass2_ms=st["pass2_ms"], walk_ms=st["walk_ms"],
+                          kernel_ms_summed=st["spec_ms"],
+                          pass2_ms=st["pass2_busy_ms"], walk_ms=st["walk_busy_ms"],
+                          pass1_class_share={c: round(x / max(1, sum(st["spec_class_cycles"])), 4)
+                                             for c, x in zip(("mixed", "S1", "S2", "S4", "S8",
+                                                              "S16"), st["spec_class_cycles"])},
                           walk_critical_chunks=st["walk_critical_chunks"],
                           walk_candidates=st["walk_candidates"],
                           walked_chunks=st["chunk_reruns"],

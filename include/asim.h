@@ -113,6 +113,15 @@ typedef struct {
                                    when last simulated (run first, split steps) */
   int64_t walk_unpredicted;     /* ... that walked but had not */
   int64_t walk_mispredicted;    /* ... that had walked but did not now */
+  /* pass 1 per stage class (index 0: mixed configs, 1..5: S = 1, 2, 4, 8, 16):
+   * warp cycles spent in its units (clock64), stage updates, lane slots */
+  int64_t spec_class_cycles[6];
+  int64_t spec_class_updates[6];
+  int64_t spec_class_slots[6];
+  /* busy time of each phase = length of the union of its launches' intervals
+   * (ms): split steps run two chunked runs concurrently, so the summed
+   * spec_ms / pass2_ms / walk_ms can exceed the wall time */
+  double spec_busy_ms, pass2_busy_ms, walk_busy_ms;
 } asim_stats;
 asim_status asim_set_profiling(asim_ctx* ctx, int32_t on);
 asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out);

@@ -53,7 +53,10 @@ class asim_stats(ctypes.Structure):
                 ("spec_ms", ctypes.c_double), ("spec_stage_updates", i64),
                 ("pass2_ms", ctypes.c_double), ("walk_ms", ctypes.c_double),
                 ("spec_lane_slots", i64), ("spec_live_lanes", i64),
-                ("walk_predicted", i64), ("walk_unpredicted", i64), ("walk_mispredicted", i64)]
+                ("walk_predicted", i64), ("walk_unpredicted", i64), ("walk_mispredicted", i64),
+                ("spec_class_cycles", i64 * 6), ("spec_class_updates", i64 * 6),
+                ("spec_class_slots", i64 * 6), ("spec_busy_ms", ctypes.c_double),
+                ("pass2_busy_ms", ctypes.c_double), ("walk_busy_ms", ctypes.c_double)]
 
 
 class asim_search_spec(ctypes.Structure):

@@ -138,7 +138,11 @@ class Simulator:
                     spec_stage_updates=s.spec_stage_updates, pass2_ms=s.pass2_ms,
                     walk_ms=s.walk_ms, spec_lane_slots=s.spec_lane_slots,
                     spec_live_lanes=s.spec_live_lanes, walk_predicted=s.walk_predicted,
-                    walk_unpredicted=s.walk_unpredicted, walk_mispredicted=s.walk_mispredicted)
+                    walk_unpredicted=s.walk_unpredicted, walk_mispredicted=s.walk_mispredicted,
+                    spec_class_cycles=list(s.spec_class_cycles),
+                    spec_class_updates=list(s.spec_class_updates),
+                    spec_class_slots=list(s.spec_class_slots), spec_busy_ms=s.spec_busy_ms,
+                    pass2_busy_ms=s.pass2_busy_ms, walk_busy_ms=s.walk_busy_ms)
 
     def set_chunk_size(self, min_requests: int) -> None:
         self._check(A.asim_set_chunk_size(self.h, int(min_requests)))

@@ -772,12 +772,17 @@ __global__ void __launch_bounds__(kWarps * 32) chunk_kernel(ChunkParams P) {
       item = P.item_perm[P.class_off[c] + local % P.class_items[c]];
     }
     const ItemDesc it = P.items[item];
+    const long long t0 = (MODE == SPEC && P.walked) ? clock64() : 0;
     if (it.base != cur_base) {
       load_base<T>(P, it, w, lane);
       cur_base = it.base;
     }
     dispatch_unit<T, MODE>(P, w, it, item, j, lane, 0);
     __syncwarp();
+    if (MODE == SPEC && P.walked && lane == 0) {  // profiling: warp cycles per stage class
+      const int cls = it.S == 1 ? 1 : it.S == 2 ? 2 : it.S == 4 ? 3 : it.S == 8 ? 4 : it.S == 16 ? 5 : 0;
+      atomicAdd(P.walked + 4 + cls, (unsigned long long)(clock64() - t0));
+    }
   }
 }
 

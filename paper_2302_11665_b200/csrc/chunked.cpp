@@ -179,6 +179,7 @@ static void pass1_work(asim_ctx* ctx, const HostBatch& hb,
   for (size_t i = 0; i < items.size(); ++i) {
     const asim::ItemDesc& it = items[i];
     const int32_t b = it.base;
+    const unsigned long long upd_i = upd, slots_i = slots;
     for (int32_t m = 0; m < M; ++m) {
       const uint64_t mk = hb.base_mask[(size_t)b * M + m];
       int64_t x = 0;
@@ -210,6 +211,9 @@ static void pass1_work(asim_ctx* ctx, const HostBatch& hb,
     for (int32_t m = 0; m < M; ++m)
       if (rel[m]) u += ctx->model_n[m];
     slots += 32ull * (unsigned long long)u;
+    const int cls = it.S == 1 ? 1 : it.S == 2 ? 2 : it.S == 4 ? 3 : it.S == 8 ? 4 : it.S == 16 ? 5 : 0;
+    ctx->p1_class[cls][0] += (int64_t)(upd - upd_i);
+    ctx->p1_class[cls][1] += (int64_t)(slots - slots_i);
   }
   ctx->p1_updates += (int64_t)upd;
   ctx->p1_live += (int64_t)live;

@@ -334,6 +334,7 @@ void asim_destroy(asim_ctx* ctx) {
       edestroy(cs.ev_done);
     }
     edestroy(ctx->ev_split);
+    edestroy(ctx->ev_ref);
   }
   delete ctx;
 }
@@ -343,6 +344,32 @@ const char* asim_last_error(const asim_ctx* ctx) {
 }
 
 int64_t asim_launch_count(const asim_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// Reference event for the phase intervals: recorded, then the device drained,
+// so every later event's elapsed time from it is >= 0.
+static cudaError_t record_ref(asim_ctx* ctx) {
+  cudaError_t e = ctx->ev_ref ? cudaSuccess : cudaEventCreate(&ctx->ev_ref);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_ref, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e;
+}
+
+// Length of the union of intervals (ms).
+static double union_ms(std::vector<std::pair<double, double>> iv) {
+  std::sort(iv.begin(), iv.end());
+  double total = 0.0, a = 0.0, b = -1.0;
+  for (const auto& x : iv) {
+    if (x.first > b) {
+      if (b > a) total += b - a;
+      a = x.first;
+      b = x.second;
+    } else if (x.second > b) {
+      b = x.second;
+    }
+  }
+  if (b > a) total += b - a;
+  return total;
+}
 
 asim_status asim_reset_stats(asim_ctx* ctx) {
   if (!ctx) return ASIM_EINVAL;
@@ -359,14 +386,16 @@ asim_status asim_reset_stats(asim_ctx* ctx) {
   ctx->sim_launches = 0;
   ctx->sim_ms = 0.0;
   for (double& x : ctx->phase_ms) x = 0.0;
+  for (auto& v : ctx->phase_iv) v.clear();
   ctx->p1_updates = ctx->p1_live = ctx->p1_slots = 0;
+  for (auto& r : ctx->p1_class) r[0] = r[1] = 0;
   for (int64_t& x : ctx->walk_pred) x = 0;
   ctx->request_evals = 0;
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemset(ctx->d_counter.p, 0, 32);
     for (ChunkSlot& cs : ctx->slot)
-      if (e == cudaSuccess) e = cudaMemset(cs.walked.p, 0, 32);
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e == cudaSuccess) e = cudaMemset(cs.walked.p, 0, kWalkedBytes);
+    if (e == cudaSuccess) e = record_ref(ctx);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "reset stats");
   }
   return ASIM_OK;
@@ -393,9 +422,10 @@ asim_status asim_set_profiling(asim_ctx* ctx, int32_t on) {
     cudaError_t e = ctx->d_counter.ensure(32);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_counter.p, 0, 32);
     for (ChunkSlot& cs : ctx->slot) {
-      if (e == cudaSuccess) e = cs.walked.ensure(32);
-      if (e == cudaSuccess) e = cudaMemset(cs.walked.p, 0, 32);
+      if (e == cudaSuccess) e = cs.walked.ensure(kWalkedBytes);
+      if (e == cudaSuccess) e = cudaMemset(cs.walked.p, 0, kWalkedBytes);
     }
+    if (e == cudaSuccess) e = record_ref(ctx);
     if (e != cudaSuccess) return asim_cuda(ctx, e, "profiling counter");
   }
   ctx->profiling = on != 0;
@@ -422,18 +452,24 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
       if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev.first, ev.second);
       if (e != cudaSuccess) return asim_cuda(ctx, e, "stats events");
       ctx->phase_ms[ph] += ms;
+      float t0 = 0.f, t1 = 0.f;
+      if (ctx->ev_ref && cudaEventElapsedTime(&t0, ctx->ev_ref, ev.first) == cudaSuccess &&
+          cudaEventElapsedTime(&t1, ctx->ev_ref, ev.second) == cudaSuccess)
+        ctx->phase_iv[ph].emplace_back(t0, t1);
       cudaEventDestroy(ev.first);
       cudaEventDestroy(ev.second);
     }
     ctx->phase_events[ph].clear();
   }
-  unsigned long long upd2[4] = {0, 0, 0, 0}, walked[4] = {0, 0, 0, 0};
+  constexpr int kW = kWalkedBytes / 8;
+  unsigned long long upd2[4] = {0, 0, 0, 0}, walked[kW] = {};
   if (ctx->d_counter.p) {
     cudaError_t e = cudaMemcpy(upd2, ctx->d_counter.p, 32, cudaMemcpyDeviceToHost);
     for (ChunkSlot& cs : ctx->slot) {
-      unsigned long long w[4] = {0, 0, 0, 0};
-      if (e == cudaSuccess && cs.walked.p) e = cudaMemcpy(w, cs.walked.p, 32, cudaMemcpyDeviceToHost);
-      for (int i = 0; i < 4; ++i) walked[i] += w[i];
+      unsigned long long w[kW] = {};
+      if (e == cudaSuccess && cs.walked.p)
+        e = cudaMemcpy(w, cs.walked.p, kWalkedBytes, cudaMemcpyDeviceToHost);
+      for (int i = 0; i < kW; ++i) walked[i] += w[i];
     }
     if (e != cudaSuccess) return asim_cuda(ctx, e, "stats counter");
   }
@@ -445,6 +481,9 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->spec_ms = ctx->phase_ms[0];
   out->pass2_ms = ctx->phase_ms[1];
   out->walk_ms = ctx->phase_ms[2];
+  out->spec_busy_ms = union_ms(ctx->phase_iv[0]);
+  out->pass2_busy_ms = union_ms(ctx->phase_iv[1]);
+  out->walk_busy_ms = union_ms(ctx->phase_iv[2]);
   out->spec_lane_slots = ctx->p1_slots;
   out->spec_live_lanes = ctx->p1_live;
   out->walk_predicted = ctx->walk_pred[0];
@@ -454,6 +493,11 @@ asim_status asim_get_stats(asim_ctx* ctx, asim_stats* out) {
   out->chunk_reruns = (int64_t)walked[0];
   out->walk_candidates = (int64_t)walked[1];
   out->walk_critical_chunks = (int64_t)walked[3];
+  for (int i = 0; i < 6; ++i) {
+    out->spec_class_cycles[i] = (int64_t)walked[4 + i];
+    out->spec_class_updates[i] = ctx->p1_class[i][0];
+    out->spec_class_slots[i] = ctx->p1_class[i][1];
+  }
   return ASIM_OK;
 }
 

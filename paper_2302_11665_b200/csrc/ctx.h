@@ -37,11 +37,14 @@ struct DBuf {
   }
 };
 
+constexpr int kWalkedBytes = 16 * 8;  // ChunkSlot::walked
+
 // One chunked run's device buffers, streams and bookkeeping (chunked.cpp).
 struct ChunkSlot {
   DBuf items, begin, spec_good, spec_sum, fix_good, fix_sum, spec_end, fix_end, spec_epoch,
       fix_epoch, flag, counter, end_src, pub, perm, item_cand, spm, fpm, sbusy, fbusy,
-      walked;  // walked: unsigned long long statistics [4] (profiling)
+      walked;  // walked: unsigned long long statistics [kWalkedBytes / 8] (profiling):
+               // [0..3] walk statistics, [4..9] pass-1 warp cycles per stage class
   cudaStream_t main = nullptr;  // the run's own stream (split steps)
   cudaStream_t side[2] = {nullptr, nullptr};  // concurrent walkers
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr}, ev_done = nullptr;
@@ -98,6 +101,11 @@ struct asim_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_events[3];
   double phase_ms[3] = {0.0, 0.0, 0.0};
   int64_t p1_updates = 0, p1_live = 0, p1_slots = 0;  // pass-1 work (host-counted, profiling)
+  int64_t p1_class[6][2] = {};
+  // phase intervals [start, end] in ms after ev_ref (profiling): with split
+  // steps two runs' phases overlap, so busy time is the union of intervals
+  cudaEvent_t ev_ref = nullptr;
+  std::vector<std::pair<double, double>> phase_iv[3];  // per stage class (dynamic, 1, 2, 4, 8, 16): stage updates, lane slots
   int64_t walk_pred[4] = {0, 0, 0, 0};  // split-step walk prediction: hit, miss, false, neither
   int64_t sim_launches = 0;
   double sim_ms = 0.0;

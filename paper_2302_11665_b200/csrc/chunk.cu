@@ -355,6 +355,138 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
   }
 }
 
+// Uniform-config request fields of model m arriving at ar (relative time),
+// computed once per request (lane-parallel per tile in run_unit):
+//   lim  the request is accepted iff v <= lim, where v = the winner's last
+//        departure (S > 1) or max(free, ar) (S == 1): the finish v + tail
+//        [+ d0] must satisfy finish - ar <= slo (C2, C3); saturated at maxv - 1
+//   cc   latency = v + cc, i.e. cc = tail - ar [+ d0] modulo 2^bits(T) (the
+//        latency itself is < 2^bits: uint32 times are chosen only then)
+//   d0   the first stage latency (S == 1)
+//   hA, hB  byte offsets of the first four hosts' first stage slots (16 bits each)
+//   h0c  hosting-list start | host count << 16 | never-acceptable << 23
+template <typename T, int S>
+__device__ __forceinline__ void uniform_fields(const WarpMem<T>& w, int m, T ar, T& lim, T& cc,
+                                               T& d0, int& hA, int& hB, int& h0c) {
+  const int h0 = w.hoff[m];
+  const int cnt = w.hoff[m + 1] - h0;
+  hA = (cnt >= 1 ? (int)w.hid[h0] : 0) | (cnt >= 2 ? (int)w.hid[h0 + 1] << 16 : 0);
+  hB = (cnt >= 3 ? (int)w.hid[h0 + 2] : 0) | (cnt >= 4 ? (int)w.hid[h0 + 3] << 16 : 0);
+  const T sl = w.slo[m], tl = w.tail[m];
+  d0 = S == 1 ? w.d[m * kSTab] : (T)0;
+  bool ok = sl >= tl;
+  T l = 0;
+  if (ok) {
+    const T room = sl - tl;
+    l = room > (T)(TT<T>::maxv() - 1 - ar) ? (T)(TT<T>::maxv() - 1) : (T)(ar + room);
+  }
+  if constexpr (S == 1) {  // v = max(free, ar); the departure is v + d0
+    ok = ok && l >= d0;
+    l = ok ? (T)(l - d0) : (T)0;
+  }
+  lim = l;
+  cc = (T)(tl + d0 - ar);
+  h0c = h0 | (cnt << 16) | (ok ? 0 : 1 << 23);
+}
+
+// Stage latencies d[0..S) of one model (row of the per-warp table, 16-byte
+// aligned): vector shared-memory loads.
+template <typename T, int S>
+__device__ __forceinline__ void load_dv(const T* row, T* dv) {
+  if constexpr (sizeof(T) == 4 && S >= 4) {
+#pragma unroll
+    for (int q = 0; q < S / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(row)[q];
+      dv[4 * q] = (T)v.x;
+      dv[4 * q + 1] = (T)v.y;
+      dv[4 * q + 2] = (T)v.z;
+      dv[4 * q + 3] = (T)v.w;
+    }
+  } else if constexpr (S >= 2) {
+#pragma unroll
+    for (int q = 0; q < S * (int)sizeof(T) / 8; ++q) {
+      const uint2 v = reinterpret_cast<const uint2*>(row)[q];
+      if constexpr (sizeof(T) == 4) {
+        dv[2 * q] = (T)v.x;
+        dv[2 * q + 1] = (T)v.y;
+      } else {
+        dv[q] = (T)(((unsigned long long)v.y << 32) | v.x);
+      }
+    }
+  } else {
+    dv[0] = row[0];
+  }
+}
+
+// One request on one trajectory of a uniform-config unit (S > 0): dispatch to
+// the earliest predicted finish among the base's hosts and this lane's added
+// replica (lowest group index on ties, C1), admission at receipt (C2, C3),
+// commit.  Hosts are byte offsets in ascending group order; the first four
+// come packed in hA / hB, further ones from the hosting list.  Returns whether
+// the request is accepted; v = the compared value (see uniform_fields), bo =
+// byte offset of the chosen group's first slot.
+template <typename T, int S>
+__device__ __forceinline__ bool step_u(const WarpMem<T>& w, T* st, int lane, int hA, int hB,
+                                       int h0c, bool mine, int my_off, bool live, T ar,
+                                       const T* dv, T lim, T& v, int& bo) {
+  constexpr int kStride = 32 * (int)sizeof(T);  // bytes between a group's stages
+  const char* stl = reinterpret_cast<const char*>(st + lane);
+  auto pred = [&](int off) -> T {
+    if constexpr (S == 1) {
+      return tmax(*reinterpret_cast<const T*>(stl + off), ar);
+    } else {
+      T x = ar;
+#pragma unroll
+      for (int k = 0; k < S; ++k) x = tmax(x, *reinterpret_cast<const T*>(stl + off + k * kStride)) + dv[k];
+      return x;
+    }
+  };
+  T best = TT<T>::maxv();
+  int b = 0x7FFFFFFF;
+  auto host = [&](int off) {
+    const T x = pred(off);
+    const bool lt = x < best;  // strict: the lowest index wins ties (C1)
+    best = lt ? x : best;
+    b = lt ? off : b;
+  };
+  const int cnt = (h0c >> 16) & 0x7F;
+  if (cnt >= 1) {
+    host(hA & 0xFFFF);
+    if (cnt >= 2) host((int)((unsigned)hA >> 16));
+    if (cnt >= 3) {
+      host(hB & 0xFFFF);
+      if (cnt >= 4) host((int)((unsigned)hB >> 16));
+      const int hs = h0c & 0xFFFF;
+      for (int h = hs + 4; h < hs + cnt; ++h) host(w.hid[h]);
+    }
+  }
+  if (mine) {  // this lane's added replica; ties resolved by group index
+    const T x = pred(my_off);
+    if (x < best || (x == best && my_off < b)) {
+      best = x;
+      b = my_off;
+    }
+  }
+  v = best;
+  bo = b;
+  const bool acc = live && b != 0x7FFFFFFF && best <= lim;
+  if (acc) {
+    char* stw = reinterpret_cast<char*>(st + lane);
+    if constexpr (S == 1) {
+      *reinterpret_cast<T*>(stw + b) = best + dv[0];
+    } else {
+      T x = ar;
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        T* p = reinterpret_cast<T*>(stw + b + k * kStride);
+        x = tmax(x, *p) + dv[k];
+        *p = x;
+      }
+    }
+  }
+  return acc;
+}
+
 // Stage occupancy sum_k d_k of model m on group g (fast-heuristic busy time).
 template <typename T, int S>
 __device__ __forceinline__ int64_t occupancy(const ChunkParams& P, const WarpMem<T>& w, int g,
@@ -474,6 +606,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
   const int my_m = in_item ? P.bt.cand_model[c] : -1;
   const int my_g = in_item ? P.bt.cand_group[c] : 0;
   const bool active = in_item && P.bt.cand_ok[c];
+  const int my_off = my_g * (S > 0 ? S : 1) * 32 * (int)sizeof(T);  // S > 0: byte offset of its first slot
   const int slots = it.slots;
   const int M = P.pr.M;
   const int64_t slot_id = (int64_t)item * 32 + lane;
@@ -581,6 +714,74 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
         per_req = a_last - E > P.theta;  // a sparse tile: fall back to per-request epochs
       }
     }
+    if constexpr (S > 0) {
+      // Uniform config (every group runs the run's config): per-request fields
+      // computed lane-parallel once per tile, then broadcast by shuffles.
+      //   lim  accept iff the winner's last departure (S > 1) / max(v, a)
+      //        (S == 1) is <= lim  (= a + slo - tail [- d0], saturated)
+      //   cc   latency = that value + cc  (tail - a [+ d0], mod 2^bits of T)
+      //   hA, hB  byte offsets of the first four hosts' first stage slots
+      //   h0c  list start | count << 16 | never-acceptable << 23
+      const T ar_l = (T)(ai - E);
+      T lim_l, cc_l, d0_l;
+      int hA_l, hB_l, h0c_l;
+      uniform_fields<T, S>(w, mi, ar_l, lim_l, cc_l, d0_l, hA_l, hB_l, h0c_l);
+      while (todo) {
+        const int jj = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int cm = __shfl_sync(FULL, mi, jj);
+        T car = __shfl_sync(FULL, ar_l, jj);
+        T lim = __shfl_sync(FULL, lim_l, jj);
+        T cc = __shfl_sync(FULL, cc_l, jj);
+        int hA = __shfl_sync(FULL, hA_l, jj), hB = __shfl_sync(FULL, hB_l, jj);
+        int h0c = __shfl_sync(FULL, h0c_l, jj);
+        if constexpr (S == 1) {
+          dv[0] = __shfl_sync(FULL, d0_l, jj);
+        } else {
+          load_dv<T, S>(w.d + cm * kSTab, dv);
+        }
+        if constexpr (TT<T>::kRel) {
+          if (per_req) {  // sparse tile: per-request epochs, fields recomputed (rare)
+            const int64_t a = __shfl_sync(FULL, ai, jj);
+            maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
+            car = (T)(a - E);
+            T d0x;
+            uniform_fields<T, S>(w, cm, car, lim, cc, d0x, hA, hB, h0c);
+          }
+        }
+        const bool live = active && ((kmask >> (cm & 63)) & 1ull) && !(h0c & (1 << 23));
+        const bool mine = live && cm == my_m;
+        T v0;
+        int bo0;
+        if (step_u<T, S>(w, w.st0, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v0, bo0)) {
+          ++good0;
+          sum0 += (int64_t)(T)(v0 + cc);
+          if (P.spec_pm) {  // SPEC: pass-1 counts; DUAL: the true side of the correction
+            const int g0 = bo0 / (S * 32 * (int)sizeof(T));
+            if constexpr (MODE == SPEC)
+              stat_add(P.spec_pm, P.spec_busy, P, j, c, cm, g0, occupancy<T, S>(P, w, g0, cm, dv), 1);
+            else
+              stat_add(P.fix_pm, P.fix_busy, P, j, c, cm, g0, occupancy<T, S>(P, w, g0, cm, dv), 1);
+          }
+        }
+        if (active) upd32 += (uint32_t)((h0c >> 16) & 0x7F) + (mine ? 1u : 0u);
+        if constexpr (MODE == DUAL) {
+          T v1;
+          int bo1;
+          if (step_u<T, S>(w, w.st1, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v1, bo1)) {
+            ++good1;
+            sum1 += (int64_t)(T)(v1 + cc);
+            if (P.spec_pm) {  // minus the speculative side
+              const int g1 = bo1 / (S * 32 * (int)sizeof(T));
+              stat_add(P.fix_pm, P.fix_busy, P, j, c, cm, g1, occupancy<T, S>(P, w, g1, cm, dv), -1);
+            }
+          }
+          if (active) upd32 += (uint32_t)((h0c >> 16) & 0x7F) + (mine ? 1u : 0u);
+        }
+      }
+      continue;
+    }
+
     // lane-parallel per-request fields, broadcast below by independent shuffles
     const T ar_l = (T)(ai - E);
     const int h0_l = w.hoff[mi];

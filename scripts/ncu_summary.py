@@ -29,6 +29,11 @@ METRICS = [
     ("DRAM read", "dram__bytes_read.sum"),
     ("DRAM write", "dram__bytes_write.sum"),
     ("L2 bytes", "lts__t_bytes.sum"),
+    ("L2 hit rate", "lts__t_sector_hit_rate.pct"),
+    ("L1 hit rate", "l1tex__t_sector_hit_rate.pct"),
+    ("Issue slots busy", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
+    ("Warp instructions executed", "smsp__inst_executed.sum"),
+    ("Achieved occupancy", "sm__warps_active.avg.per_cycle_active"),
 ]
 STALLS = ["wait", "selected", "short_scoreboard", "long_scoreboard", "branch_resolving",
           "no_instructions", "not_selected", "math_pipe_throttle", "mio_throttle", "barrier"]

@@ -155,6 +155,7 @@ struct ChunkParams {
   int64_t* fix_busy;
   int64_t stat_C;
   int32_t scalar_walk;  // 1 = small components walk with the register-state scalar walker
+  int32_t glane_walk;   // > 0: components of S <= 2 and glane_walk..32 groups take the group-lane walker
   int32_t transient;    // 1 = passes 1-2 launch one unit per warp, blocks retire (split steps)
   int64_t walk_log;     // diagnostics (ASIM_WALK_LOG=cycles): printf every walk longer than this
 };

@@ -355,6 +355,22 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
   }
 }
 
+// Position of the r-th (0-based) set bit of x (r < popc(x); else garbage):
+// a 5-step popcount select.
+__device__ __forceinline__ int nth_set_bit(unsigned x, int r) {
+  int p = 0;
+#pragma unroll
+  for (int wd = 16; wd; wd >>= 1) {
+    const int cnt = __popc(x & ((1u << wd) - 1u));
+    if (r >= cnt) {
+      r -= cnt;
+      x >>= wd;
+      p += wd;
+    }
+  }
+  return p;
+}
+
 // Uniform-config request fields of model m arriving at ar (relative time),
 // computed once per request (lane-parallel per tile in run_unit):
 //   lim  the request is accepted iff v <= lim, where v = the winner's last
@@ -726,23 +742,32 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       T lim_l, cc_l, d0_l;
       int hA_l, hB_l, h0c_l;
       uniform_fields<T, S>(w, mi, ar_l, lim_l, cc_l, d0_l, hA_l, hB_l, h0c_l);
-      while (todo) {
-        const int jj = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int cm = __shfl_sync(FULL, mi, jj);
-        T car = __shfl_sync(FULL, ar_l, jj);
-        T lim = __shfl_sync(FULL, lim_l, jj);
-        T cc = __shfl_sync(FULL, cc_l, jj);
-        int hA = __shfl_sync(FULL, hA_l, jj), hB = __shfl_sync(FULL, hB_l, jj);
-        int h0c = __shfl_sync(FULL, h0c_l, jj);
+      // compaction: lane k gathers the fields of the tile's k-th relevant
+      // request (src = the k-th set bit of todo, by a 5-step popcount select),
+      // so the per-request loop below broadcasts from lane k with a plain
+      // counter -- no find-first-set on its loop-carried chain
+      const int nreq = __popc(todo);
+      const int src = nth_set_bit(todo, lane);
+      const int mi_c = __shfl_sync(FULL, mi, src);
+      const T ar_c = __shfl_sync(FULL, ar_l, src), lim_c = __shfl_sync(FULL, lim_l, src);
+      const T cc_c = __shfl_sync(FULL, cc_l, src), d0_c = __shfl_sync(FULL, d0_l, src);
+      const int hA_c = __shfl_sync(FULL, hA_l, src), hB_c = __shfl_sync(FULL, hB_l, src);
+      const int h0c_c = __shfl_sync(FULL, h0c_l, src);
+      for (int k = 0; k < nreq; ++k) {
+        const int cm = __shfl_sync(FULL, mi_c, k);
+        T car = __shfl_sync(FULL, ar_c, k);
+        T lim = __shfl_sync(FULL, lim_c, k);
+        T cc = __shfl_sync(FULL, cc_c, k);
+        int hA = __shfl_sync(FULL, hA_c, k), hB = __shfl_sync(FULL, hB_c, k);
+        int h0c = __shfl_sync(FULL, h0c_c, k);
         if constexpr (S == 1) {
-          dv[0] = __shfl_sync(FULL, d0_l, jj);
+          dv[0] = __shfl_sync(FULL, d0_c, k);
         } else {
           load_dv<T, S>(w.d + cm * kSTab, dv);
         }
         if constexpr (TT<T>::kRel) {
           if (per_req) {  // sparse tile: per-request epochs, fields recomputed (rare)
-            const int64_t a = __shfl_sync(FULL, ai, jj);
+            const int64_t a = __shfl_sync(FULL, ai, __shfl_sync(FULL, src, k));
             maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
             car = (T)(a - E);
             T d0x;
@@ -1436,19 +1461,20 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
         upd += (unsigned long long)__reduce_add_sync(FULL, rel ? (unsigned)__popc(hml) : 0u) * S;
       }
       if (!per_req && !pm_row) {
-        // Dense tile: all 32 requests in a fixed order.  Each lane stages its
-        // request's fields in shared memory; the per-request loop reads them
-        // with broadcast loads that do not depend on the state, so they issue
-        // ahead of the dependent chain.  A request outside the component has
-        // no host here (hm = 0) and leaves the state untouched, exactly like
-        // a rejection.  Accept iff the last departure x satisfies
+        // Dense tile: the tile's requests of the component, compacted in trace
+        // order.  Each such lane stages its request's fields in shared memory
+        // at its rank among them; the per-request loop reads them with
+        // broadcast loads that do not depend on the state, so they issue
+        // ahead of the dependent chain (requests outside the component are
+        // never visited).  Accept iff the last departure x satisfies
         // x + tail - a <= slo, i.e. x <= lim = a + slo - tail (never when
-        // slo < tail, since x >= a).
+        // slo < tail, since x >= a: hm = 0, no host).
         TileReq<T>* tq = reinterpret_cast<TileReq<T>*>(w.tile);
-        {
+        const int nreq = __popc(todo);
+        if ((todo >> lane) & 1u) {
           TileReq<T> q;
           q.ar = arl;
-          q.hm = (((todo >> lane) & 1u) && sll >= tll) ? hml : 0u;
+          q.hm = sll >= tll ? hml : 0u;
           q.lim = 0;
           if (sll >= tll) {  // saturating: an unbounded SLO must not wrap
             const T room = sll - tll;
@@ -1457,11 +1483,11 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
           q.d0 = w.d[ml * kSTab];
           q.tl = tll;
           q.m = ml;
-          tq[lane] = q;
+          tq[__popc(todo & ((1u << lane) - 1u))] = q;
         }
         __syncwarp();
-#pragma unroll 8
-        for (int jj = 0; jj < 32; ++jj) {
+#pragma unroll 4
+        for (int jj = 0; jj < nreq; ++jj) {
           const TileReq<T> q = tq[jj];
           T d[S];
           if constexpr (S == 1) {
@@ -1720,6 +1746,249 @@ __device__ __forceinline__ void coop_dispatch(const ChunkParams& P, const WarpMe
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pass 3, components of <= 32 groups with S <= 2 stages: the group-lane
+// walker.  One warp per candidate; lane i holds, in registers, the S stage free
+// times of the i-th group (ascending id) of the candidate's component
+// (cand_gmask).  The tile's component requests are compacted and staged in
+// shared memory as in the scalar walker; per request every hosting lane runs
+// its group's tandem recurrence, one warp min gives the earliest last
+// departure, and the lowest lane among the minima -- the lowest group index,
+// C1 -- commits.  The per-request work no longer grows with the number of
+// groups (the scalar walker evaluates all of them in every lane).
+template <typename T, int S>
+__device__ __forceinline__ void glane_candidate(const ChunkParams& P, const WarpMem<T>& w,
+                                                const ItemDesc& it, int item, int cl, int lane,
+                                                uint32_t* end_src, unsigned long long& walked) {
+  const int64_t c = cand_of(P, it, item, cl);
+  const int my_m = P.bt.cand_model[c], my_g = P.bt.cand_group[c];
+  const uint64_t kmask = P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull;
+  const int ngroups = it.slots / S;
+  const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
+  const uint64_t gmask = (P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all;
+  // this lane's group: the lane-th set bit of gmask (-1: none)
+  int g_l = -1;
+  {
+    uint64_t b = gmask;
+    for (int i = 0; i < lane && b; ++i) b &= b - 1;
+    g_l = b ? __ffsll((long long)b) - 1 : -1;
+  }
+  // compact hosting mask of every model over the component's groups (bit i =
+  // lane i's group); the hosting-list region serves as scratch, as in the
+  // scalar walker
+  uint32_t* hmc = reinterpret_cast<uint32_t*>(w.hid);
+  for (int m = lane; m < P.pr.M; m += 32) {
+    const uint64_t hm = w.hmask[m] | (m == my_m ? (1ull << my_g) : 0ull);
+    uint32_t x = 0;
+    uint64_t b = gmask;
+    for (int i = 0; b; ++i, b &= b - 1)
+      if ((hm >> (__ffsll((long long)b) - 1)) & 1ull) x |= 1u << i;
+    hmc[m] = x;
+  }
+  __syncwarp();
+  const int64_t cstride = (int64_t)P.num_items * 32;
+  bool start_ok = true;
+  for (int j = 1; j < P.J; ++j) {
+    const int64_t u = (int64_t)j * P.num_items + item;
+    if (start_ok) {
+      if ((P.fix_flag[u] >> cl) & 1u) {  // pass 2 exact; true end of j is its fix_end
+        if (lane == 0) atomicOr(end_src + u, 1u << cl);
+        start_ok = false;
+      }
+      continue;
+    }
+    ++walked;
+    const int64_t i_begin = P.chunk_begin[j], i_end = P.chunk_begin[j + 1];
+    int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
+    // true start: chunk j-1's true end (fix_end)
+    const int64_t prev = u - P.num_items;
+    const T* s0 = reinterpret_cast<const T*>(P.fix_end) + prev * P.slots_max * 32;
+    const int64_t Ep = P.fix_epoch[prev];
+    T v[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      T x = 0;
+      if (g_l >= 0) {
+        const T raw = s0[(g_l * S + k) * 32 + cl];
+        if constexpr (TT<T>::kRel) {
+          const int64_t r = (int64_t)raw - (E - Ep);
+          x = r > 0 ? (T)r : (T)0;
+        } else {
+          x = raw;
+        }
+      }
+      v[k] = x;
+    }
+    int64_t good = 0, sum = 0;
+    int64_t al_n = i_begin + lane < i_end ? P.tr.arrival[i_begin + lane] : 0;
+    int ml_n = i_begin + lane < i_end ? (int)P.tr.model[i_begin + lane] : 0;
+    for (int64_t i0 = i_begin; i0 < i_end; i0 += 32) {
+      const bool valid = i0 + lane < i_end;
+      const int64_t al = al_n;
+      const int ml = ml_n;
+      if (i0 + 32 + lane < i_end) {
+        al_n = P.tr.arrival[i0 + 32 + lane];
+        ml_n = (int)P.tr.model[i0 + 32 + lane];
+      }
+      unsigned todo = __ballot_sync(FULL, valid && ((kmask >> (ml & 63)) & 1ull));
+      if (!todo) continue;
+      bool per_req = false;
+      if constexpr (TT<T>::kRel) {
+        const int64_t a_last = __shfl_sync(FULL, al, 31 - __clz(todo));
+        if (a_last - E > P.theta) {  // move the epoch to the tile's first request
+          const int64_t a_first = __shfl_sync(FULL, al, __ffs(todo) - 1);
+          const int64_t gap = a_first - E;
+          const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+          for (int k = 0; k < S; ++k) v[k] = v[k] > delta ? v[k] - delta : (T)0;
+          E = a_first;
+          per_req = a_last - E > P.theta;
+        }
+      }
+      // compacted component requests of the tile, staged as in the scalar walker
+      TileReq<T>* tq = reinterpret_cast<TileReq<T>*>(w.tile);
+      const int nreq = __popc(todo);
+      if ((todo >> lane) & 1u) {
+        const T arl = (T)(al - E);
+        const T tll = w.tail[ml], sll = w.slo[ml];
+        TileReq<T> q;
+        q.ar = arl;
+        q.hm = sll >= tll ? hmc[ml] : 0u;
+        q.lim = 0;
+        if (sll >= tll) {
+          const T room = sll - tll;
+          q.lim = room > (T)(TT<T>::maxv() - 1 - arl) ? (T)(TT<T>::maxv() - 1) : (T)(arl + room);
+        }
+        q.d0 = w.d[ml * kSTab];
+        q.tl = tll;
+        q.m = ml;
+        tq[__popc(todo & ((1u << lane) - 1u))] = q;
+      }
+      __syncwarp();
+      // sparse tiles (per-request epochs, rare): the staged relative arrivals
+      // may have wrapped, so each request's absolute arrival comes from its lane
+      const int src = per_req ? nth_set_bit(todo, lane) : 0;
+      for (int jj = 0; jj < nreq; ++jj) {
+        TileReq<T> q = tq[jj];
+        if constexpr (TT<T>::kRel) {
+          if (per_req) {
+            const int64_t a_abs = __shfl_sync(FULL, al, __shfl_sync(FULL, src, jj));
+            if (a_abs - E > P.theta) {
+              const int64_t gap = a_abs - E;
+              const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+              for (int k = 0; k < S; ++k) v[k] = v[k] > delta ? v[k] - delta : (T)0;
+              E = a_abs;
+            }
+            // the request's fields at the new epoch, from its model's tables
+            const T ar = (T)(a_abs - E);
+            const T tll = w.tail[q.m], sll = w.slo[q.m];
+            q.lim = 0;
+            if (sll >= tll) {
+              const T room = sll - tll;
+              q.lim = room > (T)(TT<T>::maxv() - 1 - ar) ? (T)(TT<T>::maxv() - 1) : (T)(ar + room);
+            }
+            q.ar = ar;
+          }
+        }
+        T d[S];
+        if constexpr (S == 1) {
+          d[0] = q.d0;
+        } else {
+#pragma unroll
+          for (int k = 0; k < S; ++k) d[k] = w.d[q.m * kSTab + k];
+        }
+        T x = q.ar;
+        T y[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          x = tmax(x, v[k]) + d[k];
+          y[k] = x;
+        }
+        const T key = ((q.hm >> lane) & 1u) ? x : TT<T>::maxv();
+        const T mn = warp_min<T>(key);
+        if (mn <= q.lim) {  // accepted (warp-uniform); no host: mn = maxv > lim
+          // the lowest lane among the minima: a second warp min (a ballot +
+          // find-first-set costs ~3x its latency on the chain, scripts/micro)
+          const unsigned win = __reduce_min_sync(FULL, key == mn ? (unsigned)lane : 32u);
+          if ((unsigned)lane == win) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) v[k] = y[k];
+          }
+          ++good;
+          sum += (int64_t)(mn - q.ar) + (int64_t)q.tl;
+        }
+      }
+      __syncwarp();
+    }
+    // the chunk's exact correction, and equivalence with the speculative end
+    if (lane == 0) {
+      P.fix_good[j * cstride + (int64_t)item * 32 + cl] =
+          (int32_t)(good - P.spec_good[j * cstride + (int64_t)item * 32 + cl]);
+      P.fix_sum[j * cstride + (int64_t)item * 32 + cl] =
+          sum - P.spec_sum[j * cstride + (int64_t)item * 32 + cl];
+    }
+    if (j + 1 < P.J) {
+      const int64_t a_next = P.tr.arrival[i_end];
+      const T* se = reinterpret_cast<const T*>(P.spec_end) + u * P.slots_max * 32;
+      const int64_t Es = P.spec_epoch[u];
+      bool eq = true;
+      if (g_l >= 0) {
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          const int64_t t0 = (TT<T>::kRel ? E : 0) + (int64_t)v[k];
+          const int64_t t1 = (TT<T>::kRel ? Es : 0) + (int64_t)se[(g_l * S + k) * 32 + cl];
+          eq &= (t0 > a_next ? t0 : a_next) == (t1 > a_next ? t1 : a_next);
+        }
+      }
+      start_ok = __all_sync(FULL, eq);
+      if (!start_ok) {  // publish column cl at the unit's canonical epoch
+        const int64_t Ec = P.tr.arrival[i_end - 1];
+        T* out = reinterpret_cast<T*>(P.fix_end) + u * P.slots_max * 32;
+        // slots outside the component keep their start values
+        for (int t = lane; t < it.slots; t += 32) {
+          if ((gmask >> ((t / S) & 63)) & 1ull) continue;
+          const T raw = s0[t * 32 + cl];
+          if constexpr (TT<T>::kRel) {
+            const int64_t r = (int64_t)raw + Ep - Ec;
+            out[t * 32 + cl] = r > 0 ? (T)r : (T)0;
+          } else {
+            out[t * 32 + cl] = raw;
+          }
+        }
+        if (g_l >= 0) {
+#pragma unroll
+          for (int k = 0; k < S; ++k) {
+            T x;
+            if constexpr (TT<T>::kRel) {
+              const int64_t r = (int64_t)v[k] - (Ec - E);
+              x = r > 0 ? (T)r : (T)0;
+            } else {
+              x = v[k];
+            }
+            out[(g_l * S + k) * 32 + cl] = x;
+          }
+        }
+        if (lane == 0) {
+          P.fix_epoch[u] = Ec;
+          atomicOr(end_src + u, 1u << cl);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Does candidate c walk with the group-lane walker?  S <= 2, <= 32 groups in
+// its component, at least P.glane_walk of them, and no statistics rows.
+__device__ __forceinline__ bool glane_fits(const ChunkParams& P, const ItemDesc& it, int64_t c) {
+  if (P.glane_walk <= 0 || P.fix_pm || it.S > 2) return false;
+  const int ngroups = it.slots / it.S;
+  const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
+  const int ng = __popcll((P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all);
+  return ng <= 32 && ng >= P.glane_walk;
+}
+
 // SCALAR = false: the cooperative walker for every candidate the scalar one
 // does not take; SCALAR = true: the scalar walker (separate kernel: its
 // register arrays would otherwise spill the cooperative walker).
@@ -1737,7 +2006,10 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     const int item = u >> 5, cl = u & 31;
     const ItemDesc it = P.items[item];
     if (it.S == 0 || cl >= it.count || !P.bt.cand_ok[cand_of(P, it, item, cl)]) continue;
-    const bool fits = P.scalar_walk && scalar_fits(P, it, cand_of(P, it, item, cl));
+    // the scalar kernel takes the scalar walker's and the group-lane walker's
+    // candidates, the cooperative kernel the rest
+    const bool glane = glane_fits(P, it, cand_of(P, it, item, cl));
+    const bool fits = P.scalar_walk && (glane || scalar_fits(P, it, cand_of(P, it, item, cl)));
     if (fits != SCALAR) continue;  // the other walker's candidate
     // any chunk of this candidate flagged by pass 2?  (else nothing to walk)
     bool any = false;
@@ -1753,10 +2025,18 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
     const unsigned long long u0 = upd;
     const long long t0 = clock64();
 #endif
-    if constexpr (SCALAR)
-      scalar_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
-    else
+    if constexpr (SCALAR) {
+      if (glane) {
+        if (it.S == 1)
+          glane_candidate<T, 1>(P, w, it, item, cl, lane, end_src, walked);
+        else
+          glane_candidate<T, 2>(P, w, it, item, cl, lane, end_src, walked);
+      } else {
+        scalar_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
+      }
+    } else {
       coop_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
+    }
     if (P.walked && lane == 0 && walked > w0) {  // statistics: walking candidates, longest walk
       atomicAdd(P.walked + 1, 1ull);
       atomicMax(P.walked + 2, walked - w0);
@@ -1764,8 +2044,8 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
       const long long cyc = clock64() - t0;
       if (P.walk_log > 0 && cyc > P.walk_log) {
         const int64_t c = cand_of(P, it, item, cl);
-        printf("walk scalar=%d S=%d slots=%d ng=%d models=%d chunks=%llu cycles=%lld upd=%llu\n",
-               (int)SCALAR, it.S, it.slots,
+        printf("walk kind=%d S=%d slots=%d ng=%d models=%d chunks=%llu cycles=%lld upd=%llu\n",
+               glane ? 2 : (int)SCALAR, it.S, it.slots,
                __popcll(P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull),
                __popcll(P.bt.cand_kmask ? P.bt.cand_kmask[c] : ~0ull), walked - w0, cyc, upd - u0);
       }

@@ -280,6 +280,7 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   ctx->sms = prop.multiProcessorCount;
   if (const char* sw = getenv("ASIM_SCALAR_WALK")) ctx->scalar_walk = sw[0] != '0';
   if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
+  if (const char* gw = getenv("ASIM_GLANE_WALK")) ctx->glane_walk = atoi(gw);
   if (const char* gc = getenv("ASIM_GROUP_CANDIDATES")) ctx->group_cands = gc[0] != '0';
   if (const char* sp = getenv("ASIM_SPLIT")) ctx->split_steps = sp[0] != '0';
   if (const char* mc = getenv("ASIM_MAX_CHUNKS")) ctx->max_chunks = std::max(1ll, atoll(mc));

@@ -126,9 +126,12 @@ struct asim_ctx {
   int64_t min_chunk = 4096;  // requests per time chunk (chunked path)
   int64_t max_chunks = 256;  // time chunks of a search (ASIM_MAX_CHUNKS; results do not depend on it)
   int64_t walk_log = 0;      // diagnostics: ASIM_WALK_LOG=<cycles> prints long walks (profiling on)
-  bool split_steps = true;   // search steps run walk-prone candidates concurrently (ASIM_SPLIT=0: off)
+  bool split_steps = false;  // search steps run walk-prone candidates concurrently (ASIM_SPLIT=1: on;
+                             // off by default: equal search time since the group-lane walker,
+                             // profiles/r2l)
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
+  int32_t glane_walk = 4;    // ASIM_GLANE_WALK (0: off): see ChunkParams::glane_walk
 
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;

@@ -58,7 +58,11 @@ for rep in range(args.reps):
                 s1 = sim.stats()
                 rows.append(dict(C=C, ms=(time.perf_counter() - ts) * 1e3,
                                  **{k: s1[k] - s0[k] for k in ("spec_ms", "pass2_ms", "walk_ms",
-                                                               "walk_candidates", "chunk_reruns")}))
+                                                               "walk_candidates", "chunk_reruns",
+                                                               "spec_stage_updates",
+                                                               "spec_live_lanes",
+                                                               "spec_lane_slots",
+                                                               "walk_critical_chunks")}))
         r = sh.result()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0

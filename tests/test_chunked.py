@@ -225,23 +225,48 @@ def test_uniform_config_with_empty_group_slot(sim):
             sim.set_chunk_size(4096)
 
 
+def _sim_env(key, value):
+    import os
+    from paper_2302_11665_b200 import Simulator
+    old = os.environ.get(key)
+    os.environ[key] = value
+    try:
+        return Simulator(0)
+    finally:
+        if old is None:
+            del os.environ[key]
+        else:
+            os.environ[key] = old
+
+
 @pytest.fixture(scope="module")
 def sim_coop():
     """A context whose walk uses only the cooperative walker (the scalar
     register walker switched off), so both walkers stay covered."""
-    import os
-    from paper_2302_11665_b200 import Simulator
-    old = os.environ.get("ASIM_SCALAR_WALK")
-    os.environ["ASIM_SCALAR_WALK"] = "0"
-    try:
-        s = Simulator(0)
-    finally:
-        if old is None:
-            del os.environ["ASIM_SCALAR_WALK"]
-        else:
-            os.environ["ASIM_SCALAR_WALK"] = old
+    s = _sim_env("ASIM_SCALAR_WALK", "0")
     yield s
     s.close()
+
+
+@pytest.fixture(scope="module", params=["0", "1"])
+def sim_glane(request):
+    """Group-lane walker off (the scalar walker takes every small component)
+    and on for every component of S <= 2 and <= 32 groups (one group too)."""
+    s = _sim_env("ASIM_GLANE_WALK", request.param)
+    yield s
+    s.close()
+
+
+@pytest.mark.parametrize("S", [1, 2])
+@pytest.mark.parametrize("u32", [True, False])
+def test_stage_classes_group_lane_walker(sim_glane, S, u32):
+    test_stage_classes(sim_glane, S, u32)
+
+
+def test_overload_chains_group_lane_walker(sim_glane):
+    test_overload_rerun_chains(sim_glane)
+    test_search_same_on_both_paths(sim_glane)
+    test_epoch_rebase_long_gaps(sim_glane, 2.0)
 
 
 @pytest.mark.parametrize("S", [1, 2, 8])

@@ -645,6 +645,22 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
     if (active && my_m >= 0) w.rel[my_m] = 1;
   }
 
+  // uniform configs: per model the lanes that simulate its requests (active,
+  // model in the lane's component, and the model able to meet its SLO at all
+  // under this config: slo >= tail [+ d0 for S == 1]), so a request's
+  // liveness is one broadcast load; the walkers' hosting-mask region holds it
+  uint32_t* lmask = reinterpret_cast<uint32_t*>(w.hmask);
+  if constexpr (S > 0) {
+    for (int m = 0; m < M; ++m) {
+      const T sl = w.slo[m], tl = w.tail[m];
+      const bool nev = sl < tl || (S == 1 && (T)(sl - tl) < w.d[m * kSTab]);
+      const bool l = active && !nev && (!restrict_k || (m < 64 && ((kmask >> m) & 1ull)));
+      const unsigned b = __ballot_sync(FULL, l);
+      if (lane == 0) lmask[m] = b;
+    }
+  }
+  const bool stats_on = P.spec_pm != nullptr;
+
   // initial states
   int64_t E = TT<T>::kRel ? P.tr.arrival[i_begin] : 0;
   if constexpr (MODE != WALK) {  // the speculative trajectory
@@ -774,14 +790,14 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
             uniform_fields<T, S>(w, cm, car, lim, cc, d0x, hA, hB, h0c);
           }
         }
-        const bool live = active && ((kmask >> (cm & 63)) & 1ull) && !(h0c & (1 << 23));
+        const bool live = (lmask[cm] >> lane) & 1u;
         const bool mine = live && cm == my_m;
         T v0;
         int bo0;
         if (step_u<T, S>(w, w.st0, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v0, bo0)) {
           ++good0;
           sum0 += (int64_t)(T)(v0 + cc);
-          if (P.spec_pm) {  // SPEC: pass-1 counts; DUAL: the true side of the correction
+          if (stats_on) {  // SPEC: pass-1 counts; DUAL: the true side of the correction
             const int g0 = bo0 / (S * 32 * (int)sizeof(T));
             if constexpr (MODE == SPEC)
               stat_add(P.spec_pm, P.spec_busy, P, j, c, cm, g0, occupancy<T, S>(P, w, g0, cm, dv), 1);
@@ -796,7 +812,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
           if (step_u<T, S>(w, w.st1, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v1, bo1)) {
             ++good1;
             sum1 += (int64_t)(T)(v1 + cc);
-            if (P.spec_pm) {  // minus the speculative side
+            if (stats_on) {  // minus the speculative side
               const int g1 = bo1 / (S * 32 * (int)sizeof(T));
               stat_add(P.fix_pm, P.fix_busy, P, j, c, cm, g1, occupancy<T, S>(P, w, g1, cm, dv), -1);
             }

@@ -13,6 +13,11 @@ struct DevProblem {
   const int64_t* tail;      // [M][P]
   const int64_t* slo;       // [M]
   const int32_t* cfg_stages;  // [P]
+  // stage latencies by config, padded to 16 per model (0 beyond the config's
+  // stages): [P][M][16]; uint32 copy (values clipped, used only when times
+  // are uint32, i.e. every latency fits) and int64 copy
+  const uint32_t* dtab32;
+  const int64_t* dtab64;
 };
 
 // Trace resident in HBM (asim_set_trace).  Padded to a multiple of 32 with
@@ -156,6 +161,7 @@ struct ChunkParams {
   int64_t stat_C;
   int32_t scalar_walk;  // 1 = small components walk with the register-state scalar walker
   int32_t glane_walk;   // > 0: components of S <= 2 and glane_walk..32 groups take the group-lane walker
+  int32_t glane_smax;   // largest stage count the group-lane walker takes (S >= 4: from 2 groups)
   int32_t transient;    // 1 = passes 1-2 launch one unit per warp, blocks retire (split steps)
   int64_t walk_log;     // diagnostics (ASIM_WALK_LOG=cycles): printf every walk longer than this
 };

@@ -46,6 +46,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "asim_internal.h"
 #include "chunk_common.cuh"
@@ -101,10 +102,13 @@ __host__ __device__ inline size_t tile_extra(int slots_max, size_t tsz) {
   return (size_t)slots_max * 32 * tsz >= kTileBytes ? 0 : kTileBytes;
 }
 
+// dsm: the stage-latency table lives in the region (walkers); passes 1-2
+// read it from the global per-config table through L1 instead, which keeps
+// their regions small enough for 5 blocks per SM.
 __host__ __device__ inline size_t warp_bytes(int slots_max, int M, int hid_cap, size_t tsz,
-                                             bool dual) {
+                                             bool dual, bool dsm = true) {
   size_t b = (size_t)slots_max * 32 * tsz * (dual ? 2 : 1);
-  b += (size_t)M * tsz * (kSTab + 2) + 64 * 4 + 2 * (size_t)(M + 1);
+  b += (size_t)M * tsz * ((dsm ? kSTab : 0) + 2) + 64 * 4 + 2 * (size_t)(M + 1);
   b = (b + 15) & ~size_t(15);
   b += (size_t)hid_cap + ((M + 15) & ~15) + 128;
   b = (b + 15) & ~size_t(15);
@@ -115,7 +119,8 @@ __host__ __device__ inline size_t warp_bytes(int slots_max, int M, int hid_cap, 
 }
 
 template <typename T>
-__device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkParams& P, bool dual) {
+__device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkParams& P, bool dual,
+                                            bool dsm = true) {
   // integer offsets from the shared-memory base only: pointer differences
   // would hide the address space and turn every LDS into a generic access
   WarpMem<T> w;
@@ -126,8 +131,8 @@ __device__ __forceinline__ WarpMem<T> carve(unsigned char* base, const ChunkPara
   off += st_bytes;
   w.st1 = dual ? reinterpret_cast<T*>(base + off) : nullptr;
   if (dual) off += st_bytes;
-  w.d = reinterpret_cast<T*>(base + off);
-  off += M * kSTab * sizeof(T);
+  w.d = dsm ? reinterpret_cast<T*>(base + off) : nullptr;
+  if (dsm) off += M * kSTab * sizeof(T);
   w.tail = reinterpret_cast<T*>(base + off);
   off += M * sizeof(T);
   w.slo = reinterpret_cast<T*>(base + off);
@@ -185,8 +190,9 @@ __device__ __forceinline__ void load_base(const ChunkParams& P, const ItemDesc& 
     w.slo[m] = TT<T>::clip(P.pr.slo[m]);
     if (it.cfg >= 0) {
       const int64_t* d = P.pr.stage + ((int64_t)m * PP + it.cfg) * SS;
-      for (int k = 0; k < kSTab; ++k)
-        w.d[m * kSTab + k] = (k < SS && k < it.stages) ? (T)d[k] : (T)0;
+      if (w.d)
+        for (int k = 0; k < kSTab; ++k)
+          w.d[m * kSTab + k] = (k < SS && k < it.stages) ? (T)d[k] : (T)0;
       w.tail[m] = (T)P.pr.tail[(int64_t)m * PP + it.cfg];
     }
   }
@@ -382,14 +388,14 @@ __device__ __forceinline__ int nth_set_bit(unsigned x, int r) {
 //   hA, hB  byte offsets of the first four hosts' first stage slots (16 bits each)
 //   h0c  hosting-list start | host count << 16 | never-acceptable << 23
 template <typename T, int S>
-__device__ __forceinline__ void uniform_fields(const WarpMem<T>& w, int m, T ar, T& lim, T& cc,
-                                               T& d0, int& hA, int& hB, int& h0c) {
+__device__ __forceinline__ void uniform_fields(const WarpMem<T>& w, const T* dt, int m, T ar,
+                                               T& lim, T& cc, T& d0, int& hA, int& hB, int& h0c) {
   const int h0 = w.hoff[m];
   const int cnt = w.hoff[m + 1] - h0;
   hA = (cnt >= 1 ? (int)w.hid[h0] : 0) | (cnt >= 2 ? (int)w.hid[h0 + 1] << 16 : 0);
   hB = (cnt >= 3 ? (int)w.hid[h0 + 2] : 0) | (cnt >= 4 ? (int)w.hid[h0 + 3] << 16 : 0);
   const T sl = w.slo[m], tl = w.tail[m];
-  d0 = S == 1 ? w.d[m * kSTab] : (T)0;
+  d0 = S == 1 ? __ldg(dt + m * kSTab) : (T)0;
   bool ok = sl >= tl;
   T l = 0;
   if (ok) {
@@ -412,7 +418,7 @@ __device__ __forceinline__ void load_dv(const T* row, T* dv) {
   if constexpr (sizeof(T) == 4 && S >= 4) {
 #pragma unroll
     for (int q = 0; q < S / 4; ++q) {
-      const uint4 v = reinterpret_cast<const uint4*>(row)[q];
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(row) + q);
       dv[4 * q] = (T)v.x;
       dv[4 * q + 1] = (T)v.y;
       dv[4 * q + 2] = (T)v.z;
@@ -421,7 +427,7 @@ __device__ __forceinline__ void load_dv(const T* row, T* dv) {
   } else if constexpr (S >= 2) {
 #pragma unroll
     for (int q = 0; q < S * (int)sizeof(T) / 8; ++q) {
-      const uint2 v = reinterpret_cast<const uint2*>(row)[q];
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(row) + q);
       if constexpr (sizeof(T) == 4) {
         dv[2 * q] = (T)v.x;
         dv[2 * q + 1] = (T)v.y;
@@ -430,7 +436,25 @@ __device__ __forceinline__ void load_dv(const T* row, T* dv) {
       }
     }
   } else {
-    dv[0] = row[0];
+    dv[0] = __ldg(row);
+  }
+}
+
+// The same from the walkers' shared-memory table.
+template <typename T, int S>
+__device__ __forceinline__ void load_dv_smem(const T* row, T* dv) {
+  if constexpr (sizeof(T) == 4 && S >= 4) {
+#pragma unroll
+    for (int q = 0; q < S / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(row)[q];
+      dv[4 * q] = (T)v.x;
+      dv[4 * q + 1] = (T)v.y;
+      dv[4 * q + 2] = (T)v.z;
+      dv[4 * q + 3] = (T)v.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < S; ++k) dv[k] = row[k];
   }
 }
 
@@ -650,10 +674,16 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
   // under this config: slo >= tail [+ d0 for S == 1]), so a request's
   // liveness is one broadcast load; the walkers' hosting-mask region holds it
   uint32_t* lmask = reinterpret_cast<uint32_t*>(w.hmask);
+  // uniform configs: the config's stage-latency rows [M][kSTab] (global, L1)
+  const T* dt = nullptr;
+  if constexpr (S > 0)
+    dt = reinterpret_cast<const T*>(sizeof(T) == 4 ? (const void*)P.pr.dtab32
+                                                   : (const void*)P.pr.dtab64) +
+         (int64_t)it.cfg * M * kSTab;
   if constexpr (S > 0) {
     for (int m = 0; m < M; ++m) {
       const T sl = w.slo[m], tl = w.tail[m];
-      const bool nev = sl < tl || (S == 1 && (T)(sl - tl) < w.d[m * kSTab]);
+      const bool nev = sl < tl || (S == 1 && (T)(sl - tl) < __ldg(dt + m * kSTab));
       const bool l = active && !nev && (!restrict_k || (m < 64 && ((kmask >> m) & 1ull)));
       const unsigned b = __ballot_sync(FULL, l);
       if (lane == 0) lmask[m] = b;
@@ -757,7 +787,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       const T ar_l = (T)(ai - E);
       T lim_l, cc_l, d0_l;
       int hA_l, hB_l, h0c_l;
-      uniform_fields<T, S>(w, mi, ar_l, lim_l, cc_l, d0_l, hA_l, hB_l, h0c_l);
+      uniform_fields<T, S>(w, dt, mi, ar_l, lim_l, cc_l, d0_l, hA_l, hB_l, h0c_l);
       // compaction: lane k gathers the fields of the tile's k-th relevant
       // request (src = the k-th set bit of todo, by a 5-step popcount select),
       // so the per-request loop below broadcasts from lane k with a plain
@@ -779,7 +809,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
         if constexpr (S == 1) {
           dv[0] = __shfl_sync(FULL, d0_c, k);
         } else {
-          load_dv<T, S>(w.d + cm * kSTab, dv);
+          load_dv<T, S>(dt + cm * kSTab, dv);
         }
         if constexpr (TT<T>::kRel) {
           if (per_req) {  // sparse tile: per-request epochs, fields recomputed (rare)
@@ -787,7 +817,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
             maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
             car = (T)(a - E);
             T d0x;
-            uniform_fields<T, S>(w, cm, car, lim, cc, d0x, hA, hB, h0c);
+            uniform_fields<T, S>(w, dt, cm, car, lim, cc, d0x, hA, hB, h0c);
           }
         }
         const bool live = (lmask[cm] >> lane) & 1u;
@@ -993,12 +1023,14 @@ __device__ __forceinline__ int next_unit(const ChunkParams& P, int lane) {
 }
 
 // Passes 1 and 2: persistent warps pulling (item, chunk) units.
+// 5 blocks per SM: 20 warps (<= 96 registers; measured: 8, 12, 16 warps per SM
+// gave pass 1 29.4, 21.1, 17.5 s on the day search, profiles/r2l/prof_pad_*).
 template <typename T, int MODE>
-__global__ void __launch_bounds__(kWarps * 32) chunk_kernel(ChunkParams P) {
+__global__ void __launch_bounds__(kWarps * 32, 5) chunk_kernel(ChunkParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t wb = warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL);
-  WarpMem<T> w = carve<T>(smem + warp * wb, P, MODE == DUAL);
+  const size_t wb = warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL, false);
+  WarpMem<T> w = carve<T>(smem + warp * wb, P, MODE == DUAL, false);
   int cur_base = -1;
   for (;;) {
     const int u = next_unit(P, lane);
@@ -1911,8 +1943,7 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
         if constexpr (S == 1) {
           d[0] = q.d0;
         } else {
-#pragma unroll
-          for (int k = 0; k < S; ++k) d[k] = w.d[q.m * kSTab + k];
+          load_dv_smem<T, S>(w.d + q.m * kSTab, d);
         }
         T x = q.ar;
         T y[S];
@@ -1998,11 +2029,12 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
 // Does candidate c walk with the group-lane walker?  S <= 2, <= 32 groups in
 // its component, at least P.glane_walk of them, and no statistics rows.
 __device__ __forceinline__ bool glane_fits(const ChunkParams& P, const ItemDesc& it, int64_t c) {
-  if (P.glane_walk <= 0 || P.fix_pm || it.S > 2) return false;
+  if (P.glane_walk <= 0 || P.fix_pm || it.S > P.glane_smax) return false;
   const int ngroups = it.slots / it.S;
   const uint64_t all = ngroups >= 64 ? ~0ull : ((1ull << ngroups) - 1ull);
   const int ng = __popcll((P.bt.cand_gmask ? P.bt.cand_gmask[c] : ~0ull) & all);
-  return ng <= 32 && ng >= P.glane_walk;
+  // S >= 4: the scalar walker's per-request work is NG x S >= 8 slots already at 2 groups
+  return ng <= 32 && ng >= (it.S <= 2 ? P.glane_walk : 2);
 }
 
 // SCALAR = false: the cooperative walker for every candidate the scalar one
@@ -2043,10 +2075,13 @@ __global__ void __launch_bounds__(kWarps * 32) coop_walk_kernel(ChunkParams P, u
 #endif
     if constexpr (SCALAR) {
       if (glane) {
-        if (it.S == 1)
-          glane_candidate<T, 1>(P, w, it, item, cl, lane, end_src, walked);
-        else
-          glane_candidate<T, 2>(P, w, it, item, cl, lane, end_src, walked);
+        switch (it.S) {
+          case 1: glane_candidate<T, 1>(P, w, it, item, cl, lane, end_src, walked); break;
+          case 2: glane_candidate<T, 2>(P, w, it, item, cl, lane, end_src, walked); break;
+          case 4: glane_candidate<T, 4>(P, w, it, item, cl, lane, end_src, walked); break;
+          case 8: glane_candidate<T, 8>(P, w, it, item, cl, lane, end_src, walked); break;
+          default: glane_candidate<T, 16>(P, w, it, item, cl, lane, end_src, walked); break;
+        }
       } else {
         scalar_dispatch<T>(P, w, it, item, cl, lane, end_src, walked, upd);
       }
@@ -2255,7 +2290,7 @@ cudaError_t grid_for(K kernel, size_t smem, int64_t units, int sms, int64_t* blo
 
 template <typename T, int MODE>
 cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
-  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL);
+  const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL, false);
   int64_t blocks = 1;
   cudaError_t e = grid_for(chunk_kernel<T, MODE>, smem, P.num_units, sms, &blocks);
   if (e != cudaSuccess) return e;

@@ -351,6 +351,7 @@ static asim_status run_slot(asim_ctx* ctx, ChunkSlot& cs, const HostBatch& hb,
   P.walked = ctx->profiling ? cs.walked.as<unsigned long long>() : nullptr;
   P.scalar_walk = ctx->scalar_walk ? 1 : 0;
   P.glane_walk = ctx->glane_walk;
+  P.glane_smax = ctx->glane_smax;
   P.transient = transient ? 1 : 0;
   P.walk_log = ctx->walk_log;
   P.spec_state = opt ? opt->spec_state : nullptr;

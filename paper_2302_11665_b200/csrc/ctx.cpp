@@ -281,6 +281,7 @@ asim_status asim_create(int32_t cuda_device, asim_ctx** out) {
   if (const char* sw = getenv("ASIM_SCALAR_WALK")) ctx->scalar_walk = sw[0] != '0';
   if (const char* wl = getenv("ASIM_WALK_LOG")) ctx->walk_log = atoll(wl);
   if (const char* gw = getenv("ASIM_GLANE_WALK")) ctx->glane_walk = atoi(gw);
+  if (const char* gs = getenv("ASIM_GLANE_SMAX")) ctx->glane_smax = atoi(gs);
   if (const char* gc = getenv("ASIM_GROUP_CANDIDATES")) ctx->group_cands = gc[0] != '0';
   if (const char* sp = getenv("ASIM_SPLIT")) ctx->split_steps = sp[0] != '0';
   if (const char* mc = getenv("ASIM_MAX_CHUNKS")) ctx->max_chunks = std::max(1ll, atoll(mc));
@@ -315,6 +316,7 @@ void asim_destroy(asim_ctx* ctx) {
   {
     DeviceGuard dg(ctx->device);
     DBuf* bufs[] = {&ctx->d_stage, &ctx->d_tail, &ctx->d_slo, &ctx->d_cfg_stages,
+                    &ctx->d_dtab32, &ctx->d_dtab64,
                     &ctx->d_arrival, &ctx->d_model, &ctx->d_moff, &ctx->d_midx, &ctx->d_inc,
                     &ctx->d_order, &ctx->d_mcum, &ctx->d_base_cfg, &ctx->d_base_mask,
                     &ctx->d_cand_base, &ctx->d_cand_model, &ctx->d_cand_group, &ctx->d_cand_ok,
@@ -587,6 +589,21 @@ asim_status asim_set_problem(asim_ctx* ctx, const asim_problem* p) {
   if (e == cudaSuccess) e = upload(ctx->d_tail, hp.tail, 0);
   if (e == cudaSuccess) e = upload(ctx->d_slo, hp.slo, 0);
   if (e == cudaSuccess) e = upload(ctx->d_cfg_stages, hp.cfg_stages, 0);
+  {
+    // per-config stage-latency rows for the passes (read through L1)
+    std::vector<uint32_t> t32((size_t)P * M * 16, 0u);
+    std::vector<int64_t> t64((size_t)P * M * 16, 0);
+    for (int64_t c = 0; c < P; ++c)
+      for (int64_t m = 0; m < M; ++m)
+        for (int64_t k = 0; k < std::min<int64_t>(S, 16); ++k) {
+          if (k >= hp.cfg_stages[c]) continue;
+          const int64_t d = hp.stage[(m * P + c) * S + k];
+          t64[(c * M + m) * 16 + k] = d;
+          t32[(c * M + m) * 16 + k] = d >= 0xFFFFFFFFll ? 0xFFFFFFFFu : (uint32_t)d;
+        }
+    if (e == cudaSuccess) e = upload(ctx->d_dtab32, t32, 0);
+    if (e == cudaSuccess) e = upload(ctx->d_dtab64, t64, 0);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   if (e != cudaSuccess) return asim_cuda(ctx, e, "upload problem");
   // a trace set for another model count must be set again

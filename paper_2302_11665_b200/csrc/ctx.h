@@ -80,7 +80,7 @@ struct asim_ctx {
 
   bool has_problem = false;
   HostProblem hp;
-  DBuf d_stage, d_tail, d_slo, d_cfg_stages;
+  DBuf d_stage, d_tail, d_slo, d_cfg_stages, d_dtab32, d_dtab64;
 
   bool has_trace = false;
   int64_t n = 0;
@@ -132,6 +132,7 @@ struct asim_ctx {
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
   int32_t glane_walk = 4;    // ASIM_GLANE_WALK (0: off): see ChunkParams::glane_walk
+  int32_t glane_smax = 2;    // ASIM_GLANE_SMAX: see ChunkParams::glane_smax
 
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;
@@ -147,6 +148,8 @@ struct asim_ctx {
     p.tail = d_tail.as<int64_t>();
     p.slo = d_slo.as<int64_t>();
     p.cfg_stages = d_cfg_stages.as<int32_t>();
+    p.dtab32 = d_dtab32.as<uint32_t>();
+    p.dtab64 = d_dtab64.as<int64_t>();
     return p;
   }
   asim::DevTrace dev_trace() const {

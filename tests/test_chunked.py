@@ -225,39 +225,42 @@ def test_uniform_config_with_empty_group_slot(sim):
             sim.set_chunk_size(4096)
 
 
-def _sim_env(key, value):
+def _sim_env(env):
     import os
     from paper_2302_11665_b200 import Simulator
-    old = os.environ.get(key)
-    os.environ[key] = value
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         return Simulator(0)
     finally:
-        if old is None:
-            del os.environ[key]
-        else:
-            os.environ[key] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
 
 
 @pytest.fixture(scope="module")
 def sim_coop():
     """A context whose walk uses only the cooperative walker (the scalar
     register walker switched off), so both walkers stay covered."""
-    s = _sim_env("ASIM_SCALAR_WALK", "0")
+    s = _sim_env({"ASIM_SCALAR_WALK": "0"})
     yield s
     s.close()
 
 
-@pytest.fixture(scope="module", params=["0", "1"])
+@pytest.fixture(scope="module", params=[{"ASIM_GLANE_WALK": "0"},
+                                        {"ASIM_GLANE_WALK": "1", "ASIM_GLANE_SMAX": "16"}],
+                ids=["glane-off", "glane-all"])
 def sim_glane(request):
     """Group-lane walker off (the scalar walker takes every small component)
-    and on for every component of S <= 2 and <= 32 groups (one group too)."""
-    s = _sim_env("ASIM_GLANE_WALK", request.param)
+    and on for every uniform component of <= 32 groups (one group too)."""
+    s = _sim_env(request.param)
     yield s
     s.close()
 
 
-@pytest.mark.parametrize("S", [1, 2])
+@pytest.mark.parametrize("S", [1, 2, 4, 8, 16])
 @pytest.mark.parametrize("u32", [True, False])
 def test_stage_classes_group_lane_walker(sim_glane, S, u32):
     test_stage_classes(sim_glane, S, u32)

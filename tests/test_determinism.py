@@ -86,7 +86,8 @@ def test_candidate_permutation_invariance():
 
 @pytest.mark.parametrize("env", [{"ASIM_GROUP_CANDIDATES": "0"},
                                  {"ASIM_SCALAR_WALK": "0"}, {"ASIM_GLANE_WALK": "0"},
-                                 {"ASIM_GLANE_WALK": "1"}, {"ASIM_SPLIT": "1"},
+                                 {"ASIM_GLANE_WALK": "1", "ASIM_GLANE_SMAX": "16"},
+                                 {"ASIM_SPLIT": "1"},
                                  {"ASIM_SPLIT": "1", "ASIM_GROUP_CANDIDATES": "0"}])
 def test_search_layout_invariance(env):
     """The search's step-by-step results with the candidates regrouped or not,

@@ -46,6 +46,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#ifdef ASIM_WALK_DIAGNOSTICS
+#include <cstdio>
+#endif
 #include <cstdlib>
 
 #include "asim_internal.h"

@@ -56,6 +56,7 @@ for rep in range(args.reps):
             if args.steps:
                 torch.cuda.synchronize()
                 s1 = sim.stats()
+                print(f"STEP {len(rows)} C={C}", flush=True)  # separates device walk-log lines
                 rows.append(dict(C=C, ms=(time.perf_counter() - ts) * 1e3,
                                  **{k: s1[k] - s0[k] for k in ("spec_ms", "pass2_ms", "walk_ms",
                                                                "walk_candidates", "chunk_reruns",

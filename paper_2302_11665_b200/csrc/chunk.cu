@@ -91,6 +91,7 @@ struct alignas(16) TileReq {
   T lim;         // accept iff the last departure <= lim (= ar + slo - tail, saturated)
   T d0;          // first stage latency of the request's model (S == 1)
   T tl;          // tail
+  T d1;          // second stage latency (group-lane walker, S == 2)
   uint32_t hm;   // compact hosting mask (0: no host in the component, or never acceptable)
   int32_t m;     // model
 };
@@ -1533,6 +1534,7 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
           }
           q.d0 = w.d[ml * kSTab];
           q.tl = tll;
+          q.d1 = S == 2 ? w.d[ml * kSTab + 1] : (T)0;
           q.m = ml;
           tq[__popc(todo & ((1u << lane) - 1u))] = q;
         }
@@ -1543,6 +1545,9 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
           T d[S];
           if constexpr (S == 1) {
             d[0] = q.d0;
+          } else if constexpr (S == 2) {  // staged: no dependent table load on the chain
+            d[0] = q.d0;
+            d[1] = q.d1;
           } else {
 #pragma unroll
             for (int k = 0; k < S; ++k) d[k] = w.d[q.m * kSTab + k];
@@ -1911,6 +1916,7 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
           q.lim = room > (T)(TT<T>::maxv() - 1 - arl) ? (T)(TT<T>::maxv() - 1) : (T)(arl + room);
         }
         q.d0 = w.d[ml * kSTab];
+        q.d1 = S == 2 ? w.d[ml * kSTab + 1] : (T)0;
         q.tl = tll;
         q.m = ml;
         tq[__popc(todo & ((1u << lane) - 1u))] = q;
@@ -1945,6 +1951,9 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
         T d[S];
         if constexpr (S == 1) {
           d[0] = q.d0;
+        } else if constexpr (S == 2) {
+          d[0] = q.d0;
+          d[1] = q.d1;
         } else {
           load_dv_smem<T, S>(w.d + q.m * kSTab, d);
         }

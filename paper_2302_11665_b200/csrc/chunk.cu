@@ -1965,18 +1965,33 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
           y[k] = x;
         }
         const T key = ((q.hm >> lane) & 1u) ? x : TT<T>::maxv();
-        const T mn = warp_min<T>(key);
-        if (mn <= q.lim) {  // accepted (warp-uniform); no host: mn = maxv > lim
-          // the lowest lane among the minima: a second warp min (a ballot +
-          // find-first-set costs ~3x its latency on the chain, scripts/micro)
-          const unsigned win = __reduce_min_sync(FULL, key == mn ? (unsigned)lane : 32u);
-          if ((unsigned)lane == win) {
-#pragma unroll
-            for (int k = 0; k < S; ++k) v[k] = y[k];
-          }
-          ++good;
-          sum += (int64_t)(mn - q.ar) + (int64_t)q.tl;
+        T mn;
+        unsigned win;
+        if constexpr (sizeof(T) == 4) {
+          // Two independent warp mins, issued together: the exact minimum and
+          // a coarse key (value with its low 5 bits replaced by the lane) whose
+          // minimum is the lowest lane in the minimum's 32-ns bucket.  That
+          // lane holds the minimum unless a lower lane of the bucket holds a
+          // larger value (then a third warp min finds the lowest lane among
+          // the minima: C1).  (A ballot + find-first-set costs ~3x a warp min
+          // on the chain, scripts/micro.)
+          mn = (T)__reduce_min_sync(FULL, (unsigned)key);
+          const unsigned cw = __reduce_min_sync(FULL, ((unsigned)key & ~31u) | (unsigned)lane);
+          win = cw & 31u;
+          if (__shfl_sync(FULL, (unsigned)key, win) != (unsigned)mn)
+            win = __reduce_min_sync(FULL, key == mn ? (unsigned)lane : 32u);
+        } else {
+          mn = warp_min<T>(key);
+          win = __reduce_min_sync(FULL, key == mn ? (unsigned)lane : 32u);
         }
+        // accepted iff the earliest last departure meets the limit (warp-
+        // uniform; no host: mn = maxv > lim); predicated, no branch
+        const bool acc = mn <= q.lim;
+        const bool take = acc && (unsigned)lane == win;
+#pragma unroll
+        for (int k = 0; k < S; ++k) v[k] = take ? y[k] : v[k];
+        good += acc ? 1 : 0;
+        sum += acc ? (int64_t)(mn - q.ar) + (int64_t)q.tl : 0;
       }
       __syncwarp();
     }

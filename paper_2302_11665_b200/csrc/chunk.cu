@@ -1027,10 +1027,12 @@ __device__ __forceinline__ int next_unit(const ChunkParams& P, int lane) {
 }
 
 // Passes 1 and 2: persistent warps pulling (item, chunk) units.
-// 5 blocks per SM: 20 warps (<= 96 registers; measured: 8, 12, 16 warps per SM
-// gave pass 1 29.4, 21.1, 17.5 s on the day search, profiles/r2l/prof_pad_*).
-template <typename T, int MODE>
-__global__ void __launch_bounds__(kWarps * 32, 5) chunk_kernel(ChunkParams P) {
+// MINB blocks per SM: pass 1 5 (20 warps, <= 96 registers; measured: 8, 12,
+// 16 warps per SM gave pass 1 29.4, 21.1, 17.5 s on the day search,
+// profiles/r2l/prof_pad_*); pass 2 3 (two state regions per warp: shared
+// memory holds 3 blocks, so it keeps its registers).
+template <typename T, int MODE, int MINB>
+__global__ void __launch_bounds__(kWarps * 32, MINB) chunk_kernel(ChunkParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t wb = warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL, false);
@@ -2317,15 +2319,16 @@ cudaError_t grid_for(K kernel, size_t smem, int64_t units, int sms, int64_t* blo
 
 template <typename T, int MODE>
 cudaError_t launch_pass_t(const ChunkParams& P, cudaStream_t st, int sms) {
+  constexpr int MINB = MODE == DUAL ? 3 : 5;
   const size_t smem = kWarps * warp_bytes(P.slots_max, P.pr.M, P.hid_cap, sizeof(T), MODE == DUAL, false);
   int64_t blocks = 1;
-  cudaError_t e = grid_for(chunk_kernel<T, MODE>, smem, P.num_units, sms, &blocks);
+  cudaError_t e = grid_for(chunk_kernel<T, MODE, MINB>, smem, P.num_units, sms, &blocks);
   if (e != cudaSuccess) return e;
   // a split step's runs share the GPU: one unit per warp and blocks that
   // retire, so the block scheduler interleaves the two runs by stream priority
   // (persistent blocks would hold their SMs until their run's last unit)
   if (P.transient) blocks = std::max<int64_t>(1, std::min<int64_t>((P.num_units + kWarps - 1) / kWarps, 0x7FFFFFFF));
-  chunk_kernel<T, MODE><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P);
+  chunk_kernel<T, MODE, MINB><<<(unsigned)blocks, kWarps * 32, smem, st>>>(P);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,5 @@
+set -x
+python -m pytest tests/test_chunked.py tests/test_determinism.py tests/test_search_parity.py tests/test_parity.py tests/test_fast_heuristic.py -m gpu -x -q > gpurun_out/pytest_part.log 2>&1; echo pytest rc=$?
+tail -2 gpurun_out/pytest_part.log
+python scripts/search_profile.py 24 --reps 1 > gpurun_out/prof_day.txt 2>&1
+tail -1 gpurun_out/prof_day.txt | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print({k: round(d[k]) for k in ('search_ms','sim_ms','spec_busy_ms','pass2_busy_ms','walk_busy_ms')}, d['best_good'], [round(x/1e12,2) for x in d['spec_class_cycles']])"

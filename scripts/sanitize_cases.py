@@ -58,6 +58,16 @@ def main():
             h.run()
         inc = configs.batch_increment_ns(prob.stage_ns, 0.9)
         s.evaluate_batching(cfg[:16], mask[:16], inc, 3, per_model=True)
+    # the group-lane walker for every uniform component (any stage count) and
+    # split steps (two chunked runs on concurrent streams)
+    os.environ.update(ASIM_GLANE_WALK="1", ASIM_GLANE_SMAX="16", ASIM_SPLIT="1")
+    with Simulator(0) as s:
+        s.set_problem(prob)
+        s.set_trace(tr.arrival_ns, tr.model)
+        for chunk in (40, 4096):
+            s.set_chunk_size(chunk)
+            with s.search_handle(dedup=False, prune=True) as h:
+                h.run()
     print("sanitize cases done")
 
 

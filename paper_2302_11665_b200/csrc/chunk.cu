@@ -365,6 +365,11 @@ __device__ __forceinline__ int64_t step(const ChunkParams& P, const WarpMem<T>& 
   }
 }
 
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+
 // Position of the r-th (0-based) set bit of x (r < popc(x); else garbage):
 // a 5-step popcount select.
 __device__ __forceinline__ int nth_set_bit(unsigned x, int r) {
@@ -803,7 +808,9 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       const T cc_c = __shfl_sync(FULL, cc_l, src), d0_c = __shfl_sync(FULL, d0_l, src);
       const int hA_c = __shfl_sync(FULL, hA_l, src), hB_c = __shfl_sync(FULL, hB_l, src);
       const int h0c_c = __shfl_sync(FULL, h0c_l, src);
-      for (int k = 0; k < nreq; ++k) {
+      // the request loop comes in two copies: without the per-request epoch
+      // branch (dense tiles, the rule) and with it (sparse tiles)
+      auto request = [&](int k, auto sparse) {
         const int cm = __shfl_sync(FULL, mi_c, k);
         T car = __shfl_sync(FULL, ar_c, k);
         T lim = __shfl_sync(FULL, lim_c, k);
@@ -815,14 +822,13 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
         } else {
           load_dv<T, S>(dt + cm * kSTab, dv);
         }
-        if constexpr (TT<T>::kRel) {
-          if (per_req) {  // sparse tile: per-request epochs, fields recomputed (rare)
-            const int64_t a = __shfl_sync(FULL, ai, __shfl_sync(FULL, src, k));
-            maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
-            car = (T)(a - E);
-            T d0x;
-            uniform_fields<T, S>(w, dt, cm, car, lim, cc, d0x, hA, hB, h0c);
-          }
+        if constexpr (TT<T>::kRel && decltype(sparse)::value) {
+          // sparse tile: per-request epochs, fields recomputed (rare)
+          const int64_t a = __shfl_sync(FULL, ai, __shfl_sync(FULL, src, k));
+          maybe_rebase<T, MODE>(P, w, slots, lane, a, E);
+          car = (T)(a - E);
+          T d0x;
+          uniform_fields<T, S>(w, dt, cm, car, lim, cc, d0x, hA, hB, h0c);
         }
         const bool live = (lmask[cm] >> lane) & 1u;
         const bool mine = live && cm == my_m;
@@ -853,6 +859,11 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
           }
           if (active) upd32 += (uint32_t)((h0c >> 16) & 0x7F) + (mine ? 1u : 0u);
         }
+      };
+      if (per_req) {
+        for (int k = 0; k < nreq; ++k) request(k, BoolC<true>{});
+      } else {
+        for (int k = 0; k < nreq; ++k) request(k, BoolC<false>{});
       }
       continue;
     }
@@ -1924,32 +1935,12 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
         tq[__popc(todo & ((1u << lane) - 1u))] = q;
       }
       __syncwarp();
-      // sparse tiles (per-request epochs, rare): the staged relative arrivals
-      // may have wrapped, so each request's absolute arrival comes from its lane
-      const int src = per_req ? nth_set_bit(todo, lane) : 0;
-      for (int jj = 0; jj < nreq; ++jj) {
-        TileReq<T> q = tq[jj];
-        if constexpr (TT<T>::kRel) {
-          if (per_req) {
-            const int64_t a_abs = __shfl_sync(FULL, al, __shfl_sync(FULL, src, jj));
-            if (a_abs - E > P.theta) {
-              const int64_t gap = a_abs - E;
-              const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
-#pragma unroll
-              for (int k = 0; k < S; ++k) v[k] = v[k] > delta ? v[k] - delta : (T)0;
-              E = a_abs;
-            }
-            // the request's fields at the new epoch, from its model's tables
-            const T ar = (T)(a_abs - E);
-            const T tll = w.tail[q.m], sll = w.slo[q.m];
-            q.lim = 0;
-            if (sll >= tll) {
-              const T room = sll - tll;
-              q.lim = room > (T)(TT<T>::maxv() - 1 - ar) ? (T)(TT<T>::maxv() - 1) : (T)(ar + room);
-            }
-            q.ar = ar;
-          }
-        }
+      // one request: every hosting lane's tandem recurrence, the earliest last
+      // departure by a warp min, the lowest lane among the minima by a second
+      // one (C1; a ballot + find-first-set costs ~3x a warp min on the chain,
+      // and a coarse-key variant measured slower in isolation, scripts/micro),
+      // predicated commit (acceptance is warp-uniform; no host: mn = maxv > lim)
+      auto request = [&](const TileReq<T>& q) {
         T d[S];
         if constexpr (S == 1) {
           d[0] = q.d0;
@@ -1967,33 +1958,42 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
           y[k] = x;
         }
         const T key = ((q.hm >> lane) & 1u) ? x : TT<T>::maxv();
-        T mn;
-        unsigned win;
-        if constexpr (sizeof(T) == 4) {
-          // Two independent warp mins, issued together: the exact minimum and
-          // a coarse key (value with its low 5 bits replaced by the lane) whose
-          // minimum is the lowest lane in the minimum's 32-ns bucket.  That
-          // lane holds the minimum unless a lower lane of the bucket holds a
-          // larger value (then a third warp min finds the lowest lane among
-          // the minima: C1).  (A ballot + find-first-set costs ~3x a warp min
-          // on the chain, scripts/micro.)
-          mn = (T)__reduce_min_sync(FULL, (unsigned)key);
-          const unsigned cw = __reduce_min_sync(FULL, ((unsigned)key & ~31u) | (unsigned)lane);
-          win = cw & 31u;
-          if (__shfl_sync(FULL, (unsigned)key, win) != (unsigned)mn)
-            win = __reduce_min_sync(FULL, key == mn ? (unsigned)lane : 32u);
-        } else {
-          mn = warp_min<T>(key);
-          win = __reduce_min_sync(FULL, key == mn ? (unsigned)lane : 32u);
-        }
-        // accepted iff the earliest last departure meets the limit (warp-
-        // uniform; no host: mn = maxv > lim); predicated, no branch
+        const T mn = warp_min<T>(key);
+        const unsigned win = __reduce_min_sync(FULL, key == mn ? (unsigned)lane : 32u);
         const bool acc = mn <= q.lim;
         const bool take = acc && (unsigned)lane == win;
 #pragma unroll
         for (int k = 0; k < S; ++k) v[k] = take ? y[k] : v[k];
         good += acc ? 1 : 0;
         sum += acc ? (int64_t)(mn - q.ar) + (int64_t)q.tl : 0;
+      };
+      if (!per_req) {
+        for (int jj = 0; jj < nreq; ++jj) request(tq[jj]);
+      } else if constexpr (TT<T>::kRel) {
+        // sparse tiles (per-request epochs, rare): the staged relative
+        // arrivals may have wrapped, so each request's absolute arrival comes
+        // from its lane and its fields are recomputed at the moved epoch
+        const int src = nth_set_bit(todo, lane);
+        for (int jj = 0; jj < nreq; ++jj) {
+          TileReq<T> q = tq[jj];
+          const int64_t a_abs = __shfl_sync(FULL, al, __shfl_sync(FULL, src, jj));
+          if (a_abs - E > P.theta) {
+            const int64_t gap = a_abs - E;
+            const T delta = gap >= 0xFFFFFFFFll ? (T)0xFFFFFFFFu : (T)gap;
+#pragma unroll
+            for (int k = 0; k < S; ++k) v[k] = v[k] > delta ? v[k] - delta : (T)0;
+            E = a_abs;
+          }
+          const T ar = (T)(a_abs - E);
+          const T tll = w.tail[q.m], sll = w.slo[q.m];
+          q.lim = 0;
+          if (sll >= tll) {
+            const T room = sll - tll;
+            q.lim = room > (T)(TT<T>::maxv() - 1 - ar) ? (T)(TT<T>::maxv() - 1) : (T)(ar + room);
+          }
+          q.ar = ar;
+          request(q);
+        }
       }
       __syncwarp();
     }

@@ -810,7 +810,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       const int h0c_c = __shfl_sync(FULL, h0c_l, src);
       // the request loop comes in two copies: without the per-request epoch
       // branch (dense tiles, the rule) and with it (sparse tiles)
-      auto request = [&](int k, auto sparse) {
+      auto request = [&](int k, auto sparse, auto stats) {
         const int cm = __shfl_sync(FULL, mi_c, k);
         T car = __shfl_sync(FULL, ar_c, k);
         T lim = __shfl_sync(FULL, lim_c, k);
@@ -837,7 +837,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
         if (step_u<T, S>(w, w.st0, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v0, bo0)) {
           ++good0;
           sum0 += (int64_t)(T)(v0 + cc);
-          if (stats_on) {  // SPEC: pass-1 counts; DUAL: the true side of the correction
+          if constexpr (decltype(stats)::value) {  // SPEC: pass-1 counts; DUAL: the true side
             const int g0 = bo0 / (S * 32 * (int)sizeof(T));
             if constexpr (MODE == SPEC)
               stat_add(P.spec_pm, P.spec_busy, P, j, c, cm, g0, occupancy<T, S>(P, w, g0, cm, dv), 1);
@@ -852,7 +852,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
           if (step_u<T, S>(w, w.st1, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v1, bo1)) {
             ++good1;
             sum1 += (int64_t)(T)(v1 + cc);
-            if (stats_on) {  // minus the speculative side
+            if constexpr (decltype(stats)::value) {  // minus the speculative side
               const int g1 = bo1 / (S * 32 * (int)sizeof(T));
               stat_add(P.fix_pm, P.fix_busy, P, j, c, cm, g1, occupancy<T, S>(P, w, g1, cm, dv), -1);
             }
@@ -860,10 +860,13 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
           if (active) upd32 += (uint32_t)((h0c >> 16) & 0x7F) + (mine ? 1u : 0u);
         }
       };
-      if (per_req) {
-        for (int k = 0; k < nreq; ++k) request(k, BoolC<true>{});
+      // (and without the statistics rows of the fast heuristic unless asked)
+      if (stats_on) {
+        for (int k = 0; k < nreq; ++k) request(k, BoolC<true>{}, BoolC<true>{});
+      } else if (per_req) {
+        for (int k = 0; k < nreq; ++k) request(k, BoolC<true>{}, BoolC<false>{});
       } else {
-        for (int k = 0; k < nreq; ++k) request(k, BoolC<false>{});
+        for (int k = 0; k < nreq; ++k) request(k, BoolC<false>{}, BoolC<false>{});
       }
       continue;
     }

@@ -265,6 +265,7 @@ __device__ __forceinline__ void commit(const ChunkParams& P, const WarpMem<T>& w
 
 // One request on one trajectory: dispatch (earliest predicted finish, lowest
 // index on ties), admission at receipt, commit.  Returns latency or -1.
+// Used for mixed configs (S == 0); uniform configs run step_u.
 // S > 0 (uniform config): hinfo = byte offsets of the first two hosts
 // (off0 | off1 << 16), h0 = list start | host count << 16, further hosts'
 // offsets in w.hid; every host runs the same stage latencies dv, so for
@@ -474,7 +475,7 @@ __device__ __forceinline__ void load_dv_smem(const T* row, T* dv) {
 // come packed in hA / hB, further ones from the hosting list.  Returns whether
 // the request is accepted; v = the compared value (see uniform_fields), bo =
 // byte offset of the chosen group's first slot.
-template <typename T, int S>
+template <typename T, int S, bool BF = false>
 __device__ __forceinline__ bool step_u(const WarpMem<T>& w, T* st, int lane, int hA, int hB,
                                        int h0c, bool mine, int my_off, bool live, T ar,
                                        const T* dv, T lim, T& v, int& bo) {
@@ -499,21 +500,49 @@ __device__ __forceinline__ bool step_u(const WarpMem<T>& w, T* st, int lane, int
     b = lt ? off : b;
   };
   const int cnt = (h0c >> 16) & 0x7F;
-  if (cnt >= 1) {
-    host(hA & 0xFFFF);
-    if (cnt >= 2) host((int)((unsigned)hA >> 16));
-    if (cnt >= 3) {
-      host(hB & 0xFFFF);
-      if (cnt >= 4) host((int)((unsigned)hB >> 16));
+  if constexpr (BF && S <= 2) {
+    // (pass 2) short recurrences: the first four hosts and this lane's own
+    // replica without branches (a missing host reads slot 0 and is masked):
+    // pass 2 3.03 -> 2.45 s; pass 1 got slower with it (14.8 -> 15.5 s,
+    // profiles/r2p)
+    const int o0 = hA & 0xFFFF, o1 = (int)((unsigned)hA >> 16);
+    const int o2 = hB & 0xFFFF, o3 = (int)((unsigned)hB >> 16);
+    const T x0 = pred(o0), x1 = pred(o1), x2 = pred(o2), x3 = pred(o3);
+    const T xm = pred(my_off);
+    auto take = [&](bool ok, T x, int off) {
+      const bool lt = ok && x < best;  // strict: the lowest index wins ties (C1)
+      best = lt ? x : best;
+      b = lt ? off : b;
+    };
+    take(cnt >= 1, x0, o0);
+    take(cnt >= 2, x1, o1);
+    take(cnt >= 3, x2, o2);
+    take(cnt >= 4, x3, o3);
+    if (cnt > 4) {
       const int hs = h0c & 0xFFFF;
       for (int h = hs + 4; h < hs + cnt; ++h) host(w.hid[h]);
     }
-  }
-  if (mine) {  // this lane's added replica; ties resolved by group index
-    const T x = pred(my_off);
-    if (x < best || (x == best && my_off < b)) {
-      best = x;
-      b = my_off;
+    // this lane's added replica; ties resolved by group index
+    const bool tm = mine && (xm < best || (xm == best && my_off < b));
+    best = tm ? xm : best;
+    b = tm ? my_off : b;
+  } else {
+    if (cnt >= 1) {
+      host(hA & 0xFFFF);
+      if (cnt >= 2) host((int)((unsigned)hA >> 16));
+      if (cnt >= 3) {
+        host(hB & 0xFFFF);
+        if (cnt >= 4) host((int)((unsigned)hB >> 16));
+        const int hs = h0c & 0xFFFF;
+        for (int h = hs + 4; h < hs + cnt; ++h) host(w.hid[h]);
+      }
+    }
+    if (mine) {  // this lane's added replica; ties resolved by group index
+      const T x = pred(my_off);
+      if (x < best || (x == best && my_off < b)) {
+        best = x;
+        b = my_off;
+      }
     }
   }
   v = best;
@@ -834,7 +863,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
         const bool mine = live && cm == my_m;
         T v0;
         int bo0;
-        if (step_u<T, S>(w, w.st0, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v0, bo0)) {
+        if (step_u<T, S, MODE == DUAL>(w, w.st0, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v0, bo0)) {
           ++good0;
           sum0 += (int64_t)(T)(v0 + cc);
           if constexpr (decltype(stats)::value) {  // SPEC: pass-1 counts; DUAL: the true side
@@ -849,7 +878,7 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
         if constexpr (MODE == DUAL) {
           T v1;
           int bo1;
-          if (step_u<T, S>(w, w.st1, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v1, bo1)) {
+          if (step_u<T, S, MODE == DUAL>(w, w.st1, lane, hA, hB, h0c, mine, my_off, live, car, dv, lim, v1, bo1)) {
             ++good1;
             sum1 += (int64_t)(T)(v1 + cc);
             if constexpr (decltype(stats)::value) {  // minus the speculative side
@@ -871,6 +900,9 @@ __device__ __forceinline__ uint32_t run_unit(const ChunkParams& P, WarpMem<T>& w
       continue;
     }
 
+    // Mixed configs (S == 0; uniform configs took the loop above, so the
+    // S > 0 branches below are never executed -- they remain the round-1
+    // formulation that step_u replaced):
     // lane-parallel per-request fields, broadcast below by independent shuffles
     const T ar_l = (T)(ai - E);
     const int h0_l = w.hoff[mi];

@@ -89,9 +89,9 @@ template <typename T>
 struct alignas(16) TileReq {
   T ar;          // arrival, relative to the epoch
   T lim;         // accept iff the last departure <= lim (= ar + slo - tail, saturated)
-  T d0;          // first stage latency of the request's model (S == 1)
   T tl;          // tail
-  T d1;          // second stage latency (group-lane walker, S == 2)
+  T d[4];        // the first stage latencies of the request's model (S <= 4:
+                 // staged, so no table load depends on the record on the chain)
   uint32_t hm;   // compact hosting mask (0: no host in the component, or never acceptable)
   int32_t m;     // model
 };
@@ -465,6 +465,18 @@ __device__ __forceinline__ void load_dv_smem(const T* row, T* dv) {
   } else {
 #pragma unroll
     for (int k = 0; k < S; ++k) dv[k] = row[k];
+  }
+}
+
+// A walker's stage latencies of the staged request q: from the record for S
+// <= 4, else from the per-warp table.
+template <typename T, int S>
+__device__ __forceinline__ void tile_dv(const TileReq<T>& q, const T* dtab, T* d) {
+  if constexpr (S <= 4) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) d[k] = q.d[k];
+  } else {
+    load_dv_smem<T, S>(dtab + q.m * kSTab, d);
   }
 }
 
@@ -1580,9 +1592,9 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
             const T room = sll - tll;
             q.lim = room > (T)(TT<T>::maxv() - 1 - arl) ? (T)(TT<T>::maxv() - 1) : (T)(arl + room);
           }
-          q.d0 = w.d[ml * kSTab];
           q.tl = tll;
-          q.d1 = S == 2 ? w.d[ml * kSTab + 1] : (T)0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) q.d[k] = k < S ? w.d[ml * kSTab + k] : (T)0;
           q.m = ml;
           tq[__popc(todo & ((1u << lane) - 1u))] = q;
         }
@@ -1591,15 +1603,7 @@ __device__ __forceinline__ void scalar_candidate(const ChunkParams& P, const War
         for (int jj = 0; jj < nreq; ++jj) {
           const TileReq<T> q = tq[jj];
           T d[S];
-          if constexpr (S == 1) {
-            d[0] = q.d0;
-          } else if constexpr (S == 2) {  // staged: no dependent table load on the chain
-            d[0] = q.d0;
-            d[1] = q.d1;
-          } else {
-#pragma unroll
-            for (int k = 0; k < S; ++k) d[k] = w.d[q.m * kSTab + k];
-          }
+          tile_dv<T, S>(q, w.d, d);
           T y[R];
           T val[NG];
           uint32_t oh[NG];  // one-hot winner (an index would turn the commit into local memory)
@@ -1963,8 +1967,8 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
           const T room = sll - tll;
           q.lim = room > (T)(TT<T>::maxv() - 1 - arl) ? (T)(TT<T>::maxv() - 1) : (T)(arl + room);
         }
-        q.d0 = w.d[ml * kSTab];
-        q.d1 = S == 2 ? w.d[ml * kSTab + 1] : (T)0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q.d[k] = k < S ? w.d[ml * kSTab + k] : (T)0;
         q.tl = tll;
         q.m = ml;
         tq[__popc(todo & ((1u << lane) - 1u))] = q;
@@ -1977,14 +1981,7 @@ __device__ __forceinline__ void glane_candidate(const ChunkParams& P, const Warp
       // predicated commit (acceptance is warp-uniform; no host: mn = maxv > lim)
       auto request = [&](const TileReq<T>& q) {
         T d[S];
-        if constexpr (S == 1) {
-          d[0] = q.d0;
-        } else if constexpr (S == 2) {
-          d[0] = q.d0;
-          d[1] = q.d1;
-        } else {
-          load_dv_smem<T, S>(w.d + q.m * kSTab, d);
-        }
+        tile_dv<T, S>(q, w.d, d);
         T x = q.ar;
         T y[S];
 #pragma unroll

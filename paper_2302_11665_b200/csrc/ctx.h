@@ -132,7 +132,7 @@ struct asim_ctx {
   bool group_cands = true;   // search steps: items group candidates by component (ASIM_GROUP_CANDIDATES=0: off)
   bool scalar_walk = true;   // register-state walker for small components (ASIM_SCALAR_WALK=0: off)
   int32_t glane_walk = 2;    // ASIM_GLANE_WALK (0: off): see ChunkParams::glane_walk
-  int32_t glane_smax = 2;    // ASIM_GLANE_SMAX: see ChunkParams::glane_smax
+  int32_t glane_smax = 4;    // ASIM_GLANE_SMAX: see ChunkParams::glane_smax
 
   // scratch for evaluate()
   DBuf d_base_cfg, d_base_mask, d_cand_base, d_cand_model, d_cand_group, d_cand_ok, d_items;

@@ -9,8 +9,9 @@ struct alignas(16) Req { unsigned ar, lim, d0, tl, d1, hm; int m, pad; };
 
 template <int MODE>
 __global__ void loop(const Req* __restrict__ g, int iters, unsigned* out, long long* cyc) {
-  __shared__ Req tq[32];
-  const int lane = threadIdx.x;
+  __shared__ Req tqs[32][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Req* tq = tqs[wid];
   tq[lane] = g[lane];
   __syncwarp();
   unsigned v0 = lane * 7u, v1 = lane * 11u, good = 0, base = 0;
@@ -45,8 +46,8 @@ __global__ void loop(const Req* __restrict__ g, int iters, unsigned* out, long l
     base += 1000u;
   }
   const long long t1 = clock64();
-  out[lane] = v0 + v1 + good + (unsigned)sum;
-  if (lane == 0) cyc[MODE] = t1 - t0;
+  out[threadIdx.x] = v0 + v1 + good + (unsigned)sum;
+  if (threadIdx.x == 0) cyc[MODE] = t1 - t0;
 }
 
 int main() {
@@ -57,13 +58,18 @@ int main() {
   }
   Req* g; unsigned* out; long long* cyc;
   cudaMalloc(&g, sizeof(h)); cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
-  cudaMalloc(&out, 128); cudaMallocManaged(&cyc, 16);
+  cudaMalloc(&out, 32 * 32 * 4); cudaMallocManaged(&cyc, 16);
   const int iters = 2000;
-  loop<0><<<1, 32>>>(g, iters, out, cyc); loop<1><<<1, 32>>>(g, iters, out, cyc);
-  cudaDeviceSynchronize();
-  loop<0><<<1, 32>>>(g, iters, out, cyc); loop<1><<<1, 32>>>(g, iters, out, cyc);
-  cudaDeviceSynchronize();
-  printf("two warp mins in sequence: %.1f cycles/request\n", (double)cyc[0] / (iters * 32.0));
-  printf("exact + coarse warp mins:  %.1f cycles/request\n", (double)cyc[1] / (iters * 32.0));
+  // one walker warp alone, then 4 / 8 / 16 co-resident warps in one block
+  // (one SM): does the warp-min unit serialise co-resident walkers?
+  for (int nw : {1, 4, 8, 16}) {
+    for (int rep = 0; rep < 2; ++rep) {
+      loop<0><<<1, 32 * nw>>>(g, iters, out, cyc);
+      loop<1><<<1, 32 * nw>>>(g, iters, out, cyc);
+      cudaDeviceSynchronize();
+    }
+    printf("%2d warps/SM: two warp mins in sequence %.1f, exact + coarse %.1f cycles/request\n", nw,
+           (double)cyc[0] / (iters * 32.0), (double)cyc[1] / (iters * 32.0));
+  }
   return 0;
 }
